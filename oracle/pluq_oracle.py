@@ -451,19 +451,23 @@ def reconstruct(packed, psig, qsig, r, p):
 
 
 def _mulmod_exact(x: np.ndarray, y: np.ndarray, p: int) -> np.ndarray:
-    """Exact X Y mod p for int64 residues via 12-bit splitting of Y in float64."""
+    """Exact X Y mod p for int64 residues (p < 2^32) using float64 BLAS on 16-bit halves."""
     k = x.shape[1]
-    bits = int(p - 1).bit_length()
     if (p - 1) ** 2 * k < _F64_EXACT:
         return np.mod(x.astype(np.float64) @ y.astype(np.float64), p).astype(np.int64)
-    lo_bits = 12
-    ylo = (y & ((1 << lo_bits) - 1)).astype(np.float64)
-    yhi = (y >> lo_bits).astype(np.float64)
-    assert (p - 1) * (1 << max(lo_bits, bits - lo_bits)) * k < _F64_EXACT, "generator split not exact"
-    xf = x.astype(np.float64)
-    lo = np.mod(xf @ ylo, p).astype(np.int64)
-    hi = np.mod(xf @ yhi, p).astype(np.int64)
-    return np.mod(hi * (1 << lo_bits) + lo, p)
+    assert k < (1 << 21), "16-bit split exact only for K < 2^21"
+    x = np.asarray(x, dtype=np.int64)
+    y = np.asarray(y, dtype=np.int64)
+    x0, x1 = (x & 0xFFFF).astype(np.float64), (x >> 16).astype(np.float64)
+    y0, y1 = (y & 0xFFFF).astype(np.float64), (y >> 16).astype(np.float64)
+
+    def mm(u, v):
+        return np.mod(u @ v, p).astype(np.int64)
+
+    ll, lh, hl, hh = mm(x0, y0), mm(x0, y1), mm(x1, y0), mm(x1, y1)
+    s16, s32 = (1 << 16) % p, (1 << 32) % p
+    mid = np.mod(lh + hl, p) * s16 % p
+    return (ll + mid + hh * s32 % p) % p
 
 
 def gen_xy_rank(m, n, r, p, seed, permute=True):

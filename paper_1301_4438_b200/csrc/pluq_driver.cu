@@ -1,0 +1,783 @@
+// Host recursion driver + C ABI for the B200 PLUQ-mod-p path.
+//
+// The driver mirrors Algorithm 1 (/root/reference/pkg/src/pluq/recursive.py:186-256)
+// node for node on device-resident data:
+//   * nodes that fit in shared memory run whole inside one CTA (pluq_small.cuh);
+//   * base-case blocks too large for shared memory run the CTA base case on global
+//     memory (pluq_basecase.cuh);
+//   * larger nodes are split here: permutations, TRSM and the modular GEMM are
+//     launched on the context stream; the host reads back only the ranks and
+//     permutations of finished children (one sync per child) because the shapes of
+//     F, G, R depend on r1, r2, r3;
+//   * an all-zero block short-circuits to (I, I, 0) — bit-exact with the reference,
+//     which walks the zero tree and returns identity/0 with no charges.
+// OpCounts are charged in the reference's closed forms (kernels.py:1-16) on the host
+// for the kernel calls it issues and on the device for work done inside kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pluq_b200.h"
+#include "pluq_kernels.cuh"
+#include "pluq_tc_gemm.cuh"
+
+using namespace pluq;
+
+namespace {
+
+struct PluqError : std::runtime_error {
+  int code;
+  PluqError(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw PluqError(e_ == cudaErrorMemoryAllocation ? kNoMemory : kCuda,               \
+                      std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+using Perm = std::vector<int32_t>;
+
+Perm ident(int64_t s) {
+  Perm p(s);
+  for (int64_t i = 0; i < s; ++i) p[i] = (int32_t)i;
+  return p;
+}
+Perm inverse(const Perm& a) {
+  Perm out(a.size());
+  for (size_t i = 0; i < a.size(); ++i) out[a[i]] = (int32_t)i;
+  return out;
+}
+bool is_ident(const Perm& a) {
+  for (size_t i = 0; i < a.size(); ++i)
+    if (a[i] != (int32_t)i) return false;
+  return true;
+}
+
+}  // namespace
+
+struct pluq_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // pinned staging ring for small host->device uploads (reset after every sync)
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_off = 0;
+  // result staging of base-case / small-node kernels
+  int* d_res = nullptr;
+  size_t d_res_cap = 0;
+  int* h_res = nullptr;
+  size_t h_res_cap = 0;
+  unsigned long long* d_counts = nullptr;  // 4 device tallies
+  unsigned long long* h_counts = nullptr;
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;
+  // options
+  int64_t small_cap = 128 * 128;   // max m*n of a node factored whole by one CTA
+  int64_t small_threads = 256;
+  int64_t use_tc = 1;
+  int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
+  int64_t tc_min_k = 32;
+  // stats of the last factorization
+  int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
+          st_simt = 0, st_zero_skips = 0;
+  TcGemm tc;
+
+  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = 0; }
+
+  void sync() {
+    CU(cudaStreamSynchronize(stream));
+    ++st_sync;
+    pin_off = 0;
+  }
+  void* stage(const void* src, size_t bytes) {
+    size_t need = (bytes + 255) & ~size_t(255);
+    if (pin_off + need > pin_cap) {
+      sync();
+      if (need > pin_cap) {
+        if (pin) CU(cudaFreeHost(pin));
+        pin_cap = std::max(need, size_t(16) << 20);
+        CU(cudaHostAlloc((void**)&pin, pin_cap, cudaHostAllocDefault));
+      }
+    }
+    void* dst = pin + pin_off;
+    pin_off += need;
+    std::memcpy(dst, src, bytes);
+    return dst;
+  }
+  void ensure_res(size_t ints) {
+    if (ints > d_res_cap) {
+      sync();
+      if (d_res) CU(cudaFree(d_res));
+      if (h_res) CU(cudaFreeHost(h_res));
+      d_res_cap = h_res_cap = std::max(ints, size_t(1) << 16);
+      CU(cudaMalloc((void**)&d_res, d_res_cap * sizeof(int)));
+      CU(cudaHostAlloc((void**)&h_res, h_res_cap * sizeof(int), cudaHostAllocDefault));
+    }
+  }
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    CU(cudaMallocAsync(&p, count * sizeof(T), stream));
+    return reinterpret_cast<T*>(p);
+  }
+  void dfree(void* p) {
+    if (p) CU(cudaFreeAsync(p, stream));
+  }
+  void check_launch() {
+    ++st_launch;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw PluqError(kCuda, std::string("kernel launch: ") + cudaGetErrorString(e));
+  }
+};
+
+namespace {
+
+inline int grid_rows(int64_t rows) { return (int)std::max<int64_t>(1, std::min<int64_t>(rows, 65535)); }
+
+struct Ops {
+  pluq_ctx* c;
+  ModP mp;
+
+  // ---- modular GEMM: C <- C - A B  (kernels.py:38-55) ------------------------------
+  void gemm(const View& cv, const View& av, const View& bv) {
+    if (cv.m == 0 || cv.n == 0 || av.n == 0) return;
+    if (c->use_tc && cv.m >= c->tc_min_dim && cv.n >= c->tc_min_dim && av.n >= c->tc_min_k) {
+      int st = c->tc.run(cv, av, bv, mp, c->stream);
+      if (st == kOk) { ++c->st_tc; c->st_launch += 3; return; }
+      if (st != kUnsupported) throw PluqError(st, "tensor-core GEMM failed: " + c->tc.last_error);
+    }
+    dim3 grid((cv.n + SG_BN - 1) / SG_BN, (cv.m + SG_BM - 1) / SG_BM);
+    if (grid.y > 65535) {  // split very tall C into row chunks
+      for (int r0 = 0; r0 < cv.m; r0 += 65535 * SG_BM) {
+        int rr = std::min(cv.m - r0, 65535 * SG_BM);
+        gemm(cv.sub(r0, 0, rr, cv.n), av.sub(r0, 0, rr, av.n), bv);
+      }
+      return;
+    }
+    if (mp.kchunk < 2 * SG_BK)
+      simt_gemm_kernel<true><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp);
+    else
+      simt_gemm_kernel<false><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp);
+    ++c->st_simt;
+    c->check_launch();
+  }
+
+  static int split(int r) {
+    int h = r / 2;
+    if (r >= 256) h = std::max(64, (h / 64) * 64);
+    return h;
+  }
+
+  // ---- B <- L^-1 B (kernels.py:59-83) -------------------------------------------------
+  void trsm_l(const View& l, const View& b) {
+    const int r = l.m;
+    if (r == 0 || b.n == 0) return;
+    if (r <= TR_BASE) {
+      trsm_llu_base_kernel<<<(b.n + 127) / 128, 128, 0, c->stream>>>(l, b, mp);
+      c->check_launch();
+      return;
+    }
+    int h = split(r);
+    trsm_l(l.sub(0, 0, h, h), b.sub(0, 0, h, b.n));
+    gemm(b.sub(h, 0, r - h, b.n), l.sub(h, 0, r - h, h), b.sub(0, 0, h, b.n));
+    trsm_l(l.sub(h, h, r - h, r - h), b.sub(h, 0, r - h, b.n));
+  }
+
+  // ---- B <- B U^-1 (kernels.py:85-120) ------------------------------------------------
+  void trsm_u(const View& b, const View& u) {
+    const int r = u.m;
+    if (r == 0 || b.m == 0) return;
+    if (r <= TR_BASE) {
+      trsm_ru_base_kernel<<<(b.m + 63) / 64, 64, 0, c->stream>>>(b, u, mp);
+      c->check_launch();
+      return;
+    }
+    int h = split(r);
+    trsm_u(b.sub(0, 0, b.m, h), u.sub(0, 0, h, h));
+    gemm(b.sub(0, h, b.m, r - h), b.sub(0, 0, b.m, h), u.sub(0, h, h, r - h));
+    trsm_u(b.sub(0, h, b.m, r - h), u.sub(h, h, r - h, r - h));
+  }
+
+  // ---- gathers restricted to the moved set (matrix.py:249-283) ----------------------
+  void gather_rows(const View& x, const Perm& g) {
+    if (x.m == 0 || x.n == 0) return;
+    std::vector<int32_t> src, dst;
+    for (int i = 0; i < x.m; ++i)
+      if (g[i] != i) { dst.push_back(i); src.push_back(g[i]); }
+    if (dst.empty()) return;
+    const int nmv = (int)dst.size();
+    int* d_idx = c->dalloc<int>(2 * (size_t)nmv);
+    std::vector<int32_t> both(src);
+    both.insert(both.end(), dst.begin(), dst.end());
+    void* h = c->stage(both.data(), both.size() * 4);
+    CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    uint32_t* tmp = c->dalloc<uint32_t>((size_t)nmv * x.n);
+    dim3 grid((x.n + 255) / 256, grid_rows(nmv));
+    rows_to_tmp_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx, nmv, tmp);
+    c->check_launch();
+    tmp_to_rows_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx + nmv, nmv, tmp);
+    c->check_launch();
+    c->dfree(tmp);
+    c->dfree(d_idx);
+  }
+  void gather_cols(const View& x, const Perm& g) {
+    if (x.m == 0 || x.n == 0) return;
+    std::vector<int32_t> src, dst;
+    for (int j = 0; j < x.n; ++j)
+      if (g[j] != j) { dst.push_back(j); src.push_back(g[j]); }
+    if (dst.empty()) return;
+    const int nmv = (int)dst.size();
+    int* d_idx = c->dalloc<int>(2 * (size_t)nmv);
+    std::vector<int32_t> both(src);
+    both.insert(both.end(), dst.begin(), dst.end());
+    void* h = c->stage(both.data(), both.size() * 4);
+    CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    uint32_t* tmp = c->dalloc<uint32_t>((size_t)nmv * x.m);
+    dim3 grid((nmv + 255) / 256, grid_rows(x.m));
+    cols_to_tmp_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx, nmv, tmp);
+    c->check_launch();
+    tmp_to_cols_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx + nmv, nmv, tmp);
+    c->check_launch();
+    c->dfree(tmp);
+    c->dfree(d_idx);
+  }
+
+  bool nonzero(const View& x) {
+    CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    dim3 grid((unsigned)std::min<int64_t>(4, (x.n + 255) / 256), grid_rows(std::min<int64_t>(x.m, 4096)));
+    nonzero_kernel<<<grid, 256, 0, c->stream>>>(x, c->d_flag);
+    c->check_launch();
+    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return *c->h_flag != 0;
+  }
+
+  void copy(const View& dst, const View& src) {
+    if (dst.m == 0 || dst.n == 0) return;
+    dim3 grid((dst.n + 255) / 256, grid_rows(dst.m));
+    copy_view_kernel<<<grid, 256, 0, c->stream>>>(dst, src);
+    c->check_launch();
+  }
+};
+
+struct NodeRes {
+  Perm P, Q;
+  int r;
+};
+
+struct Driver {
+  pluq_ctx* c;
+  ModP mp;
+  int threshold;
+  Counts host_counts{0, 0, 0, 0};
+  Ops ops;
+
+  Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ModP::make(p)), threshold(thr), ops{ctx, ModP::make(p)} {}
+
+  bool fits_small(int64_t m, int64_t n) const {
+    return m * n <= c->small_cap && small_smem_bytes(m, n) <= 227 * 1024;
+  }
+
+  NodeRes readback(int m, int n) {
+    CU(cudaMemcpyAsync(c->h_res, c->d_res, (size_t)(m + n + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    NodeRes res;
+    res.P.assign(c->h_res, c->h_res + m);
+    res.Q.assign(c->h_res + m, c->h_res + m + n);
+    res.r = c->h_res[m + n];
+    return res;
+  }
+
+  NodeRes leaf_small(const View& x) {
+    c->ensure_res((size_t)x.m + x.n + 1);
+    SmallArgs a;
+    a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
+    a.p_out = c->d_res; a.q_out = c->d_res + x.m; a.r_out = c->d_res + x.m + x.n;
+    a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
+    size_t smem = small_smem_bytes(x.m, x.n);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
+    c->check_launch();
+    ++c->st_small;
+    return readback(x.m, x.n);
+  }
+
+  NodeRes leaf_global(const View& x) {
+    const int m = x.m, n = x.n, mn = std::min(m, n);
+    c->ensure_res((size_t)m + n + 1);
+    size_t words = (size_t)(m + n + 3) / 4 + 2 * (size_t)mn + m + n + 8;
+    int* scratch = c->dalloc<int>(words);
+    uint32_t* tmp = c->dalloc<uint32_t>((size_t)m * n);
+    BaseArgs a;
+    a.x = x; a.mp = mp;
+    a.s.prow = reinterpret_cast<uint8_t*>(scratch);
+    a.s.pcol = a.s.prow + m;
+    int* p = scratch + (m + n + 3) / 4 + 1;
+    a.s.rord = p; p += mn;
+    a.s.cord = p; p += mn;
+    a.s.rowat = p; p += m;
+    a.s.colat = p;
+    a.tmp = tmp; a.res = c->d_res; a.cnt_out = c->d_counts;
+    basecase_global_kernel<<<1, 1024, 0, c->stream>>>(a);
+    c->check_launch();
+    ++c->st_base;
+    c->dfree(tmp);
+    c->dfree(scratch);
+    return readback(m, n);
+  }
+
+  NodeRes rec(const View& x) {
+    const int m = x.m, n = x.n;
+    ++c->st_nodes;
+    if (m == 0 || n == 0) return NodeRes{ident(m), ident(n), 0};
+    const bool base = m == 1 || n == 1 || std::min(m, n) <= threshold;
+    if (fits_small(m, n)) return leaf_small(x);
+    if (base) return leaf_global(x);
+    if (!ops.nonzero(x)) {
+      ++c->st_zero_skips;
+      return NodeRes{ident(m), ident(n), 0};
+    }
+    const int kr = m / 2, kc = n / 2;
+    NodeRes A1 = rec(x.sub(0, 0, kr, kc));
+    const int r1 = A1.r;
+    ops.gather_rows(x.sub(0, kc, kr, n - kc), inverse(A1.P));
+    ops.gather_cols(x.sub(kr, 0, m - kr, kc), A1.Q);
+    ops.trsm_l(x.sub(0, 0, r1, r1), x.sub(0, kc, r1, n - kc));            // D
+    ops.trsm_u(x.sub(kr, 0, m - kr, r1), x.sub(0, 0, r1, r1));            // E
+    ops.gemm(x.sub(r1, kc, kr - r1, n - kc), x.sub(r1, 0, kr - r1, r1), x.sub(0, kc, r1, n - kc));  // F
+    ops.gemm(x.sub(kr, r1, m - kr, n - r1), x.sub(kr, 0, m - kr, r1), x.sub(0, r1, r1, n - r1));    // G|H
+    charge_trsm_l(host_counts, r1, n - kc);
+    charge_trsm_u(host_counts, m - kr, r1);
+    charge_mm(host_counts, kr - r1, n - kc, r1);
+    charge_mm(host_counts, m - kr, kc - r1, r1);
+    charge_mm(host_counts, m - kr, n - kc, r1);
+
+    NodeRes F = rec(x.sub(r1, kc, kr - r1, n - kc));
+    const int r2 = F.r;
+    NodeRes G = rec(x.sub(kr, r1, m - kr, kc - r1));
+    const int r3 = G.r;
+    {
+      Perm ip3 = inverse(G.P), ip2 = inverse(F.P);
+      ops.gather_rows(x.sub(kr, kc, m - kr, n - kc), ip3);
+      ops.gather_cols(x.sub(kr, kc, m - kr, n - kc), F.Q);
+      ops.gather_rows(x.sub(kr, 0, m - kr, r1), ip3);
+      ops.gather_rows(x.sub(r1, 0, kr - r1, r1), ip2);
+      ops.gather_cols(x.sub(0, kc, r1, n - kc), F.Q);
+      ops.gather_cols(x.sub(0, r1, r1, kc - r1), G.Q);
+    }
+    const View u2 = x.sub(r1, kc, r2, r2);
+    const View l3 = x.sub(kr, r1, r3, r3);
+    const int m4 = m - kr - r3, n4 = n - kc - r2;
+    ops.trsm_u(x.sub(kr, kc, r3, r2), u2);                                  // I
+    if (r3 > 0 && r2 > 0) {
+      uint32_t* jbuf = c->dalloc<uint32_t>((size_t)r3 * r2);
+      View J{jbuf, r2, r3, r2};
+      ops.copy(J, x.sub(kr, kc, r3, r2));
+      ops.trsm_l(l3, J);                                                    // J (scratch)
+      ops.trsm_u(x.sub(kr + r3, kc, m4, r2), u2);                           // K
+      ops.trsm_l(l3, x.sub(kr, kc + r2, r3, n4));                           // N
+      ops.gemm(x.sub(kr, kc + r2, r3, n4), J, x.sub(r1, kc + r2, r2, n4));  // O
+      c->dfree(jbuf);
+    } else {
+      ops.trsm_u(x.sub(kr + r3, kc, m4, r2), u2);
+      ops.trsm_l(l3, x.sub(kr, kc + r2, r3, n4));
+    }
+    ops.gemm(x.sub(kr + r3, kc + r2, m4, n4), x.sub(kr + r3, kc, m4, r2), x.sub(r1, kc + r2, r2, n4));
+    ops.gemm(x.sub(kr + r3, kc + r2, m4, n4), x.sub(kr + r3, r1, m4, r3), x.sub(kr, kc + r2, r3, n4));
+    charge_trsm_u(host_counts, r3, r2);
+    charge_trsm_l(host_counts, r3, r2);
+    charge_trsm_u(host_counts, m4, r2);
+    charge_trsm_l(host_counts, r3, n4);
+    charge_mm(host_counts, r3, n4, r2);
+    charge_mm(host_counts, m4, n4, r2);
+    charge_mm(host_counts, m4, n4, r3);
+
+    NodeRes R = rec(x.sub(kr + r3, kc + r2, m4, n4));
+    const int r4 = R.r;
+    ops.gather_rows(x.sub(kr + r3, 0, m4, kc + r2), inverse(R.P));
+    ops.gather_cols(x.sub(0, kc + r2, kr + r3, n4), R.Q);
+
+    Perm S(m), T(n);
+    for (int t = 0; t < m; ++t) S[t] = s_sigma_h(t, r1, r2, r3, r4, kr);
+    for (int t = 0; t < n; ++t) T[t] = t_sigma_h(t, r1, r2, r3, r4, kc);
+    if (!is_ident(S)) ops.gather_rows(x, inverse(S));
+    if (!is_ident(T)) ops.gather_cols(x, T);
+
+    NodeRes out;
+    out.P.resize(m);
+    out.Q.resize(n);
+    for (int t = 0; t < m; ++t) {
+      int y;
+      if (t < kr) { int z = A1.P[t]; y = z < r1 ? z : r1 + F.P[z - r1]; }
+      else { int z = G.P[t - kr]; y = kr + (z < r3 ? z : r3 + R.P[z - r3]); }
+      out.P[t] = S[y];
+    }
+    for (int t = 0; t < n; ++t) {
+      int z = T[t], y;
+      if (z < kc) { int w = z < r1 ? z : r1 + G.Q[z - r1]; y = A1.Q[w]; }
+      else { int zz = z - kc; int w = zz < r2 ? zz : r2 + R.Q[zz - r2]; y = kc + F.Q[w]; }
+      out.Q[t] = y;
+    }
+    out.r = r1 + r2 + r3 + r4;
+    return out;
+  }
+
+  static int s_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
+    int a = r1 + r2, cc = r3 + r4, b = k - a;
+    if (x >= a && x < k) return x + cc;
+    if (x >= k && x < k + cc) return x - b;
+    return x;
+  }
+  static int t_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
+    if (x < r1) return x;
+    if (x < r1 + r2) return x + (k - r1);
+    if (x < r1 + r2 + r3) return x - r2;
+    if (x < r1 + r2 + r3 + r4) return x + (k + r2 - (r1 + r2 + r3));
+    if (x < k + r2 + r4) return x - (r2 + r4);
+    return x;
+  }
+};
+
+int validate(int64_t m, int64_t n, int64_t p) {
+  if (m < 0 || n < 0 || m > INT32_MAX / 2 || n > INT32_MAX / 2) return kInvalid;
+  if (p < 2 || p >= (int64_t(1) << 31)) return kInvalid;
+  return kOk;
+}
+
+template <class F>
+int guarded(pluq_ctx* ctx, F&& f) {
+  if (!ctx) return kInvalid;
+  try {
+    CU(cudaSetDevice(ctx->device));
+    f();
+    return kOk;
+  } catch (const PluqError& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    ctx->err = "host out of memory";
+    return kNoMemory;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return kCuda;
+  }
+}
+
+void finish_counts(pluq_ctx* c, const Counts& hc, int64_t* counts) {
+  CU(cudaMemcpyAsync(c->h_counts, c->d_counts, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (counts) {
+    counts[0] += (int64_t)(hc.mul + c->h_counts[0]);
+    counts[1] += (int64_t)(hc.add + c->h_counts[1]);
+    counts[2] += (int64_t)(hc.inv + c->h_counts[2]);
+    counts[3] += (int64_t)(hc.red + c->h_counts[3]);
+  }
+}
+
+void factor_device(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p,
+                   int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts,
+                   bool iterative) {
+  c->reset_stats();
+  CU(cudaMemsetAsync(c->d_counts, 0, 4 * sizeof(unsigned long long), c->stream));
+  Driver d(c, (uint32_t)p, (int)std::min<int64_t>(threshold, INT32_MAX));
+  View x{dA, ld, (int)m, (int)n};
+  NodeRes res;
+  if (iterative) {
+    d.threshold = INT32_MAX;  // Algorithm 2 on the whole matrix
+    if (m == 0 || n == 0) res = NodeRes{ident(m), ident(n), 0};
+    else if (d.fits_small(m, n)) res = d.leaf_small(x);
+    else res = d.leaf_global(x);
+  } else {
+    res = d.rec(x);
+  }
+  finish_counts(c, d.host_counts, counts);
+  for (int64_t i = 0; i < m; ++i) psig[i] = res.P[i];
+  for (int64_t j = 0; j < n; ++j) qsig[j] = res.Q[j];
+  *rank = res.r;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+int pluq_create(pluq_ctx** out, int device, void* stream) {
+  if (!out) return kInvalid;
+  pluq_ctx* c = new pluq_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  int st = guarded(c, [&] {
+    CU(cudaMalloc((void**)&c->d_counts, 4 * sizeof(unsigned long long)));
+    CU(cudaHostAlloc((void**)&c->h_counts, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
+    CU(cudaMalloc((void**)&c->d_flag, sizeof(int)));
+    CU(cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault));
+    cudaMemPool_t pool;
+    CU(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;
+    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->ensure_res(1 << 16);
+    // rec_smem recurses on the device: give each thread room for the deepest
+    // small-node recursion (threshold 1 on a 128x128 node is ~8 frames).
+    size_t stack = 0;
+    CU(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+    if (stack < 8192) CU(cudaDeviceSetLimit(cudaLimitStackSize, 8192));
+  });
+  if (st != kOk) {
+    *out = nullptr;
+    delete c;
+    return st;
+  }
+  *out = c;
+  return kOk;
+}
+
+int pluq_destroy(pluq_ctx* c) {
+  if (!c) return kOk;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->tc.release();
+  if (c->pin) cudaFreeHost(c->pin);
+  if (c->d_res) cudaFree(c->d_res);
+  if (c->h_res) cudaFreeHost(c->h_res);
+  if (c->d_counts) cudaFree(c->d_counts);
+  if (c->h_counts) cudaFreeHost(c->h_counts);
+  if (c->d_flag) cudaFree(c->d_flag);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  delete c;
+  return kOk;
+}
+
+int pluq_set_stream(pluq_ctx* c, void* stream) {
+  if (!c) return kInvalid;
+  c->stream = (cudaStream_t)stream;
+  return kOk;
+}
+
+int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return kInvalid;
+  std::string k(key);
+  if (k == "small_cap") c->small_cap = value;
+  else if (k == "small_threads") c->small_threads = value;
+  else if (k == "use_tc") c->use_tc = value;
+  else if (k == "tc_min_dim") c->tc_min_dim = value;
+  else if (k == "tc_min_k") c->tc_min_k = value;
+  else if (k == "tc_k_pass") c->tc.k_pass_override = value;
+  else return kInvalid;
+  return kOk;
+}
+
+const char* pluq_last_error(pluq_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
+  if (!c || !out) return kInvalid;
+  int64_t v[8] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt, c->st_zero_skips};
+  for (int64_t i = 0; i < nout && i < 8; ++i) out[i] = v[i];
+  return kOk;
+}
+
+int pluq_factor(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p,
+                int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
+  if (threshold < 1) return kInvalid;
+  if (int v = validate(m, n, p)) return v;
+  if (ld < n || !rank || (m && !psig) || (n && !qsig)) return kInvalid;
+  return guarded(c, [&] { factor_device(c, dA, ld, m, n, p, threshold, psig, qsig, rank, counts, false); });
+}
+
+int pluq_factor_iterative(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p,
+                          int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
+  if (int v = validate(m, n, p)) return v;
+  if (ld < n || !rank || (m && !psig) || (n && !qsig)) return kInvalid;
+  return guarded(c, [&] { factor_device(c, dA, ld, m, n, p, 1, psig, qsig, rank, counts, true); });
+}
+
+int64_t pluq_batched_max_elems(pluq_ctx*, int64_t m, int64_t n) {
+  return small_smem_bytes(m, n) <= 227 * 1024 ? m * n : 0;
+}
+
+int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch, int64_t m, int64_t n,
+                        int64_t p, int64_t threshold, int32_t* d_p, int32_t* d_q, int32_t* d_rank,
+                        uint64_t* d_counts) {
+  if (threshold < 1 || batch < 0) return kInvalid;
+  if (int v = validate(m, n, p)) return v;
+  if (small_smem_bytes(m, n) > 227 * 1024) return kUnsupported;
+  if (batch == 0) return kOk;
+  return guarded(c, [&] {
+    SmallArgs a;
+    a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;
+    a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
+    a.mp = ModP::make((uint32_t)p);
+    a.p_out = d_p; a.q_out = d_q; a.r_out = d_rank;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counts);
+    if (!cnt) cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
+    a.cnt_out = cnt; a.cnt_accumulate = 0;
+    size_t smem = small_smem_bytes(m, n);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int64_t b0 = 0; b0 < batch; b0 += 2147483647ll) {
+      small_pluq_kernel<<<(unsigned)std::min<int64_t>(batch - b0, 2147483647ll), (unsigned)c->small_threads, smem, c->stream>>>(a);
+      c->check_launch();
+    }
+    if (!d_counts) c->dfree(cnt);
+  });
+}
+
+static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n, int64_t p, int64_t threshold,
+                       int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
+  if (threshold < 1) return kInvalid;
+  if (int v = validate(m, n, p)) return v;
+  if (!rank || (m && !psig) || (n && !qsig)) return kInvalid;
+  return guarded(c, [&] {
+    const int64_t cnt = m * n;
+    void* raw = c->dalloc<char>((size_t)cnt * 8);
+    uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+    if (cnt) CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
+    if (cnt) {
+      if (is_f64) from_f64_kernel<<<grid, 256, 0, c->stream>>>((const double*)raw, dA, cnt);
+      else from_i64_kernel<<<grid, 256, 0, c->stream>>>((const int64_t*)raw, dA, cnt);
+      c->check_launch();
+    }
+    factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
+    if (cnt) {
+      if (is_f64) to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA, (double*)raw, cnt);
+      else to_i64_kernel<<<grid, 256, 0, c->stream>>>(dA, (int64_t*)raw, cnt);
+      c->check_launch();
+      CU(cudaMemcpyAsync(hA, raw, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    c->dfree(dA);
+    c->dfree(raw);
+    c->sync();
+  });
+}
+
+int pluq_factor_host_f64(pluq_ctx* c, double* hA, int64_t m, int64_t n, int64_t p, int64_t threshold,
+                         int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
+  return factor_host(c, hA, true, m, n, p, threshold, psig, qsig, rank, counts);
+}
+
+int pluq_factor_host_i64(pluq_ctx* c, int64_t* hA, int64_t m, int64_t n, int64_t p, int64_t threshold,
+                         int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
+  return factor_host(c, hA, false, m, n, p, threshold, psig, qsig, rank, counts);
+}
+
+int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t m, int64_t n, int64_t p,
+                                 int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* ranks) {
+  if (threshold < 1 || batch < 0) return kInvalid;
+  if (int v = validate(m, n, p)) return v;
+  if (small_smem_bytes(m, n) > 227 * 1024) return kUnsupported;
+  return guarded(c, [&] {
+    const int64_t cnt = batch * m * n;
+    if (cnt == 0) return;
+    double* raw = c->dalloc<double>((size_t)cnt);
+    uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+    int32_t* dp = c->dalloc<int32_t>((size_t)(batch * (m + n + 1)));
+    CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
+    from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw, dA, cnt);
+    c->check_launch();
+    int st = pluq_factor_batched(c, dA, m * n, batch, m, n, p, threshold, dp, dp + batch * m,
+                                 dp + batch * (m + n), nullptr);
+    if (st != kOk) throw PluqError(st, c->err);
+    to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA, raw, cnt);
+    c->check_launch();
+    CU(cudaMemcpyAsync(hA, raw, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int32_t> host((size_t)(batch * (m + n + 1)));
+    CU(cudaMemcpyAsync(host.data(), dp, host.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    c->dfree(dp);
+    c->dfree(dA);
+    c->dfree(raw);
+    c->sync();
+    for (int64_t i = 0; i < batch * m; ++i) psig[i] = host[i];
+    for (int64_t i = 0; i < batch * n; ++i) qsig[i] = host[batch * m + i];
+    for (int64_t i = 0; i < batch; ++i) ranks[i] = host[batch * (m + n) + i];
+  });
+}
+
+int pluq_modgemm_sub(pluq_ctx* c, uint32_t* dC, int64_t ldc, const uint32_t* dA, int64_t lda,
+                     const uint32_t* dB, int64_t ldb, int64_t m, int64_t n, int64_t k, int64_t p) {
+  if (int v = validate(m, n, p)) return v;
+  if (k < 0 || k > INT32_MAX / 2) return kInvalid;
+  return guarded(c, [&] {
+    Ops ops{c, ModP::make((uint32_t)p)};
+    ops.gemm(View{dC, ldc, (int)m, (int)n}, View{const_cast<uint32_t*>(dA), lda, (int)m, (int)k},
+             View{const_cast<uint32_t*>(dB), ldb, (int)k, (int)n});
+  });
+}
+
+int pluq_modgemm_sub_tc(pluq_ctx* c, uint32_t* dC, int64_t ldc, const uint32_t* dA, int64_t lda,
+                        const uint32_t* dB, int64_t ldb, int64_t m, int64_t n, int64_t k, int64_t p) {
+  if (int v = validate(m, n, p)) return v;
+  if (k < 0 || k > INT32_MAX / 2) return kInvalid;
+  if (!c) return kInvalid;
+  int st = kOk;
+  int g = guarded(c, [&] {
+    st = c->tc.run(View{dC, ldc, (int)m, (int)n}, View{const_cast<uint32_t*>(dA), lda, (int)m, (int)k},
+                   View{const_cast<uint32_t*>(dB), ldb, (int)k, (int)n}, ModP::make((uint32_t)p), c->stream);
+    if (st != kOk && st != kUnsupported) throw PluqError(st, c->tc.last_error);
+  });
+  return g != kOk ? g : st;
+}
+
+int pluq_trsm_llu(pluq_ctx* c, const uint32_t* dL, int64_t ldl, uint32_t* dB, int64_t ldb, int64_t r,
+                  int64_t n, int64_t p) {
+  if (int v = validate(r, n, p)) return v;
+  return guarded(c, [&] {
+    Ops ops{c, ModP::make((uint32_t)p)};
+    ops.trsm_l(View{const_cast<uint32_t*>(dL), ldl, (int)r, (int)r}, View{dB, ldb, (int)r, (int)n});
+  });
+}
+
+int pluq_trsm_ru(pluq_ctx* c, uint32_t* dB, int64_t ldb, const uint32_t* dU, int64_t ldu, int64_t m,
+                 int64_t r, int64_t p) {
+  if (int v = validate(m, r, p)) return v;
+  int zero = 0;
+  int g = guarded(c, [&] {
+    View u{const_cast<uint32_t*>(dU), ldu, (int)r, (int)r};
+    if (r > 0) {
+      CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+      diag_zero_kernel<<<(unsigned)((r + 255) / 256), 256, 0, c->stream>>>(u, c->d_flag);
+      c->check_launch();
+      CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      if (*c->h_flag) { zero = 1; return; }
+    }
+    Ops ops{c, ModP::make((uint32_t)p)};
+    ops.trsm_u(View{dB, ldb, (int)m, (int)r}, u);
+  });
+  if (g != kOk) return g;
+  if (zero) { c->err = "upper triangular factor has a zero diagonal entry"; return kZeroDivision; }
+  return kOk;
+}
+
+int pluq_permute_rows(pluq_ctx* c, uint32_t* dX, int64_t ld, int64_t rows, int64_t cols, const int64_t* g) {
+  if (rows < 0 || cols < 0 || (rows && !g)) return kInvalid;
+  return guarded(c, [&] {
+    Perm gg(rows);
+    for (int64_t i = 0; i < rows; ++i) gg[i] = (int32_t)g[i];
+    Ops ops{c, ModP::make(2)};
+    ops.gather_rows(View{dX, ld, (int)rows, (int)cols}, gg);
+  });
+}
+
+int pluq_permute_cols(pluq_ctx* c, uint32_t* dX, int64_t ld, int64_t rows, int64_t cols, const int64_t* g) {
+  if (rows < 0 || cols < 0 || (cols && !g)) return kInvalid;
+  return guarded(c, [&] {
+    Perm gg(cols);
+    for (int64_t j = 0; j < cols; ++j) gg[j] = (int32_t)g[j];
+    Ops ops{c, ModP::make(2)};
+    ops.gather_cols(View{dX, ld, (int)rows, (int)cols}, gg);
+  });
+}
+
+}  // extern "C"

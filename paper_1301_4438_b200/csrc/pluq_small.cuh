@@ -1,0 +1,319 @@
+// Whole-node PLUQ inside one CTA, with the block resident in shared memory.
+//
+// This is Algorithm 1 (/root/reference/pkg/src/pluq/recursive.py:186-256) run
+// cooperatively by one CTA: same split (m//2, n//2), same terminal tests, same
+// 12 block permutations / 6 TRSM / 6 MM calls, same S/T block permutations and
+// P/Q composition.  It serves (a) the batched API (one CTA per independent
+// matrix, BASELINE cfg2) and (b) every node of the large-matrix recursion that
+// fits in shared memory, so the host driver never walks the small nodes.
+//
+// Shared-memory layout: the block with an odd row pitch (bank-conflict free
+// column walks) followed by a bump "stack" of int32 words.  Every thread runs
+// the same control flow and derives identical stack offsets, so allocation
+// needs no synchronisation.
+#pragma once
+#include "pluq_basecase.cuh"
+
+namespace pluq {
+
+struct SmallCtx {
+  ModP mp;
+  int threshold;
+  Counts* cnt;      // shared, touched by thread 0 only
+  BcShared* sh;
+};
+
+__device__ __forceinline__ void cta_ident(int* a, int n) {
+  for (int t = threadIdx.x; t < n; t += blockDim.x) a[t] = t;
+}
+
+__device__ __forceinline__ bool cta_is_ident(const int* g, int n) {
+  bool ok = true;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) ok &= (g[t] == t);
+  return __syncthreads_and(ok);
+}
+
+__device__ __forceinline__ void cta_inverse(const int* g, int* out, int n) {
+  for (int t = threadIdx.x; t < n; t += blockDim.x) out[g[t]] = t;
+  __syncthreads();
+}
+
+// Cycle decomposition of gather vector g (new[x] = old[g[x]]), built by thread 0.
+// seq lists each cycle as s, g[s], g[g[s]], ...; lens[c] its length. Returns #cycles.
+__device__ __forceinline__ int cta_cycles(const int* g, int n, int* seq, int* lens, int* mark, BcShared* sh) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n; ++s) mark[s] = 0;
+    int pos = 0, nc = 0;
+    for (int s = 0; s < n; ++s) {
+      if (mark[s] || g[s] == s) continue;
+      int cur = s, len = 0;
+      do { seq[pos++] = cur; mark[cur] = 1; cur = g[cur]; ++len; } while (cur != s);
+      lens[nc++] = len;
+    }
+    sh->minv = nc;
+  }
+  __syncthreads();
+  int nc = sh->minv;
+  __syncthreads();
+  return nc;
+}
+
+// In-place row gather of view v: new row x = old row g[x] (matrix.py:249-276 semantics).
+__device__ void cta_gather_rows(const View& v, const int* g, int* scratch, BcShared* sh) {
+  if (v.m == 0 || v.n == 0 || cta_is_ident(g, v.m)) return;
+  int* seq = scratch; int* lens = seq + v.m; int* mark = lens + v.m;
+  int nc = cta_cycles(g, v.m, seq, lens, mark, sh);
+  for (int c = threadIdx.x; c < v.n; c += blockDim.x) {
+    int pos = 0;
+    for (int cy = 0; cy < nc; ++cy) {
+      int len = lens[cy];
+      uint32_t tmp = v.at(seq[pos], c);
+      for (int q = 0; q + 1 < len; ++q) v.at(seq[pos + q], c) = v.at(seq[pos + q + 1], c);
+      v.at(seq[pos + len - 1], c) = tmp;
+      pos += len;
+    }
+  }
+  __syncthreads();
+}
+
+// In-place column gather: new column x = old column g[x].
+__device__ void cta_gather_cols(const View& v, const int* g, int* scratch, BcShared* sh) {
+  if (v.m == 0 || v.n == 0 || cta_is_ident(g, v.n)) return;
+  int* seq = scratch; int* lens = seq + v.n; int* mark = lens + v.n;
+  int nc = cta_cycles(g, v.n, seq, lens, mark, sh);
+  for (int rr = threadIdx.x; rr < v.m; rr += blockDim.x) {
+    uint32_t* row = v.row(rr);
+    int pos = 0;
+    for (int cy = 0; cy < nc; ++cy) {
+      int len = lens[cy];
+      uint32_t tmp = row[seq[pos]];
+      for (int q = 0; q + 1 < len; ++q) row[seq[pos + q]] = row[seq[pos + q + 1]];
+      row[seq[pos + len - 1]] = tmp;
+      pos += len;
+    }
+  }
+  __syncthreads();
+}
+
+// C <- C - A B mod p (kernels.py:38-55), outputs spread over the CTA.
+__device__ void cta_mm_sub(const View& c, const View& a, const View& b, const ModP& mp) {
+  const int m = c.m, n = c.n, k = a.n;
+  if (m == 0 || n == 0 || k == 0) return;
+  const bool fast = (uint64_t)k <= mp.kchunk;
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    int i = idx / n, j = idx - i * n;
+    const uint32_t* ar = a.row(i);
+    uint64_t acc = 0;
+    if (fast) {
+      for (int t = 0; t < k; ++t) acc += (uint64_t)ar[t] * b.at(t, j);
+    } else {
+      uint64_t cntk = 0;
+      for (int t = 0; t < k; ++t) {
+        acc += (uint64_t)ar[t] * b.at(t, j);
+        if (++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+      }
+    }
+    c.at(i, j) = submod(c.at(i, j), reduce64(acc, mp), mp);
+  }
+  __syncthreads();
+}
+
+// B <- L^-1 B, L unit lower (kernels.py:59-83); one thread per column of B.
+__device__ void cta_trsm_llu(const View& l, const View& b, const ModP& mp) {
+  const int r = l.m, n = b.n;
+  if (r == 0 || n == 0) return;
+  const bool fast = (uint64_t)r <= mp.kchunk;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    for (int i = 1; i < r; ++i) {
+      const uint32_t* lr = l.row(i);
+      uint64_t acc = 0, cntk = 0;
+      for (int t = 0; t < i; ++t) {
+        acc += (uint64_t)lr[t] * b.at(t, c);
+        if (!fast && ++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+      }
+      b.at(i, c) = submod(b.at(i, c), reduce64(acc, mp), mp);
+    }
+  }
+  __syncthreads();
+}
+
+// B <- B U^-1, U upper with nonzero diagonal (kernels.py:85-120); one thread per row.
+__device__ void cta_trsm_ru(const View& b, const View& u, int* inv_scratch, const ModP& mp) {
+  const int m = b.m, r = u.m;
+  if (r == 0 || m == 0) return;
+  uint32_t* inv = reinterpret_cast<uint32_t*>(inv_scratch);
+  for (int j = threadIdx.x; j < r; j += blockDim.x) inv[j] = invmod(u.at(j, j), mp);
+  __syncthreads();
+  const bool fast = (uint64_t)r <= mp.kchunk;
+  for (int rr = threadIdx.x; rr < m; rr += blockDim.x) {
+    uint32_t* row = b.row(rr);
+    for (int j = 0; j < r; ++j) {
+      uint64_t acc = 0, cntk = 0;
+      for (int i = 0; i < j; ++i) {
+        acc += (uint64_t)row[i] * u.at(i, j);
+        if (!fast && ++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+      }
+      row[j] = mulmod(submod(row[j], reduce64(acc, mp), mp), inv[j], mp);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cta_copy(const View& dst, const View& src) {
+  for (int idx = threadIdx.x; idx < dst.m * dst.n; idx += blockDim.x) {
+    int i = idx / dst.n, j = idx - i * dst.n;
+    dst.at(i, j) = src.at(i, j);
+  }
+  __syncthreads();
+}
+
+// Base case in shared memory; scratch from the stack.
+__device__ int base_smem(const View& x, int* P, int* Q, int* stk, SmallCtx& c) {
+  const int m = x.m, n = x.n, mn = min(m, n);
+  BcScratch s;
+  s.prow = reinterpret_cast<uint8_t*>(stk);
+  s.pcol = s.prow + m;
+  int* p = stk + (m + n + 3) / 4 + 1;
+  s.rord = p; p += mn;
+  s.cord = p; p += mn;
+  s.rowat = p; p += m;
+  s.colat = p; p += n;
+  int* cyc = p;
+  BcShared* sh = c.sh;
+  auto gather = [&](const int* rowat, const int* colat, int) {
+    cta_gather_rows(x, rowat, cyc, sh);
+    cta_gather_cols(x, colat, cyc, sh);
+  };
+  Counts* cnt = c.cnt;
+  return basecase_cta(x, P, Q, s, sh, c.mp, cnt, gather);
+}
+
+// Row-block permutation S and column-block permutation T (recursive.py:77-99).
+__device__ __forceinline__ int s_sigma(int x, int r1, int r2, int r3, int r4, int k) {
+  int a = r1 + r2, c = r3 + r4, b = k - a;
+  if (x >= a && x < k) return x + c;
+  if (x >= k && x < k + c) return x - b;
+  return x;
+}
+__device__ __forceinline__ int t_sigma(int x, int r1, int r2, int r3, int r4, int k) {
+  if (x < r1) return x;
+  if (x < r1 + r2) return x + (k - r1);
+  if (x < r1 + r2 + r3) return x - r2;
+  if (x < r1 + r2 + r3 + r4) return x + (k + r2 - (r1 + r2 + r3));
+  if (x < k + r2 + r4) return x - (r2 + r4);
+  return x;
+}
+
+__device__ int rec_smem(const View& x, int* P, int* Q, int* stk, SmallCtx& c) {
+  const int m = x.m, n = x.n;
+  BcShared* sh = c.sh;
+  if (m == 0 || n == 0) {
+    cta_ident(P, m); cta_ident(Q, n); __syncthreads();
+    return 0;
+  }
+  if (m == 1 || n == 1 || min(m, n) <= c.threshold) return base_smem(x, P, Q, stk, c);
+  const int kr = m / 2, kc = n / 2;
+  const ModP& mp = c.mp;
+  const bool t0 = threadIdx.x == 0;
+
+  int* P1 = stk; int* Q1 = P1 + kr; int* top = Q1 + kc;
+  const int r1 = rec_smem(x.sub(0, 0, kr, kc), P1, Q1, top, c);
+  {
+    int* g = top; int* scr = g + max(m, n);
+    cta_inverse(P1, g, kr);
+    cta_gather_rows(x.sub(0, kc, kr, n - kc), g, scr, sh);
+    cta_gather_cols(x.sub(kr, 0, m - kr, kc), Q1, scr, sh);
+  }
+  cta_trsm_llu(x.sub(0, 0, r1, r1), x.sub(0, kc, r1, n - kc), mp);
+  cta_trsm_ru(x.sub(kr, 0, m - kr, r1), x.sub(0, 0, r1, r1), top, mp);
+  if (t0) {
+    charge_trsm_l(*c.cnt, r1, n - kc);
+    charge_trsm_u(*c.cnt, m - kr, r1);
+    charge_mm(*c.cnt, kr - r1, n - kc, r1);
+    charge_mm(*c.cnt, m - kr, kc - r1, r1);
+    charge_mm(*c.cnt, m - kr, n - kc, r1);
+  }
+  cta_mm_sub(x.sub(r1, kc, kr - r1, n - kc), x.sub(r1, 0, kr - r1, r1), x.sub(0, kc, r1, n - kc), mp);
+  // G and H share A = E: one pass over the contiguous column range r1..n
+  cta_mm_sub(x.sub(kr, r1, m - kr, n - r1), x.sub(kr, 0, m - kr, r1), x.sub(0, r1, r1, n - r1), mp);
+
+  int* P2 = top; int* Q2 = P2 + (kr - r1); top = Q2 + (n - kc);
+  const int r2 = rec_smem(x.sub(r1, kc, kr - r1, n - kc), P2, Q2, top, c);
+  int* P3 = top; int* Q3 = P3 + (m - kr); top = Q3 + (kc - r1);
+  const int r3 = rec_smem(x.sub(kr, r1, m - kr, kc - r1), P3, Q3, top, c);
+  {
+    int* ip3 = top; int* ip2 = ip3 + (m - kr); int* scr = ip2 + (kr - r1);
+    cta_inverse(P3, ip3, m - kr);
+    cta_inverse(P2, ip2, kr - r1);
+    cta_gather_rows(x.sub(kr, kc, m - kr, n - kc), ip3, scr, sh);
+    cta_gather_cols(x.sub(kr, kc, m - kr, n - kc), Q2, scr, sh);
+    cta_gather_rows(x.sub(kr, 0, m - kr, r1), ip3, scr, sh);
+    cta_gather_rows(x.sub(r1, 0, kr - r1, r1), ip2, scr, sh);
+    cta_gather_cols(x.sub(0, kc, r1, n - kc), Q2, scr, sh);
+    cta_gather_cols(x.sub(0, r1, r1, kc - r1), Q3, scr, sh);
+  }
+  const View u2 = x.sub(r1, kc, r2, r2);
+  const View l3 = x.sub(kr, r1, r3, r3);
+  const int m4 = m - kr - r3, n4 = n - kc - r2;
+  cta_trsm_ru(x.sub(kr, kc, r3, r2), u2, top, mp);                       // I
+  View J{reinterpret_cast<uint32_t*>(top), r2, r3, r2};
+  int* top2 = top + r3 * r2 + 1;
+  cta_copy(J, x.sub(kr, kc, r3, r2));
+  cta_trsm_llu(l3, J, mp);                                               // J (scratch)
+  cta_trsm_ru(x.sub(kr + r3, kc, m4, r2), u2, top2, mp);                 // K
+  cta_trsm_llu(l3, x.sub(kr, kc + r2, r3, n4), mp);                      // N
+  cta_mm_sub(x.sub(kr, kc + r2, r3, n4), J, x.sub(r1, kc + r2, r2, n4), mp);   // O
+  cta_mm_sub(x.sub(kr + r3, kc + r2, m4, n4), x.sub(kr + r3, kc, m4, r2), x.sub(r1, kc + r2, r2, n4), mp);
+  cta_mm_sub(x.sub(kr + r3, kc + r2, m4, n4), x.sub(kr + r3, r1, m4, r3), x.sub(kr, kc + r2, r3, n4), mp);
+  if (t0) {
+    charge_trsm_u(*c.cnt, r3, r2);
+    charge_trsm_l(*c.cnt, r3, r2);
+    charge_trsm_u(*c.cnt, m4, r2);
+    charge_trsm_l(*c.cnt, r3, n4);
+    charge_mm(*c.cnt, r3, n4, r2);
+    charge_mm(*c.cnt, m4, n4, r2);
+    charge_mm(*c.cnt, m4, n4, r3);
+  }
+
+  int* P4 = top; int* Q4 = P4 + m4; top = Q4 + n4;
+  const int r4 = rec_smem(x.sub(kr + r3, kc + r2, m4, n4), P4, Q4, top, c);
+  {
+    int* ip4 = top; int* scr = ip4 + m4;
+    cta_inverse(P4, ip4, m4);
+    cta_gather_rows(x.sub(kr + r3, 0, m4, kc + r2), ip4, scr, sh);
+    cta_gather_cols(x.sub(0, kc + r2, kr + r3, n4), Q4, scr, sh);
+  }
+  {
+    int* is = top; int* tg = is + m; int* scr = tg + n;
+    for (int t = threadIdx.x; t < m; t += blockDim.x) is[s_sigma(t, r1, r2, r3, r4, kr)] = t;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) tg[t] = t_sigma(t, r1, r2, r3, r4, kc);
+    __syncthreads();
+    cta_gather_rows(x, is, scr, sh);
+    cta_gather_cols(x, tg, scr, sh);
+  }
+  // P = Diag(P1 Diag(I,P2), P3 Diag(I,P4)) S ; Q = T Diag(Diag(I,Q3) Q1, Diag(I,Q4) Q2)
+  for (int t = threadIdx.x; t < m; t += blockDim.x) {
+    int y;
+    if (t < kr) { int z = P1[t]; y = z < r1 ? z : r1 + P2[z - r1]; }
+    else { int z = P3[t - kr]; y = kr + (z < r3 ? z : r3 + P4[z - r3]); }
+    P[t] = s_sigma(y, r1, r2, r3, r4, kr);
+  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    int z = t_sigma(t, r1, r2, r3, r4, kc);
+    int y;
+    if (z < kc) { int w = z < r1 ? z : r1 + Q3[z - r1]; y = Q1[w]; }
+    else { int zz = z - kc; int w = zz < r2 ? zz : r2 + Q4[zz - r2]; y = kc + Q2[w]; }
+    Q[t] = y;
+  }
+  __syncthreads();
+  return r1 + r2 + r3 + r4;
+}
+
+// Worst-case stack words for rec_smem on an m x n node (host + device).
+PLUQ_HD int64_t small_stack_words(int64_t m, int64_t n) {
+  int64_t depth = 2;
+  for (int64_t s = (m > n ? m : n); s > 1; s >>= 1) ++depth;
+  return 6 * (m + n) * depth + ((m + 1) / 2) * ((n + 1) / 2) + 64;
+}
+
+}  // namespace pluq

@@ -1,0 +1,397 @@
+// Tensor-core modular GEMM  C <- C - A B  (mod p)  on sm_100a.
+//
+// Replaces ClassicalKernels.mm_acc (/root/reference/pkg/src/pluq/kernels.py:38-55),
+// whose arithmetic core is numpy float64/int64 matmul (field.py:149-161).
+//
+// Representation: residues (< p < 2^31) are split into L = ceil(bits(p-1)/8)
+// unsigned 8-bit limbs.  A B = sum_{i,j} 2^{8(i+j)} A_i B_j, so the L^2 limb
+// products are accumulated by `tcgen05.mma.cta_group::1.kind::i8` (u8 x u8 -> s32)
+// into 2L-1 TMEM accumulators, one per limb position s = i+j.  Position s holds at
+// most L products of K terms each < 255^2, so one pass is exact while
+// K * L * 255^2 < 2^31; longer K is split into passes.  The fused epilogue reads
+// the accumulators with tcgen05.ld, recombines them by Horner mod p
+// (v <- v*256 + acc_s), subtracts from C and stores.
+//
+// Data movement: a conversion kernel writes the limb planes of the A view
+// (row-major = K-major) and of B^T (K-major) into zero-padded scratch, so every
+// TMA box is in bounds and no K tail needs masking.  TMA (SWIZZLE_128B) stages
+// 128x128-byte A tiles and BNx128-byte B tiles per limb into a STAGES-deep
+// mbarrier ring; one elected thread issues the MMAs; four epilogue warps own the
+// 128 TMEM lanes.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "pluq_common.cuh"
+
+namespace pluq {
+
+// ------------------------------- PTX wrappers ---------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* holder, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(holder)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row groups 1024 B apart).
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;              // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // stride byte offset
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+  return d;
+}
+
+// kind::i8 instruction descriptor: s32 accumulate, u8 x u8, both K-major, M=128.
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+template <int L>
+struct TcCfg;
+template <> struct TcCfg<1> { static constexpr int BN = 256, STAGES = 4, TCOLS = 256; };
+template <> struct TcCfg<2> { static constexpr int BN = 128, STAGES = 3, TCOLS = 512; };
+template <> struct TcCfg<3> { static constexpr int BN = 64, STAGES = 3, TCOLS = 512; };
+template <> struct TcCfg<4> { static constexpr int BN = 64, STAGES = 2, TCOLS = 512; };
+
+constexpr int TC_BM = 128, TC_BK = 128;
+
+template <int L>
+constexpr size_t tc_smem_bytes() {
+  return 1024 + (size_t)TcCfg<L>::STAGES * L * (TC_BM * TC_BK + TcCfg<L>::BN * TC_BK) + 256;
+}
+
+template <int L>
+__global__ void __launch_bounds__(256, 1)
+    tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
+                      int m_pad, int n_pad, int kblocks, ModP mp) {
+  constexpr int BN = TcCfg<L>::BN, STAGES = TcCfg<L>::STAGES, TCOLS = TcCfg<L>::TCOLS;
+  constexpr int NPOS = 2 * L - 1;
+  constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
+  constexpr uint32_t STAGE_BYTES = L * (A_TILE + B_TILE);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                  // [STAGES][L][128x128]
+  uint8_t* sB = smem + (size_t)STAGES * L * A_TILE;    // [STAGES][L][BNx128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)STAGES * L * B_TILE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) tmem_alloc(tholder, TCOLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tholder;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+      mbar_expect_tx(&full[s], STAGE_BYTES);
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        tma_load_2d(sA + ((size_t)s * L + l) * A_TILE, &ta, &full[s], kb * TC_BK, l * m_pad + m0);
+        tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], kb * TC_BK, l * n_pad + n0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread) ----------------
+    constexpr uint32_t idesc = idesc_i8(BN);
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA + (size_t)s * L * A_TILE);
+      const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 32; ++kk) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+#pragma unroll
+          for (int j = 0; j < L; ++j) {
+            const int pos = i + j;
+            const int first_i = pos < L ? 0 : pos - (L - 1);
+            const uint32_t acc = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
+            const uint64_t ad = desc_k_sw128(a0 + i * A_TILE + kk * 32);
+            const uint64_t bd = desc_k_sw128(b0 + j * B_TILE + kk * 32);
+            mma_i8(tbase + (uint32_t)(pos * BN), ad, bd, idesc, acc);
+          }
+        }
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(tfull);
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> recombine mod p -> C ----------------
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    uint32_t* crow = row < c.m ? c.row(row) : nullptr;
+#pragma unroll 1
+    for (int cc = 0; cc < BN; cc += 8) {
+      uint32_t acc[NPOS][8];
+#pragma unroll
+      for (int s = 0; s < NPOS; ++s) tmem_ld8(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+      tmem_ld_wait();
+      if (crow) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int col = n0 + cc + t;
+          if (col < c.n) {
+            uint32_t v = reduce64(acc[NPOS - 1][t], mp);
+#pragma unroll
+            for (int s = NPOS - 2; s >= 0; --s) v = reduce64(((uint64_t)v << 8) + acc[s][t], mp);
+            crow[col] = submod(crow[col], v, mp);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, TCOLS);
+  }
+}
+
+// Limb planes of a row-major view (K-major operand): out[l][i][kk] = limb_l(v[i][kk]),
+// zero-padded to rows_pad x k_pad.  4 consecutive bytes per thread.
+__global__ void limb_rows_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad) {
+  const int64_t plane = (int64_t)rows_pad * k_pad;
+  const int kq = k_pad / 4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rows_pad * kq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / kq), k4 = (int)(t - (int64_t)i * kq) * 4;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (i < v.m) {
+      const uint32_t* r = v.row(i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[e] = (k4 + e < v.n) ? r[k4 + e] : 0u;
+    }
+    for (int l = 0; l < L; ++l) {
+      const int sh = 8 * l;
+      uint32_t packed = ((w[0] >> sh) & 255u) | (((w[1] >> sh) & 255u) << 8) | (((w[2] >> sh) & 255u) << 16) |
+                        (((w[3] >> sh) & 255u) << 24);
+      *reinterpret_cast<uint32_t*>(out + l * plane + (int64_t)i * k_pad + k4) = packed;
+    }
+  }
+}
+
+// Limb planes of B^T (B is k x n row-major): out[l][j][kk] = limb_l(B[kk][j]),
+// zero-padded to n_pad x k_pad; 32x32 tiles transposed through shared memory.
+__global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_pad) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t plane = (int64_t)n_pad * k_pad;
+  const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  for (int r = ty; r < 32; r += 8) {
+    const int kk = k0 + r, j = j0 + tx;
+    tile[r][tx] = (kk < b.m && j < b.n) ? b.at(kk, j) : 0u;
+  }
+  __syncthreads();
+  // each thread writes 4 consecutive kk bytes of one column j
+  const int jj = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
+  if (j0 + jj < n_pad) {
+    for (int l = 0; l < L; ++l) {
+      const int sh = 8 * l;
+      uint32_t packed = ((tile[kq][jj] >> sh) & 255u) | (((tile[kq + 1][jj] >> sh) & 255u) << 8) |
+                        (((tile[kq + 2][jj] >> sh) & 255u) << 16) | (((tile[kq + 3][jj] >> sh) & 255u) << 24);
+      *reinterpret_cast<uint32_t*>(out + l * plane + (int64_t)(j0 + jj) * k_pad + k0 + kq) = packed;
+    }
+  }
+}
+
+// ------------------------------- host side ---------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct TcGemm {
+  PFN_encodeTiled encode = nullptr;
+  std::string last_error;
+  int64_t k_pass_override = 0;  // tests: force multi-pass K splitting
+  bool attrs_set[5] = {false, false, false, false, false};
+
+  static int limbs(uint32_t p) {
+    int bits = 0;
+    for (uint32_t v = p - 1; v; v >>= 1) ++bits;
+    return bits <= 8 ? 1 : (bits + 7) / 8;
+  }
+  // largest exact K per pass, multiple of TC_BK: K * L * 255^2 < 2^31
+  static int64_t k_pass(int L) {
+    int64_t kp = ((int64_t(1) << 31) - 1) / ((int64_t)L * 255 * 255);
+    return (kp / TC_BK) * TC_BK;
+  }
+
+  void release() {}
+
+  bool load() {
+    if (encode) return true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      last_error = "cuTensorMapEncodeTiled unavailable";
+      return false;
+    }
+    encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    return true;
+  }
+
+  bool make_map(CUtensorMap* map, void* base, int64_t inner_bytes, int64_t rows, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)inner_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)inner_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+      return false;
+    }
+    return true;
+  }
+
+  template <int L>
+  int launch(const View& c, const View& a, const View& b, const ModP& mp, cudaStream_t st) {
+    constexpr int BN = TcCfg<L>::BN;
+    const int m = c.m, n = c.n, k = a.n;
+    const int m_pad = (m + TC_BM - 1) / TC_BM * TC_BM;
+    const int n_pad = (n + BN - 1) / BN * BN;
+    int64_t kp = k_pass_override > 0 ? k_pass_override : k_pass(L);
+    kp = (kp / TC_BK) * TC_BK;
+    if (kp <= 0) kp = TC_BK;
+    const int64_t k_first = std::min<int64_t>(k, kp);
+    const int kpad_max = (int)((k_first + TC_BK - 1) / TC_BK * TC_BK);
+    uint8_t *da = nullptr, *db = nullptr;
+    if (cudaMallocAsync((void**)&da, (size_t)L * m_pad * kpad_max, st) != cudaSuccess ||
+        cudaMallocAsync((void**)&db, (size_t)L * n_pad * kpad_max, st) != cudaSuccess) {
+      last_error = "workspace allocation failed";
+      return kNoMemory;
+    }
+    constexpr size_t smem = tc_smem_bytes<L>();
+    if (!attrs_set[L]) {
+      if (cudaFuncSetAttribute(tc_modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess) {
+        last_error = "cannot set shared memory size";
+        return kCuda;
+      }
+      attrs_set[L] = true;
+    }
+    for (int64_t k0 = 0; k0 < k; k0 += kp) {
+      const int kc = (int)std::min<int64_t>(kp, k - k0);
+      const int k_pad = (kc + TC_BK - 1) / TC_BK * TC_BK;
+      View as = a.sub(0, (int)k0, m, kc);
+      View bs = b.sub((int)k0, 0, kc, n);
+      {
+        int64_t work = (int64_t)m_pad * (k_pad / 4);
+        int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 32);
+        limb_rows_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad);
+      }
+      {
+        dim3 grid(n_pad / 32, k_pad / 32);
+        limb_cols_kernel<<<grid, 256, 0, st>>>(bs, db, L, n_pad, k_pad);
+      }
+      CUtensorMap ta, tb;
+      if (!make_map(&ta, da, k_pad, (int64_t)L * m_pad, TC_BM) || !make_map(&tb, db, k_pad, (int64_t)L * n_pad, BN)) {
+        cudaFreeAsync(da, st);
+        cudaFreeAsync(db, st);
+        return kCuda;
+      }
+      dim3 grid(n_pad / BN, m_pad / TC_BM);
+      tc_modgemm_kernel<L><<<grid, 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);
+        cudaFreeAsync(da, st);
+        cudaFreeAsync(db, st);
+        return kCuda;
+      }
+    }
+    cudaFreeAsync(da, st);
+    cudaFreeAsync(db, st);
+    return kOk;
+  }
+
+  int run(const View& c, const View& a, const View& b, const ModP& mp, cudaStream_t st) {
+    if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
+    if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
+    if (!load()) return kUnsupported;
+    switch (limbs(mp.p)) {
+      case 1: return launch<1>(c, a, b, mp, st);
+      case 2: return launch<2>(c, a, b, mp, st);
+      case 3: return launch<3>(c, a, b, mp, st);
+      case 4: return launch<4>(c, a, b, mp, st);
+    }
+    return kUnsupported;
+  }
+};
+
+}  // namespace pluq
