@@ -285,7 +285,7 @@ struct Driver {
   Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ModP::make(p)), threshold(thr), ops{ctx, ModP::make(p)} {}
 
   bool fits_small(int64_t m, int64_t n) const {
-    return m * n <= c->small_cap && small_smem_bytes(m, n) <= 227 * 1024;
+    return m * n <= c->small_cap && small_smem_bytes(m, n, threshold) <= 227 * 1024;
   }
 
   NodeRes readback(int m, int n) {
@@ -304,7 +304,7 @@ struct Driver {
     a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
     a.p_out = c->d_res; a.q_out = c->d_res + x.m; a.r_out = c->d_res + x.m + x.n;
     a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
-    size_t smem = small_smem_bytes(x.m, x.n);
+    size_t smem = small_smem_bytes(x.m, x.n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
     c->check_launch();
@@ -603,7 +603,7 @@ int pluq_factor_iterative(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int6
 }
 
 int64_t pluq_batched_max_elems(pluq_ctx*, int64_t m, int64_t n) {
-  return small_smem_bytes(m, n) <= 227 * 1024 ? m * n : 0;
+  return small_smem_bytes(m, n, 30) <= 227 * 1024 ? m * n : 0;
 }
 
 int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch, int64_t m, int64_t n,
@@ -611,7 +611,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
                         uint64_t* d_counts) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (small_smem_bytes(m, n) > 227 * 1024) return kUnsupported;
+  if (small_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
   if (batch == 0) return kOk;
   return guarded(c, [&] {
     SmallArgs a;
@@ -622,7 +622,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counts);
     if (!cnt) cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
     a.cnt_out = cnt; a.cnt_accumulate = 0;
-    size_t smem = small_smem_bytes(m, n);
+    size_t smem = small_smem_bytes(m, n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t b0 = 0; b0 < batch; b0 += 2147483647ll) {
       small_pluq_kernel<<<(unsigned)std::min<int64_t>(batch - b0, 2147483647ll), (unsigned)c->small_threads, smem, c->stream>>>(a);
@@ -675,7 +675,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
                                  int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* ranks) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (small_smem_bytes(m, n) > 227 * 1024) return kUnsupported;
+  if (small_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
   return guarded(c, [&] {
     const int64_t cnt = batch * m * n;
     if (cnt == 0) return;

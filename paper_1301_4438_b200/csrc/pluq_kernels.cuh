@@ -59,9 +59,10 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   }
 }
 
-inline size_t small_smem_bytes(int64_t m, int64_t n) {
+// Dynamic shared memory of small_pluq_kernel: block (odd pitch) + P/Q + recursion stack.
+inline size_t small_smem_bytes(int64_t m, int64_t n, int64_t thr) {
   int64_t lds = n | 1;
-  return (size_t)((((m * lds) + 3) & ~3ll) + small_stack_words(m, n)) * 4;
+  return (size_t)((((m * lds) + 3) & ~3ll) + m + n + small_stack_words(m, n, thr) + 64) * 4;
 }
 
 // ---------------------------------------------------------------------------------

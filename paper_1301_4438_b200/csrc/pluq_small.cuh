@@ -309,11 +309,22 @@ __device__ int rec_smem(const View& x, int* P, int* Q, int* stk, SmallCtx& c) {
   return r1 + r2 + r3 + r4;
 }
 
-// Worst-case stack words for rec_smem on an m x n node (host + device).
-PLUQ_HD int64_t small_stack_words(int64_t m, int64_t n) {
-  int64_t depth = 2;
-  for (int64_t s = (m > n ? m : n); s > 1; s >>= 1) ++depth;
-  return 6 * (m + n) * depth + ((m + 1) / 2) * ((n + 1) / 2) + 64;
+// Worst-case stack words used by rec_smem on an m x n node with the given threshold,
+// following its allocation pattern: at most 2(m+n) words of live child permutations,
+// then either the transient buffers of this level (gather/cycle scratch, S/T vectors,
+// the J scratch of at most ceil(m/2) x ceil(n/2)) or a child's own stack, where every
+// child block (A1, F, G, R) is at most ceil(m/2) x ceil(n/2).
+inline int64_t small_stack_words(int64_t m, int64_t n, int64_t thr) {
+  if (m == 0 || n == 0) return 0;
+  const int64_t mx = m > n ? m : n, mn = m < n ? m : n;
+  if (m == 1 || n == 1 || mn <= thr)  // base_smem: flags, orders, positions, cycles
+    return (m + n + 3) / 4 + 1 + 2 * mn + m + n + 3 * mx + 8;
+  const int64_t hm = (m + 1) / 2, hn = (n + 1) / 2;
+  int64_t own = 5 * mx + m + n;                  // S/T vectors + cycle scratch
+  int64_t jbuf = hm * hn + 1 + mx;               // J scratch + TRSM inverse scratch
+  int64_t child = small_stack_words(hm, hn, thr);
+  int64_t t = own > jbuf ? own : jbuf;
+  return 2 * (m + n) + (t > child ? t : child) + 8;
 }
 
 }  // namespace pluq
