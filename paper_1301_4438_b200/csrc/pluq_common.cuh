@@ -39,33 +39,36 @@ struct ModP {
 };
 
 // x mod p for any 64-bit x.
-PLUQ_HD uint32_t reduce64(uint64_t x, const ModP& m) {
+// Barrett: q = floor(x * mu / 2^64) underestimates floor(x / p) by at most 2, so two
+// branch-free conditional subtractions finish the reduction.
+PLUQ_HD uint32_t reduce64(uint64_t x, const ModP m) {
 #ifdef __CUDA_ARCH__
   uint64_t q = __umul64hi(x, m.mu);
 #else
   uint64_t q = (uint64_t)(((unsigned __int128)x * m.mu) >> 64);
 #endif
   uint64_t r = x - q * (uint64_t)m.p;
-  while (r >= m.p) r -= m.p;
+  r = r >= m.p ? r - m.p : r;
+  r = r >= m.p ? r - m.p : r;
   return (uint32_t)r;
 }
 
-PLUQ_HD uint32_t mulmod(uint32_t a, uint32_t b, const ModP& m) {
+PLUQ_HD uint32_t mulmod(uint32_t a, uint32_t b, const ModP m) {
   return reduce64((uint64_t)a * b, m);
 }
 
-PLUQ_HD uint32_t addmod(uint32_t a, uint32_t b, const ModP& m) {
+PLUQ_HD uint32_t addmod(uint32_t a, uint32_t b, const ModP m) {
   uint32_t s = a + b;  // a, b < 2^31 so no wrap
   return s >= m.p ? s - m.p : s;
 }
 
-PLUQ_HD uint32_t submod(uint32_t a, uint32_t b, const ModP& m) {
+PLUQ_HD uint32_t submod(uint32_t a, uint32_t b, const ModP m) {
   return a >= b ? a - b : a + (m.p - b);
 }
 
 // Multiplicative inverse via extended Euclid (field.py:41-52); a != 0 mod p.
 // 32-bit arithmetic throughout: remainders are < p < 2^31 and |Bezout coefficients| <= p.
-PLUQ_HD uint32_t invmod(uint32_t a, const ModP& m) {
+PLUQ_HD uint32_t invmod(uint32_t a, const ModP m) {
   uint32_t old_r = a, r = m.p;
   int32_t old_s = 1, s = 0;
   while (r) {

@@ -82,7 +82,8 @@ struct pluq_ctx {
   int* h_flag = nullptr;
   // options
   int64_t small_cap = 128 * 128;   // max m*n of a node factored whole by one CTA
-  int64_t small_threads = 256;
+  int64_t small_threads = 256;    // CTA size of a host-recursion leaf node
+  int64_t batch_threads = 32;     // CTA size of the batched kernel (one matrix per CTA)
   int64_t use_tc = 1;
   int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
   int64_t tc_min_k = 32;
@@ -90,6 +91,20 @@ struct pluq_ctx {
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
           st_simt = 0, st_zero_skips = 0;
   TcGemm tc;
+  uint16_t* d_invtab = nullptr;  // inverse table for invtab_p (p < 2^16)
+  uint32_t invtab_p = 0;
+
+  const uint16_t* invtab(uint32_t p) {
+    if (p >= 65536) return nullptr;
+    if (invtab_p != p) {
+      if (!d_invtab) CU(cudaMalloc((void**)&d_invtab, 65536 * sizeof(uint16_t)));
+      invtab_kernel<<<64, 256, 0, stream>>>(d_invtab, ModP::make(p));
+      check_launch();
+      invtab_p = p;
+      CU(cudaStreamSynchronize(stream));  // one-time; the table may be read from other streams
+    }
+    return d_invtab;
+  }
 
   void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = 0; }
 
@@ -172,40 +187,58 @@ struct Ops {
     c->check_launch();
   }
 
+  // split point on the 64-grid of the precomputed diagonal-block inverses
   static int split(int r) {
-    int h = r / 2;
-    if (r >= 256) h = std::max(64, (h / 64) * 64);
-    return h;
+    int nb = (r + TR_BASE - 1) / TR_BASE;
+    return TR_BASE * (nb / 2);
   }
 
   // ---- B <- L^-1 B (kernels.py:59-83) -------------------------------------------------
   void trsm_l(const View& l, const View& b) {
     const int r = l.m;
     if (r == 0 || b.n == 0) return;
+    const int nb = (r + TR_BASE - 1) / TR_BASE;
+    uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
+    trinv_lower_unit_kernel<<<nb, 64, 0, c->stream>>>(l, inv, mp);
+    c->check_launch();
+    trsm_l_rec(l, b, inv);
+    c->dfree(inv);
+  }
+  void trsm_l_rec(const View& l, const View& b, const uint32_t* inv) {
+    const int r = l.m;
     if (r <= TR_BASE) {
-      trsm_llu_base_kernel<<<(b.n + 127) / 128, 128, 0, c->stream>>>(l, b, mp);
+      trsm_apply_left_kernel<<<(b.n + 63) / 64, 256, 0, c->stream>>>(inv, b, mp);
       c->check_launch();
       return;
     }
     int h = split(r);
-    trsm_l(l.sub(0, 0, h, h), b.sub(0, 0, h, b.n));
+    trsm_l_rec(l.sub(0, 0, h, h), b.sub(0, 0, h, b.n), inv);
     gemm(b.sub(h, 0, r - h, b.n), l.sub(h, 0, r - h, h), b.sub(0, 0, h, b.n));
-    trsm_l(l.sub(h, h, r - h, r - h), b.sub(h, 0, r - h, b.n));
+    trsm_l_rec(l.sub(h, h, r - h, r - h), b.sub(h, 0, r - h, b.n), inv + (size_t)(h / TR_BASE) * TR_BASE * TR_BASE);
   }
 
   // ---- B <- B U^-1 (kernels.py:85-120) ------------------------------------------------
   void trsm_u(const View& b, const View& u) {
     const int r = u.m;
     if (r == 0 || b.m == 0) return;
+    const int nb = (r + TR_BASE - 1) / TR_BASE;
+    uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
+    trinv_upper_kernel<<<nb, 64, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p));
+    c->check_launch();
+    trsm_u_rec(b, u, inv);
+    c->dfree(inv);
+  }
+  void trsm_u_rec(const View& b, const View& u, const uint32_t* inv) {
+    const int r = u.m;
     if (r <= TR_BASE) {
-      trsm_ru_base_kernel<<<(b.m + 63) / 64, 64, 0, c->stream>>>(b, u, mp);
+      trsm_apply_right_kernel<<<(b.m + 63) / 64, 256, 0, c->stream>>>(b, inv, mp);
       c->check_launch();
       return;
     }
     int h = split(r);
-    trsm_u(b.sub(0, 0, b.m, h), u.sub(0, 0, h, h));
+    trsm_u_rec(b.sub(0, 0, b.m, h), u.sub(0, 0, h, h), inv);
     gemm(b.sub(0, h, b.m, r - h), b.sub(0, 0, b.m, h), u.sub(0, h, h, r - h));
-    trsm_u(b.sub(0, h, b.m, r - h), u.sub(h, h, r - h, r - h));
+    trsm_u_rec(b.sub(0, h, b.m, r - h), u.sub(h, h, r - h, r - h), inv + (size_t)(h / TR_BASE) * TR_BASE * TR_BASE);
   }
 
   // ---- gathers restricted to the moved set (matrix.py:249-283) ----------------------
@@ -304,6 +337,7 @@ struct Driver {
     a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
     a.p_out = c->d_res; a.q_out = c->d_res + x.m; a.r_out = c->d_res + x.m + x.n;
     a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
+    a.invtab = c->invtab(mp.p);
     size_t smem = small_smem_bytes(x.m, x.n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
@@ -554,6 +588,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->d_counts) cudaFree(c->d_counts);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
+  if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   delete c;
   return kOk;
@@ -570,6 +605,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   std::string k(key);
   if (k == "small_cap") c->small_cap = value;
   else if (k == "small_threads") c->small_threads = value;
+  else if (k == "batch_threads") c->batch_threads = value;
   else if (k == "use_tc") c->use_tc = value;
   else if (k == "tc_min_dim") c->tc_min_dim = value;
   else if (k == "tc_min_k") c->tc_min_k = value;
@@ -622,10 +658,11 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counts);
     if (!cnt) cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
     a.cnt_out = cnt; a.cnt_accumulate = 0;
+    a.invtab = c->invtab((uint32_t)p);
     size_t smem = small_smem_bytes(m, n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t b0 = 0; b0 < batch; b0 += 2147483647ll) {
-      small_pluq_kernel<<<(unsigned)std::min<int64_t>(batch - b0, 2147483647ll), (unsigned)c->small_threads, smem, c->stream>>>(a);
+      small_pluq_kernel<<<(unsigned)std::min<int64_t>(batch - b0, 2147483647ll), (unsigned)c->batch_threads, smem, c->stream>>>(a);
       c->check_launch();
     }
     if (!d_counts) c->dfree(cnt);

@@ -18,6 +18,7 @@ struct SmallArgs {
   int* r_out;           // batch
   unsigned long long* cnt_out;  // batch x 4 (or 4 if cnt_accumulate)
   int cnt_accumulate;
+  const uint16_t* invtab;       // inverse table when p < 2^16 (else nullptr)
 };
 
 __global__ void small_pluq_kernel(SmallArgs args) {
@@ -35,7 +36,7 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   }
   if (threadIdx.x == 0) { cnt.mul = cnt.add = cnt.inv = cnt.red = 0; }
   __syncthreads();
-  SmallCtx c{args.mp, args.threshold, &cnt, &sh};
+  SmallCtx c{args.mp, args.threshold, &cnt, &sh, args.invtab};
   View x{sa, lds, m, n};
   int* P = stk; int* Q = P + m; int* top = Q + n;
   const int r = rec_smem(x, P, Q, top, c);
@@ -199,74 +200,128 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(View c, View a, View b, 
 }
 
 // ---------------------------------------------------------------------------------
-// TRSM base kernels (r <= 64): L / U resident in shared memory.
+// TRSM (kernels.py:59-120) as "invert the 64x64 diagonal blocks once, then multiply".
+// All diagonal-block inverses of a triangular factor are computed in ONE launch
+// (one CTA per block), so the recursive TRSM's critical path is only small
+// GEMM-shaped kernels; exact arithmetic makes the result identical to substitution.
 // ---------------------------------------------------------------------------------
 constexpr int TR_BASE = 64;
 
-// B <- L^-1 B for a strip of 128 columns per CTA (thread per column).
-__global__ void __launch_bounds__(128) trsm_llu_base_kernel(View l, View b, ModP mp) {
-  __shared__ uint32_t Ls[TR_BASE][TR_BASE];
-  __shared__ uint32_t Bs[TR_BASE][128];
-  const int r = l.m, n = b.n;
-  const int c0 = blockIdx.x * 128;
-  for (int idx = threadIdx.x; idx < r * r; idx += 128) {
-    int i = idx / r, j = idx % r;
-    Ls[i][j] = l.at(i, j);
-  }
-  for (int i = 0; i < r; ++i) {
-    int c = c0 + threadIdx.x;
-    Bs[i][threadIdx.x] = c < n ? b.at(i, c) : 0u;
-  }
-  __syncthreads();
-  const int c = threadIdx.x;
-  const bool fast = (uint64_t)r <= mp.kchunk;
-  for (int i = 1; i < r; ++i) {
-    uint64_t acc = 0, cntk = 0;
-    for (int t = 0; t < i; ++t) {
-      acc += (uint64_t)Ls[i][t] * Bs[t][c];
-      if (!fast && ++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+__device__ __forceinline__ uint32_t acc_dot(const uint32_t* a, int sa, const uint32_t* b, int sb, int k,
+                                            const ModP mp) {
+  uint64_t acc = 0;
+  if ((uint64_t)k <= mp.kchunk) {
+    for (int t = 0; t < k; ++t) acc += (uint64_t)a[t * sa] * b[t * sb];
+  } else {
+    uint64_t c = 0;
+    for (int t = 0; t < k; ++t) {
+      acc += (uint64_t)a[t * sa] * b[t * sb];
+      if (++c == mp.kchunk) { acc = reduce64(acc, mp); c = 0; }
     }
-    Bs[i][c] = submod(Bs[i][c], reduce64(acc, mp), mp);
   }
-  __syncthreads();
-  for (int i = 0; i < r; ++i) {
-    int cc = c0 + threadIdx.x;
-    if (cc < n) b.at(i, cc) = Bs[i][threadIdx.x];
-  }
+  return reduce64(acc, mp);
 }
 
-// B <- B U^-1 for a strip of 64 rows per CTA (thread per row, 64 threads).
-__global__ void __launch_bounds__(64) trsm_ru_base_kernel(View b, View u, ModP mp) {
+// out[b] = inverse of the b-th 64x64 diagonal block of U (upper, nonzero diagonal); 64 threads.
+__global__ void __launch_bounds__(64) trinv_upper_kernel(View u, uint32_t* out, ModP mp, const uint16_t* invtab) {
   __shared__ uint32_t Us[TR_BASE][TR_BASE + 1];
-  __shared__ uint32_t Bs[64][TR_BASE + 1];
-  __shared__ uint32_t inv[TR_BASE];
-  const int m = b.m, r = u.m;
-  const int r0 = blockIdx.x * 64;
-  for (int idx = threadIdx.x; idx < r * r; idx += 64) {
-    int i = idx / r, j = idx % r;
-    Us[i][j] = u.at(i, j);
-  }
-  for (int j = threadIdx.x; j < r; j += 64) inv[j] = invmod(u.at(j, j), mp);
-  for (int idx = threadIdx.x; idx < 64 * r; idx += 64) {
-    int i = idx / r, j = idx % r;
-    Bs[i][j] = (r0 + i < m) ? b.at(r0 + i, j) : 0u;
+  __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
+  __shared__ uint32_t dinv[TR_BASE];
+  const int base = blockIdx.x * TR_BASE;
+  const int w = min(TR_BASE, u.m - base);
+  for (int idx = threadIdx.x; idx < w * w; idx += 64) {
+    int i = idx / w, j = idx % w;
+    Us[i][j] = u.at(base + i, base + j);
   }
   __syncthreads();
-  const int i = threadIdx.x;
-  const bool fast = (uint64_t)r <= mp.kchunk;
-  for (int j = 0; j < r; ++j) {
-    uint64_t acc = 0, cntk = 0;
-    for (int t = 0; t < j; ++t) {
-      acc += (uint64_t)Bs[i][t] * Us[t][j];
-      if (!fast && ++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+  if ((int)threadIdx.x < w) dinv[threadIdx.x] = invtab ? invtab[Us[threadIdx.x][threadIdx.x]] : invmod(Us[threadIdx.x][threadIdx.x], mp);
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < w) {
+    for (int i = 0; i < w; ++i) X[i][j] = 0;
+    X[j][j] = dinv[j];
+    for (int i = j - 1; i >= 0; --i) {
+      uint32_t s = acc_dot(&Us[i][i + 1], 1, &X[i + 1][j], TR_BASE + 1, j - i, mp);
+      X[i][j] = mulmod(s ? mp.p - s : 0u, dinv[i], mp);
     }
-    Bs[i][j] = mulmod(submod(Bs[i][j], reduce64(acc, mp), mp), inv[j], mp);
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < 64 * r; idx += 64) {
-    int ii = idx / r, j = idx % r;
-    if (r0 + ii < m) b.at(r0 + ii, j) = Bs[ii][j];
+  uint32_t* o = out + (size_t)blockIdx.x * TR_BASE * TR_BASE;
+  for (int idx = threadIdx.x; idx < w * w; idx += 64) o[(idx / w) * TR_BASE + idx % w] = X[idx / w][idx % w];
+}
+
+// out[b] = inverse of the b-th diagonal block of unit-lower L (diagonal implicit 1); 64 threads.
+__global__ void __launch_bounds__(64) trinv_lower_unit_kernel(View l, uint32_t* out, ModP mp) {
+  __shared__ uint32_t Ls[TR_BASE][TR_BASE + 1];
+  __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
+  const int base = blockIdx.x * TR_BASE;
+  const int w = min(TR_BASE, l.m - base);
+  for (int idx = threadIdx.x; idx < w * w; idx += 64) {
+    int i = idx / w, j = idx % w;
+    Ls[i][j] = l.at(base + i, base + j);
   }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < w) {
+    for (int i = 0; i < w; ++i) X[i][j] = 0;
+    X[j][j] = 1;
+    for (int i = j + 1; i < w; ++i) {
+      uint32_t s = acc_dot(&Ls[i][j], 1, &X[j][j], TR_BASE + 1, i - j, mp);
+      X[i][j] = s ? mp.p - s : 0u;
+    }
+  }
+  __syncthreads();
+  uint32_t* o = out + (size_t)blockIdx.x * TR_BASE * TR_BASE;
+  for (int idx = threadIdx.x; idx < w * w; idx += 64) o[(idx / w) * TR_BASE + idx % w] = X[idx / w][idx % w];
+}
+
+// B <- B * Uinv for a w-column block (w <= 64): one CTA owns 64 rows of B (in place).
+__global__ void __launch_bounds__(256) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp) {
+  __shared__ uint32_t Bs[64][TR_BASE + 1];
+  __shared__ uint32_t Ui[TR_BASE][TR_BASE + 1];
+  const int w = b.n, r0 = blockIdx.x * 64, rows = min(64, b.m - r0);
+  for (int idx = threadIdx.x; idx < w * w; idx += 256) Ui[idx / w][idx % w] = uinv[(idx / w) * TR_BASE + idx % w];
+  for (int idx = threadIdx.x; idx < rows * w; idx += 256) Bs[idx / w][idx % w] = b.at(r0 + idx / w, idx % w);
+  __syncthreads();
+  const int rr = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 16;
+  uint32_t res[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int cc = c0 + q;
+    // X[rr][cc] = sum_{t<=cc} B[rr][t] Uinv[t][cc]
+    res[q] = (rr < rows && cc < w) ? acc_dot(&Bs[rr][0], 1, &Ui[0][cc], TR_BASE + 1, cc + 1, mp) : 0u;
+  }
+  __syncthreads();
+  if (rr < rows)
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (c0 + q < w) b.at(r0 + rr, c0 + q) = res[q];
+}
+
+// B <- Linv * B for a w-row block (w <= 64): one CTA owns 64 columns of B (in place).
+__global__ void __launch_bounds__(256) trsm_apply_left_kernel(const uint32_t* linv, View b, ModP mp) {
+  __shared__ uint32_t Bs[TR_BASE][64 + 1];
+  __shared__ uint32_t Li[TR_BASE][TR_BASE + 1];
+  const int w = b.m, c0 = blockIdx.x * 64, cols = min(64, b.n - c0);
+  for (int idx = threadIdx.x; idx < w * w; idx += 256) Li[idx / w][idx % w] = linv[(idx / w) * TR_BASE + idx % w];
+  for (int idx = threadIdx.x; idx < w * 64; idx += 256) {
+    int i = idx / 64, j = idx % 64;
+    Bs[i][j] = j < cols ? b.at(i, c0 + j) : 0u;
+  }
+  __syncthreads();
+  const int cc = threadIdx.x & 63, r0 = (threadIdx.x >> 6) * 16;
+  uint32_t res[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int rr = r0 + q;
+    // X[rr][cc] = sum_{t<=rr} Linv[rr][t] B[t][cc]
+    res[q] = (rr < w && cc < cols) ? acc_dot(&Li[rr][0], 1, &Bs[0][cc], 65, rr + 1, mp) : 0u;
+  }
+  __syncthreads();
+  if (cc < cols)
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (r0 + q < w) b.at(r0 + q, c0 + cc) = res[q];
 }
 
 // flag <- 1 if any diagonal entry of U is zero (kernels.py:93-95).
@@ -321,6 +376,12 @@ __global__ void copy_view_kernel(View dst, View src) {
   for (int i = blockIdx.y; i < dst.m; i += gridDim.y)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < dst.n; j += gridDim.x * blockDim.x)
       dst.at(i, j) = src.at(i, j);
+}
+
+// Table of inverses mod p (p < 2^16): tab[a] = a^-1, tab[0] = 0.
+__global__ void invtab_kernel(uint16_t* tab, ModP mp) {
+  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < mp.p; a += gridDim.x * blockDim.x)
+    tab[a] = a ? (uint16_t)invmod(a, mp) : 0;
 }
 
 // Host-format conversion: float64 / int64 residues <-> uint32 device storage.

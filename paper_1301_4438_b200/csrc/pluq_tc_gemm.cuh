@@ -100,12 +100,15 @@ __host__ __device__ constexpr uint32_t idesc_i8(int n) {
   return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
+// Persistent tiling: each CTA (one per SM) walks output tiles; TMEM holds TWO
+// accumulator sets (NPOS positions x BN columns each) so the epilogue of tile t
+// overlaps the MMAs of tile t+1.
 template <int L>
 struct TcCfg;
-template <> struct TcCfg<1> { static constexpr int BN = 256, STAGES = 4, TCOLS = 256; };
-template <> struct TcCfg<2> { static constexpr int BN = 128, STAGES = 3, TCOLS = 512; };
-template <> struct TcCfg<3> { static constexpr int BN = 64, STAGES = 3, TCOLS = 512; };
-template <> struct TcCfg<4> { static constexpr int BN = 64, STAGES = 2, TCOLS = 512; };
+template <> struct TcCfg<1> { static constexpr int BN = 256, STAGES = 4; };
+template <> struct TcCfg<2> { static constexpr int BN = 64, STAGES = 4; };
+template <> struct TcCfg<3> { static constexpr int BN = 32, STAGES = 3; };
+template <> struct TcCfg<4> { static constexpr int BN = 32, STAGES = 2; };
 
 constexpr int TC_BM = 128, TC_BK = 128;
 
@@ -114,12 +117,19 @@ constexpr size_t tc_smem_bytes() {
   return 1024 + (size_t)TcCfg<L>::STAGES * L * (TC_BM * TC_BK + TcCfg<L>::BN * TC_BK) + 256;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 template <int L>
 __global__ void __launch_bounds__(256, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
                       int m_pad, int n_pad, int kblocks, ModP mp) {
-  constexpr int BN = TcCfg<L>::BN, STAGES = TcCfg<L>::STAGES, TCOLS = TcCfg<L>::TCOLS;
+  constexpr int BN = TcCfg<L>::BN, STAGES = TcCfg<L>::STAGES;
   constexpr int NPOS = 2 * L - 1;
+  constexpr int ACC_COLS = NPOS * BN;               // one accumulator set
+  constexpr uint32_t TCOLS = 512;
+  static_assert(2 * ACC_COLS <= 512, "two accumulator sets must fit in TMEM");
   constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
   constexpr uint32_t STAGE_BYTES = L * (A_TILE + B_TILE);
   extern __shared__ uint8_t smem_raw[];
@@ -128,15 +138,16 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = smem + (size_t)STAGES * L * A_TILE;    // [STAGES][L][BNx128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)STAGES * L * B_TILE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+  const int tiles_n = n_pad / BN, tiles = (m_pad / TC_BM) * tiles_n;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) tmem_alloc(tholder, TCOLS);
@@ -147,69 +158,91 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-      mbar_expect_tx(&full[s], STAGE_BYTES);
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
+      for (int kb = 0; kb < kblocks; ++kb, ++g) {
+        const uint32_t s = g % STAGES;
+        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], STAGE_BYTES);
 #pragma unroll
-      for (int l = 0; l < L; ++l) {
-        tma_load_2d(sA + ((size_t)s * L + l) * A_TILE, &ta, &full[s], kb * TC_BK, l * m_pad + m0);
-        tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], kb * TC_BK, l * n_pad + n0);
+        for (int l = 0; l < L; ++l) {
+          tma_load_2d(sA + ((size_t)s * L + l) * A_TILE, &ta, &full[s], kb * TC_BK, l * m_pad + m0);
+          tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], kb * TC_BK, l * n_pad + n0);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
     constexpr uint32_t idesc = idesc_i8(BN);
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (kb / STAGES) & 1);
+    uint32_t g = 0, local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      const uint32_t buf = local & 1, use = local >> 1;
+      mbar_wait(&tempty[buf], (use & 1) ^ 1);
       tc_fence_after();
-      const uint32_t a0 = smem_u32(sA + (size_t)s * L * A_TILE);
-      const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
+      const uint32_t dacc = tbase + buf * ACC_COLS;
+      for (int kb = 0; kb < kblocks; ++kb, ++g) {
+        const uint32_t s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + (size_t)s * L * A_TILE);
+        const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
 #pragma unroll
-      for (int kk = 0; kk < TC_BK / 32; ++kk) {
+        for (int kk = 0; kk < TC_BK / 32; ++kk) {
 #pragma unroll
-        for (int i = 0; i < L; ++i) {
+          for (int i = 0; i < L; ++i) {
 #pragma unroll
-          for (int j = 0; j < L; ++j) {
-            const int pos = i + j;
-            const int first_i = pos < L ? 0 : pos - (L - 1);
-            const uint32_t acc = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
-            const uint64_t ad = desc_k_sw128(a0 + i * A_TILE + kk * 32);
-            const uint64_t bd = desc_k_sw128(b0 + j * B_TILE + kk * 32);
-            mma_i8(tbase + (uint32_t)(pos * BN), ad, bd, idesc, acc);
+            for (int j = 0; j < L; ++j) {
+              const int pos = i + j;
+              const int first_i = pos < L ? 0 : pos - (L - 1);
+              const uint32_t acc = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
+              const uint64_t ad = desc_k_sw128(a0 + i * A_TILE + kk * 32);
+              const uint64_t bd = desc_k_sw128(b0 + j * B_TILE + kk * 32);
+              mma_i8(dacc + (uint32_t)(pos * BN), ad, bd, idesc, acc);
+            }
           }
         }
+        mma_commit(&empty[s]);
       }
-      mma_commit(&empty[s]);
+      mma_commit(&tfull[buf]);
     }
-    mma_commit(tfull);
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> recombine mod p -> C ----------------
-    mbar_wait(tfull, 0);
-    tc_fence_after();
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
-    uint32_t* crow = row < c.m ? c.row(row) : nullptr;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      const uint32_t buf = local & 1, use = local >> 1;
+      const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
+      uint32_t* crow = row < c.m ? c.row(row) : nullptr;
 #pragma unroll 1
-    for (int cc = 0; cc < BN; cc += 8) {
-      uint32_t acc[NPOS][8];
+      for (int cc = 0; cc < BN; cc += 8) {
+        uint32_t acc[NPOS][8];
 #pragma unroll
-      for (int s = 0; s < NPOS; ++s) tmem_ld8(lane_base + (uint32_t)(s * BN + cc), acc[s]);
-      tmem_ld_wait();
-      if (crow) {
+        for (int s = 0; s < NPOS; ++s) tmem_ld8(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+        tmem_ld_wait();
+        if (crow) {
+          uint32_t cur[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const int col = n0 + cc + t;
-          if (col < c.n) {
-            uint32_t v = reduce64(acc[NPOS - 1][t], mp);
+          for (int t = 0; t < 8; ++t) cur[t] = (n0 + cc + t < c.n) ? crow[n0 + cc + t] : 0u;
 #pragma unroll
-            for (int s = NPOS - 2; s >= 0; --s) v = reduce64(((uint64_t)v << 8) + acc[s][t], mp);
-            crow[col] = submod(crow[col], v, mp);
+          for (int t = 0; t < 8; ++t) {
+            const int col = n0 + cc + t;
+            if (col < c.n) {
+              uint32_t v = reduce64(acc[NPOS - 1][t], mp);
+#pragma unroll
+              for (int s = NPOS - 2; s >= 0; --s) v = reduce64(((uint64_t)v << 8) + acc[s][t], mp);
+              crow[col] = submod(cur[t], v, mp);
+            }
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   tc_fence_before();
@@ -289,6 +322,17 @@ struct TcGemm {
     return (kp / TC_BK) * TC_BK;
   }
 
+  int sms = 0;
+  int num_sms() {
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    return sms;
+  }
+
   void release() {}
 
   bool load() {
@@ -320,7 +364,7 @@ struct TcGemm {
   }
 
   template <int L>
-  int launch(const View& c, const View& a, const View& b, const ModP& mp, cudaStream_t st) {
+  int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st) {
     constexpr int BN = TcCfg<L>::BN;
     const int m = c.m, n = c.n, k = a.n;
     const int m_pad = (m + TC_BM - 1) / TC_BM * TC_BM;
@@ -365,8 +409,8 @@ struct TcGemm {
         cudaFreeAsync(db, st);
         return kCuda;
       }
-      dim3 grid(n_pad / BN, m_pad / TC_BM);
-      tc_modgemm_kernel<L><<<grid, 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp);
+      const int tiles = (n_pad / BN) * (m_pad / TC_BM);
+      tc_modgemm_kernel<L><<<std::min(tiles, num_sms()), 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);
@@ -380,7 +424,7 @@ struct TcGemm {
     return kOk;
   }
 
-  int run(const View& c, const View& a, const View& b, const ModP& mp, cudaStream_t st) {
+  int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st) {
     if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
     if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
     if (!load()) return kUnsupported;

@@ -12,7 +12,7 @@ what = sys.argv[1] if len(sys.argv) > 1 else "all"
 if what in ("all", "batch"):
     batch = torch.from_numpy(orc.gen_cfg2(seed=0, batch=4096)).cuda().to(torch.int32)
     for th in (32, 64, 128, 256):
-        ctx.set_option("small_threads", th)
+        ctx.set_option("batch_threads", th)
         ts = []
         for it in range(4):
             x = batch.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
