@@ -284,6 +284,10 @@ __device__ int basecase_ff(const View x, int* psig, int* qsig, const BcScratch s
   __syncthreads();
   int r = 0, i = 0, j = 0;  // meaningful in warp 0
   unsigned long long c_mul = 0, c_add = 0, c_inv = 0, c_red = 0;
+  // update layout for n <= nt: C column lanes (power of two >= n) x R rows in flight
+  int C = 1;
+  while (C < n && C < nt) C <<= 1;
+  const int R = nt / C, tc = tid & (C - 1), tr = tid / C;
   while (true) {
     if (warp == 0) {
       __syncwarp();
@@ -368,44 +372,39 @@ __device__ int basecase_ff(const View x, int* psig, int* qsig, const BcScratch s
     const uint32_t a = A[pr * ld + pc];
     const uint32_t spr = S[pr];
     const uint32_t* __restrict__ prw = A + pr * ld;
-    const int items = (m - pr - 1) * n;
-    // snapshot the pivot column: a row may straddle two update chunks below
+    // snapshot the pivot column; afterwards every element is read and written by the
+    // same thread (only the snapshot, the untouched pivot row and the flags are shared)
     for (int rho = pr + 1 + tid; rho < m; rho += nt) bcol[rho] = prow[rho] ? 0u : A[rho * ld + pc];
     __syncthreads();
-    for (int base = 0; base < items; base += 4 * nt) {
-      uint32_t nv[4];
-      int where[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        where[k] = -1;
-        const int t = base + k * nt + tid;
-        if (t < items) {
-          const int rho = pr + 1 + t / n, g = t - (t / n) * n;
-          {
-            const uint32_t b = bcol[rho];
-            if (b) {
-              const uint32_t v = A[rho * ld + g];
-              uint32_t w;
-              if (g == pc) w = mulmod(b, spr, mp);
-              else if (g > pc && !pcol[g]) w = submod(mulmod(a, v, mp), mulmod(b, prw[g], mp), mp);
-              else w = mulmod(a, v, mp);
-              nv[k] = w;
-              where[k] = rho * n + g;
-            }
-          }
+    if (n <= nt) {
+      for (int rho = pr + 1 + tr; rho < m; rho += R) {
+        const uint32_t b = bcol[rho];
+        if (!b || tc >= n) continue;
+        uint32_t* row = A + rho * ld;
+        const int g = tc;
+        const uint32_t v = row[g];
+        uint32_t w;
+        if (g == pc) { w = mulmod(b, spr, mp); S[rho] = mulmod(S[rho], a, mp); }
+        else if (g > pc && !pcol[g]) w = submod(mulmod(a, v, mp), mulmod(b, prw[g], mp), mp);
+        else w = mulmod(a, v, mp);
+        row[g] = w;
+      }
+    } else {
+      for (int rho = pr + 1; rho < m; ++rho) {
+        const uint32_t b = bcol[rho];
+        if (!b) continue;
+        uint32_t* row = A + rho * ld;
+        for (int g = tid; g < n; g += nt) {
+          const uint32_t v = row[g];
+          uint32_t w;
+          if (g == pc) { w = mulmod(b, spr, mp); S[rho] = mulmod(S[rho], a, mp); }
+          else if (g > pc && !pcol[g]) w = submod(mulmod(a, v, mp), mulmod(b, prw[g], mp), mp);
+          else w = mulmod(a, v, mp);
+          row[g] = w;
         }
       }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (where[k] >= 0) {
-          const int rho = where[k] / n, g = where[k] - rho * n;
-          A[rho * ld + g] = nv[k];
-          if (g == pc) S[rho] = mulmod(S[rho], a, mp);
-        }
-      }
-      __syncthreads();
     }
+    __syncthreads();
     if (tid == 0) { prow[pr] = 1; pcol[pc] = 1; rord[r] = pr; cord[r] = pc; }
     ++r;
   }
@@ -420,10 +419,10 @@ __device__ int basecase_ff(const View x, int* psig, int* qsig, const BcScratch s
   }
   __syncthreads();
   const int rr = sh->r;
-  for (int t = tid; t < m * n; t += nt) {
-    const int rho = t / n, g = t - rho * n;
+  for (int rho = tid / C; rho < m; rho += R) {
     const uint32_t iv = S[rho];
-    if (iv != 1u) A[rho * ld + g] = mulmod(A[rho * ld + g], iv, mp);
+    if (iv == 1u) continue;
+    for (int g = tc; g < n; g += C) A[rho * ld + g] = mulmod(A[rho * ld + g], iv, mp);
   }
   // final positions: pivots first, then the non-pivots in original order
   for (int t = tid; t < rr; t += nt) { s.rowat[t] = rord[t]; s.colat[t] = cord[t]; }

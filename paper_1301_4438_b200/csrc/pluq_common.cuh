@@ -24,12 +24,14 @@ enum Status : int {
 
 struct ModP {
   uint32_t p;
+  uint32_t mu32;     // floor((2^32 - 1) / p) when p < 2^16 (32-bit Barrett), else 0
   uint64_t mu;       // floor((2^64 - 1) / p), Barrett constant
   uint64_t kchunk;   // max number of (p-1)^2 products summable in uint64 without overflow
 
   static ModP make(uint32_t p_) {
     ModP m;
     m.p = p_;
+    m.mu32 = p_ < 65536u ? 0xffffffffu / p_ : 0u;
     m.mu = ~0ull / p_;
     unsigned __int128 sq = (unsigned __int128)(p_ - 1) * (p_ - 1);
     m.kchunk = sq ? (uint64_t)(((unsigned __int128)~0ull - (unsigned __int128)(p_ - 1)) / sq) : ~0ull;
@@ -53,7 +55,21 @@ PLUQ_HD uint32_t reduce64(uint64_t x, const ModP m) {
   return (uint32_t)r;
 }
 
+// x mod p for x < 2^32 when p < 2^16: q = floor(x * mu32 / 2^32) is short by at most 2.
+PLUQ_HD uint32_t reduce32(uint32_t x, const ModP m) {
+#ifdef __CUDA_ARCH__
+  uint32_t q = __umulhi(x, m.mu32);
+#else
+  uint32_t q = (uint32_t)(((uint64_t)x * m.mu32) >> 32);
+#endif
+  uint32_t r = x - q * m.p;
+  r = r >= m.p ? r - m.p : r;
+  r = r >= m.p ? r - m.p : r;
+  return r;
+}
+
 PLUQ_HD uint32_t mulmod(uint32_t a, uint32_t b, const ModP m) {
+  if (m.mu32) return reduce32(a * b, m);  // a, b < p < 2^16: the product fits 32 bits
   return reduce64((uint64_t)a * b, m);
 }
 

@@ -80,10 +80,13 @@ struct pluq_ctx {
   unsigned long long* h_counts = nullptr;
   int* d_flag = nullptr;
   int* h_flag = nullptr;
+  int* d_zflags = nullptr;   // per-depth "node is nonzero" flags (deferred zero test)
+  int* h_zflags = nullptr;
+  static constexpr int kMaxDepth = 96;
   // options
   int64_t small_cap = 128 * 128;   // max m*n of a node factored whole by one CTA
   int64_t small_threads = 256;    // CTA size of a host-recursion leaf node
-  int64_t batch_threads = 32;     // CTA size of the batched kernel (one matrix per CTA)
+  int64_t batch_threads = 64;     // CTA size of the batched kernel (one matrix per CTA)
   int64_t use_tc = 1;
   int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
   int64_t tc_min_k = 32;
@@ -199,7 +202,7 @@ struct Ops {
     if (r == 0 || b.n == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_lower_unit_kernel<<<nb, 64, 0, c->stream>>>(l, inv, mp);
+    trinv_lower_unit_kernel<<<nb, 256, 0, c->stream>>>(l, inv, mp);
     c->check_launch();
     trsm_l_rec(l, b, inv);
     c->dfree(inv);
@@ -207,7 +210,7 @@ struct Ops {
   void trsm_l_rec(const View& l, const View& b, const uint32_t* inv) {
     const int r = l.m;
     if (r <= TR_BASE) {
-      trsm_apply_left_kernel<<<(b.n + 63) / 64, 256, 0, c->stream>>>(inv, b, mp);
+      trsm_apply_left_kernel<<<(b.n + 31) / 32, 128, 0, c->stream>>>(inv, b, mp);
       c->check_launch();
       return;
     }
@@ -223,7 +226,7 @@ struct Ops {
     if (r == 0 || b.m == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_upper_kernel<<<nb, 64, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p));
+    trinv_upper_kernel<<<nb, 256, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p));
     c->check_launch();
     trsm_u_rec(b, u, inv);
     c->dfree(inv);
@@ -231,7 +234,7 @@ struct Ops {
   void trsm_u_rec(const View& b, const View& u, const uint32_t* inv) {
     const int r = u.m;
     if (r <= TR_BASE) {
-      trsm_apply_right_kernel<<<(b.m + 63) / 64, 256, 0, c->stream>>>(b, inv, mp);
+      trsm_apply_right_kernel<<<(b.m + 31) / 32, 128, 0, c->stream>>>(b, inv, mp);
       c->check_launch();
       return;
     }
@@ -295,6 +298,14 @@ struct Ops {
     return *c->h_flag != 0;
   }
 
+  // Launch the zero test of x into d_zflags[slot] without waiting for it.
+  void nonzero_async(const View& x, int slot) {
+    CU(cudaMemsetAsync(c->d_zflags + slot, 0, sizeof(int), c->stream));
+    dim3 grid((unsigned)std::min<int64_t>(4, (x.n + 255) / 256), grid_rows(std::min<int64_t>(x.m, 4096)));
+    nonzero_kernel<<<grid, 256, 0, c->stream>>>(x, c->d_zflags + slot);
+    c->check_launch();
+  }
+
   void copy(const View& dst, const View& src) {
     if (dst.m == 0 || dst.n == 0) return;
     dim3 grid((dst.n + 255) / 256, grid_rows(dst.m));
@@ -321,9 +332,17 @@ struct Driver {
     return m * n <= c->small_cap && small_smem_bytes(m, n, threshold) <= 227 * 1024;
   }
 
+  int depth = 0;            // depth of the node being processed
+  int flagged_depth = -1;   // deepest ancestor slot with a zero test in flight
+  bool zero_known[pluq_ctx::kMaxDepth] = {};
+
   NodeRes readback(int m, int n) {
     CU(cudaMemcpyAsync(c->h_res, c->d_res, (size_t)(m + n + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (flagged_depth >= 0)
+      CU(cudaMemcpyAsync(c->h_zflags, c->d_zflags, (size_t)(flagged_depth + 1) * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+    for (int d = 0; d <= flagged_depth; ++d) zero_known[d] = c->h_zflags[d] == 0;
     NodeRes res;
     res.P.assign(c->h_res, c->h_res + m);
     res.Q.assign(c->h_res + m, c->h_res + m + n);
@@ -377,12 +396,30 @@ struct Driver {
     const bool base = m == 1 || n == 1 || std::min(m, n) <= threshold;
     if (fits_small(m, n)) return leaf_small(x);
     if (base) return leaf_global(x);
-    if (!ops.nonzero(x)) {
+    // Zero-block short-circuit without a dedicated sync: the test result travels back
+    // with the next leaf readback (inside A1's subtree).  Factoring A1 of a zero block
+    // is exact (identity, r=0, data untouched), so only the left spine is spent.
+    const int slot = depth;
+    const bool flag_here = slot < pluq_ctx::kMaxDepth;
+    if (flag_here) {
+      ops.nonzero_async(x, slot);
+      flagged_depth = std::max(flagged_depth, slot);
+      zero_known[slot] = false;
+    } else if (!ops.nonzero(x)) {
       ++c->st_zero_skips;
       return NodeRes{ident(m), ident(n), 0};
     }
     const int kr = m / 2, kc = n / 2;
+    ++depth;
     NodeRes A1 = rec(x.sub(0, 0, kr, kc));
+    --depth;
+    if (flag_here) {
+      flagged_depth = std::min(flagged_depth, slot - 1);
+      if (zero_known[slot]) {
+        ++c->st_zero_skips;
+        return NodeRes{ident(m), ident(n), 0};
+      }
+    }
     const int r1 = A1.r;
     ops.gather_rows(x.sub(0, kc, kr, n - kc), inverse(A1.P));
     ops.gather_cols(x.sub(kr, 0, m - kr, kc), A1.Q);
@@ -396,10 +433,12 @@ struct Driver {
     charge_mm(host_counts, m - kr, kc - r1, r1);
     charge_mm(host_counts, m - kr, n - kc, r1);
 
+    ++depth;
     NodeRes F = rec(x.sub(r1, kc, kr - r1, n - kc));
     const int r2 = F.r;
     NodeRes G = rec(x.sub(kr, r1, m - kr, kc - r1));
     const int r3 = G.r;
+    --depth;
     {
       Perm ip3 = inverse(G.P), ip2 = inverse(F.P);
       ops.gather_rows(x.sub(kr, kc, m - kr, n - kc), ip3);
@@ -436,7 +475,9 @@ struct Driver {
     charge_mm(host_counts, m4, n4, r2);
     charge_mm(host_counts, m4, n4, r3);
 
+    ++depth;
     NodeRes R = rec(x.sub(kr + r3, kc + r2, m4, n4));
+    --depth;
     const int r4 = R.r;
     ops.gather_rows(x.sub(kr + r3, 0, m4, kc + r2), inverse(R.P));
     ops.gather_cols(x.sub(0, kc + r2, kr + r3, n4), R.Q);
@@ -557,6 +598,8 @@ int pluq_create(pluq_ctx** out, int device, void* stream) {
     CU(cudaHostAlloc((void**)&c->h_counts, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_flag, sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault));
+    CU(cudaMalloc((void**)&c->d_zflags, pluq_ctx::kMaxDepth * sizeof(int)));
+    CU(cudaHostAlloc((void**)&c->h_zflags, pluq_ctx::kMaxDepth * sizeof(int), cudaHostAllocDefault));
     cudaMemPool_t pool;
     CU(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = ~0ull;
@@ -589,6 +632,8 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_invtab) cudaFree(c->d_invtab);
+  if (c->d_zflags) cudaFree(c->d_zflags);
+  if (c->h_zflags) cudaFreeHost(c->h_zflags);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   delete c;
   return kOk;
@@ -714,23 +759,70 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
   if (int v = validate(m, n, p)) return v;
   if (small_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
   return guarded(c, [&] {
-    const int64_t cnt = batch * m * n;
-    if (cnt == 0) return;
-    double* raw = c->dalloc<double>((size_t)cnt);
-    uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+    const int64_t mn = m * n;
+    if (batch == 0 || mn == 0) {
+      for (int64_t b = 0; b < batch; ++b) {
+        for (int64_t i = 0; i < m; ++i) psig[b * m + i] = i;
+        for (int64_t j = 0; j < n; ++j) qsig[b * n + j] = j;
+        ranks[b] = 0;
+      }
+      return;
+    }
+    // Chunked pipeline: H2D of chunk k+1, factorization of chunk k and D2H of chunk k-1
+    // overlap on three streams (two copy engines + compute).
+    const int64_t nchunks = std::min<int64_t>(8, batch);
+    const int64_t per = (batch + nchunks - 1) / nchunks;
+    double* raw = c->dalloc<double>((size_t)batch * mn);
+    uint32_t* dA = c->dalloc<uint32_t>((size_t)batch * mn);
     int32_t* dp = c->dalloc<int32_t>((size_t)(batch * (m + n + 1)));
-    CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
-    from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw, dA, cnt);
-    c->check_launch();
-    int st = pluq_factor_batched(c, dA, m * n, batch, m, n, p, threshold, dp, dp + batch * m,
-                                 dp + batch * (m + n), nullptr);
-    if (st != kOk) throw PluqError(st, c->err);
-    to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA, raw, cnt);
-    c->check_launch();
-    CU(cudaMemcpyAsync(hA, raw, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));  // allocations visible to the side streams
+    cudaStream_t sin, sout;
+    CU(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev_in(nchunks), ev_done(nchunks);
+    for (int64_t k = 0; k < nchunks; ++k) {
+      CU(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming));
+    }
+    const ModP mp = ModP::make((uint32_t)p);
+    SmallArgs a;
+    a.lda = n; a.bstride = mn; a.m = (int)m; a.n = (int)n;
+    a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
+    a.mp = mp; a.invtab = c->invtab((uint32_t)p);
+    unsigned long long* cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
+    a.cnt_accumulate = 0;
+    const size_t smem = small_smem_bytes(m, n, threshold);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int64_t k = 0; k < nchunks; ++k) {
+      const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
+      if (nb <= 0) break;
+      CU(cudaMemcpyAsync(raw + b0 * mn, hA + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyHostToDevice, sin));
+      CU(cudaEventRecord(ev_in[k], sin));
+      CU(cudaStreamWaitEvent(c->stream, ev_in[k], 0));
+      const int64_t cntk = nb * mn;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cntk + 255) / 256));
+      from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw + b0 * mn, dA + b0 * mn, cntk);
+      c->check_launch();
+      a.a = dA + b0 * mn;
+      a.p_out = dp + b0 * m; a.q_out = dp + batch * m + b0 * n; a.r_out = dp + batch * (m + n) + b0;
+      a.cnt_out = cnt + 4 * b0;
+      small_pluq_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, smem, c->stream>>>(a);
+      c->check_launch();
+      to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA + b0 * mn, raw + b0 * mn, cntk);
+      c->check_launch();
+      CU(cudaEventRecord(ev_done[k], c->stream));
+      CU(cudaStreamWaitEvent(sout, ev_done[k], 0));
+      CU(cudaMemcpyAsync(hA + b0 * mn, raw + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyDeviceToHost, sout));
+    }
     std::vector<int32_t> host((size_t)(batch * (m + n + 1)));
-    CU(cudaMemcpyAsync(host.data(), dp, host.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamWaitEvent(sout, ev_done[nchunks - 1], 0));
+    CU(cudaMemcpyAsync(host.data(), dp, host.size() * 4, cudaMemcpyDeviceToHost, sout));
+    CU(cudaStreamSynchronize(sout));
+    CU(cudaStreamSynchronize(c->stream));
+    for (int64_t k = 0; k < nchunks; ++k) { cudaEventDestroy(ev_in[k]); cudaEventDestroy(ev_done[k]); }
+    cudaStreamDestroy(sin);
+    cudaStreamDestroy(sout);
+    c->dfree(cnt);
     c->dfree(dp);
     c->dfree(dA);
     c->dfree(raw);

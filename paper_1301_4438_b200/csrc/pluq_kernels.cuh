@@ -30,9 +30,17 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
   uint32_t* sa = smem_dyn;
   int* stk = reinterpret_cast<int*>(sa + (((int64_t)m * lds + 3) & ~3ll));
-  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
-    int i = idx / n, j = idx - i * n;
-    sa[i * lds + j] = ga[(int64_t)i * args.lda + j];
+  {
+    // coalesced staging: warps over rows, lanes over columns, 4 rows in flight per warp
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (int i0 = 4 * w; i0 < m; i0 += 4 * nw)
+      for (int j = ln; j < n; j += 32) {
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = i0 + q < m ? ga[(int64_t)(i0 + q) * args.lda + j] : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) if (i0 + q < m) sa[(i0 + q) * lds + j] = v[q];
+      }
   }
   if (threadIdx.x == 0) { cnt.mul = cnt.add = cnt.inv = cnt.red = 0; }
   __syncthreads();
@@ -40,9 +48,10 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   View x{sa, lds, m, n};
   int* P = stk; int* Q = P + m; int* top = Q + n;
   const int r = rec_smem(x, P, Q, top, c);
-  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
-    int i = idx / n, j = idx - i * n;
-    ga[(int64_t)i * args.lda + j] = sa[i * lds + j];
+  {
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (int i = w; i < m; i += nw)
+      for (int j = ln; j < n; j += 32) ga[(int64_t)i * args.lda + j] = sa[i * lds + j];
   }
   int* po = args.p_out + (int64_t)blockIdx.x * m;
   int* qo = args.q_out + (int64_t)blockIdx.x * n;
@@ -143,15 +152,26 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(View c, View a, View b, 
     for (int j = 0; j < 4; ++j) acc[i][j] = 0;
   uint64_t since = 0;
   for (int k0 = 0; k0 < k; k0 += SG_BK) {
-    for (int idx = tid; idx < SG_BM * SG_BK; idx += 256) {
-      int i = idx / SG_BK, kk = idx % SG_BK;
-      int gi = m0 + i, gk = k0 + kk;
-      As[kk][i] = (gi < m && gk < k) ? a.at(gi, gk) : 0u;
-    }
-    for (int idx = tid; idx < SG_BK * SG_BN; idx += 256) {
-      int kk = idx / SG_BN, j = idx % SG_BN;
-      int gk = k0 + kk, gj = n0 + j;
-      Bs[kk][j] = (gk < k && gj < n) ? b.at(gk, gj) : 0u;
+    {
+      uint32_t va[8], vb[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + q * 256, i = idx / SG_BK, kk = idx % SG_BK;
+        const int gi = m0 + i, gk = k0 + kk;
+        va[q] = (gi < m && gk < k) ? a.at(gi, gk) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + q * 256, kk = idx / SG_BN, j = idx % SG_BN;
+        const int gk = k0 + kk, gj = n0 + j;
+        vb[q] = (gk < k && gj < n) ? b.at(gk, gj) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + q * 256;
+        As[idx % SG_BK][idx / SG_BK] = va[q];
+        Bs[idx / SG_BN][idx % SG_BN] = vb[q];
+      }
     }
     __syncthreads();
 #pragma unroll 8
@@ -222,106 +242,257 @@ __device__ __forceinline__ uint32_t acc_dot(const uint32_t* a, int sa, const uin
   return reduce64(acc, mp);
 }
 
-// out[b] = inverse of the b-th 64x64 diagonal block of U (upper, nonzero diagonal); 64 threads.
-__global__ void __launch_bounds__(64) trinv_upper_kernel(View u, uint32_t* out, ModP mp, const uint16_t* invtab) {
+// Blocked triangular inverse of one 64x64 diagonal block (padded with the identity
+// past w): 16x16 diagonal sub-blocks by substitution (thread per column), then two
+// merge levels  X12 = -X11 * U12 * X22  (upper)  /  X21 = -X22 * L21 * X11  (lower).
+// 256 threads; the serial chain is <= 16 substitution steps instead of 63.
+template <bool kUpper>
+__device__ void trinv_block(uint32_t (*M)[TR_BASE + 1], uint32_t (*X)[TR_BASE + 1], uint32_t (*T)[33],
+                            const uint32_t* dinv, const ModP mp) {
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < TR_BASE * TR_BASE; idx += blockDim.x) X[idx >> 6][idx & 63] = 0u;
+  __syncthreads();
+  if (tid < 64) {  // 4 sub-blocks x 16 columns
+    const int b0 = (tid >> 4) * 16, j = tid & 15;
+    if (kUpper) {
+      X[b0 + j][b0 + j] = dinv[b0 + j];
+      for (int i = j - 1; i >= 0; --i) {
+        uint64_t acc = 0;
+        for (int t = i + 1; t <= j; ++t) acc = acc + (uint64_t)M[b0 + i][b0 + t] * X[b0 + t][b0 + j];
+        const uint32_t s = reduce64(acc, mp);
+        X[b0 + i][b0 + j] = mulmod(s ? mp.p - s : 0u, dinv[b0 + i], mp);
+      }
+    } else {
+      X[b0 + j][b0 + j] = 1u;
+      for (int i = j + 1; i < 16; ++i) {
+        uint64_t acc = 0;
+        for (int t = j; t < i; ++t) acc = acc + (uint64_t)M[b0 + i][b0 + t] * X[b0 + t][b0 + j];
+        const uint32_t s = reduce64(acc, mp);
+        X[b0 + i][b0 + j] = s ? mp.p - s : 0u;
+      }
+    }
+  }
+  __syncthreads();
+  for (int h = 16; h < TR_BASE; h *= 2) {
+    // pairs of h x h blocks at offsets b0 (first) and b0 + h (second)
+    const int npairs = TR_BASE / (2 * h);
+    // T = M12 * X22 (upper)  or  T = M21 * X11 (lower), h x h per pair
+    for (int idx = tid; idx < npairs * h * h; idx += blockDim.x) {
+      const int pi = idx / (h * h), e = idx % (h * h), i = e / h, j = e % h;
+      const int b0 = pi * 2 * h;
+      uint64_t acc = 0;
+      if (kUpper)
+        for (int t = 0; t < h; ++t) acc += (uint64_t)M[b0 + i][b0 + h + t] * X[b0 + h + t][b0 + h + j];
+      else
+        for (int t = 0; t < h; ++t) acc += (uint64_t)M[b0 + h + i][b0 + t] * X[b0 + t][b0 + j];
+      T[pi * h + i][j] = reduce64(acc, mp);  // h <= 32, npairs*h <= 32
+    }
+    __syncthreads();
+    // X12 = -X11 * T (upper)  or  X21 = -X22 * T (lower)
+    for (int idx = tid; idx < npairs * h * h; idx += blockDim.x) {
+      const int pi = idx / (h * h), e = idx % (h * h), i = e / h, j = e % h;
+      const int b0 = pi * 2 * h;
+      uint64_t acc = 0;
+      if (kUpper)
+        for (int t = 0; t < h; ++t) acc += (uint64_t)X[b0 + i][b0 + t] * T[pi * h + t][j];
+      else
+        for (int t = 0; t < h; ++t) acc += (uint64_t)X[b0 + h + i][b0 + h + t] * T[pi * h + t][j];
+      const uint32_t s = reduce64(acc, mp);
+      if (kUpper) X[b0 + i][b0 + h + j] = s ? mp.p - s : 0u;
+      else X[b0 + h + i][b0 + j] = s ? mp.p - s : 0u;
+    }
+    __syncthreads();
+  }
+}
+
+// Products of <= 32 terms stay below 2^64 only when 32 (p-1)^2 < 2^64: p < 2^29.5.
+// Larger p (allow_large_modulus) fall back to per-product reduction via the slow path.
+__device__ __forceinline__ bool trinv_fast(const ModP mp) { return mp.kchunk >= 32; }
+
+template <bool kUpper>
+__device__ void trinv_block_slow(uint32_t (*M)[TR_BASE + 1], uint32_t (*X)[TR_BASE + 1], int w,
+                                 const uint32_t* dinv, const ModP mp) {
+  // column substitution with per-product reduction (rare: p > 2^29)
+  const int j = threadIdx.x;
+  if (j < TR_BASE) {
+    for (int i = 0; i < TR_BASE; ++i) X[i][j] = 0;
+    if (kUpper) {
+      X[j][j] = dinv[j];
+      for (int i = j - 1; i >= 0; --i) {
+        uint64_t acc = 0;
+        for (int t = i + 1; t <= j; ++t) acc = reduce64(acc + (uint64_t)M[i][t] * X[t][j], mp);
+        X[i][j] = mulmod(acc ? mp.p - (uint32_t)acc : 0u, dinv[i], mp);
+      }
+    } else {
+      X[j][j] = 1;
+      for (int i = j + 1; i < TR_BASE; ++i) {
+        uint64_t acc = 0;
+        for (int t = j; t < i; ++t) acc = reduce64(acc + (uint64_t)M[i][t] * X[t][j], mp);
+        X[i][j] = acc ? mp.p - (uint32_t)acc : 0u;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// out[b] = inverse of the b-th 64x64 diagonal block of U (upper, nonzero diagonal).
+__global__ void __launch_bounds__(256) trinv_upper_kernel(View u, uint32_t* out, ModP mp, const uint16_t* invtab) {
   __shared__ uint32_t Us[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
+  __shared__ uint32_t T[32][33];
   __shared__ uint32_t dinv[TR_BASE];
   const int base = blockIdx.x * TR_BASE;
   const int w = min(TR_BASE, u.m - base);
-  for (int idx = threadIdx.x; idx < w * w; idx += 64) {
-    int i = idx / w, j = idx % w;
-    Us[i][j] = u.at(base + i, base + j);
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < w) dinv[threadIdx.x] = invtab ? invtab[Us[threadIdx.x][threadIdx.x]] : invmod(Us[threadIdx.x][threadIdx.x], mp);
-  __syncthreads();
-  const int j = threadIdx.x;
-  if (j < w) {
-    for (int i = 0; i < w; ++i) X[i][j] = 0;
-    X[j][j] = dinv[j];
-    for (int i = j - 1; i >= 0; --i) {
-      uint32_t s = acc_dot(&Us[i][i + 1], 1, &X[i + 1][j], TR_BASE + 1, j - i, mp);
-      X[i][j] = mulmod(s ? mp.p - s : 0u, dinv[i], mp);
+  {
+    const int j = threadIdx.x & 63, i0 = threadIdx.x >> 6;  // 4 rows per pass
+    uint32_t v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = i0 + 4 * q;
+      v[q] = (i < w && j < w) ? u.at(base + i, base + j) : (i == j ? 1u : 0u);
     }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Us[i0 + 4 * q][j] = v[q];
   }
   __syncthreads();
+  if (threadIdx.x < TR_BASE) {
+    const uint32_t d = Us[threadIdx.x][threadIdx.x];
+    dinv[threadIdx.x] = invtab ? invtab[d] : invmod(d, mp);
+  }
+  __syncthreads();
+  if (trinv_fast(mp)) trinv_block<true>(Us, X, T, dinv, mp);
+  else trinv_block_slow<true>(Us, X, w, dinv, mp);
   uint32_t* o = out + (size_t)blockIdx.x * TR_BASE * TR_BASE;
-  for (int idx = threadIdx.x; idx < w * w; idx += 64) o[(idx / w) * TR_BASE + idx % w] = X[idx / w][idx % w];
+  for (int idx = threadIdx.x; idx < TR_BASE * TR_BASE; idx += blockDim.x) o[idx] = X[idx >> 6][idx & 63];
 }
 
-// out[b] = inverse of the b-th diagonal block of unit-lower L (diagonal implicit 1); 64 threads.
-__global__ void __launch_bounds__(64) trinv_lower_unit_kernel(View l, uint32_t* out, ModP mp) {
+// out[b] = inverse of the b-th diagonal block of unit-lower L (diagonal implicit 1).
+__global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t* out, ModP mp) {
   __shared__ uint32_t Ls[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
+  __shared__ uint32_t T[32][33];
+  __shared__ uint32_t dinv[TR_BASE];
   const int base = blockIdx.x * TR_BASE;
   const int w = min(TR_BASE, l.m - base);
-  for (int idx = threadIdx.x; idx < w * w; idx += 64) {
-    int i = idx / w, j = idx % w;
-    Ls[i][j] = l.at(base + i, base + j);
-  }
-  __syncthreads();
-  const int j = threadIdx.x;
-  if (j < w) {
-    for (int i = 0; i < w; ++i) X[i][j] = 0;
-    X[j][j] = 1;
-    for (int i = j + 1; i < w; ++i) {
-      uint32_t s = acc_dot(&Ls[i][j], 1, &X[j][j], TR_BASE + 1, i - j, mp);
-      X[i][j] = s ? mp.p - s : 0u;
+  {
+    const int j = threadIdx.x & 63, i0 = threadIdx.x >> 6;
+    uint32_t v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = i0 + 4 * q;
+      v[q] = (i < w && j < w && j < i) ? l.at(base + i, base + j) : (i == j ? 1u : 0u);
     }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Ls[i0 + 4 * q][j] = v[q];
   }
+  if (threadIdx.x < TR_BASE) dinv[threadIdx.x] = 1u;
   __syncthreads();
+  if (trinv_fast(mp)) trinv_block<false>(Ls, X, T, dinv, mp);
+  else trinv_block_slow<false>(Ls, X, w, dinv, mp);
   uint32_t* o = out + (size_t)blockIdx.x * TR_BASE * TR_BASE;
-  for (int idx = threadIdx.x; idx < w * w; idx += 64) o[(idx / w) * TR_BASE + idx % w] = X[idx / w][idx % w];
+  for (int idx = threadIdx.x; idx < TR_BASE * TR_BASE; idx += blockDim.x) o[idx] = X[idx >> 6][idx & 63];
 }
 
-// B <- B * Uinv for a w-column block (w <= 64): one CTA owns 64 rows of B (in place).
-__global__ void __launch_bounds__(256) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp) {
-  __shared__ uint32_t Bs[64][TR_BASE + 1];
-  __shared__ uint32_t Ui[TR_BASE][TR_BASE + 1];
-  const int w = b.n, r0 = blockIdx.x * 64, rows = min(64, b.m - r0);
-  for (int idx = threadIdx.x; idx < w * w; idx += 256) Ui[idx / w][idx % w] = uinv[(idx / w) * TR_BASE + idx % w];
-  for (int idx = threadIdx.x; idx < rows * w; idx += 256) Bs[idx / w][idx % w] = b.at(r0 + idx / w, idx % w);
-  __syncthreads();
-  const int rr = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 16;
-  uint32_t res[16];
+// B <- B * Uinv for a w-column block (w <= 64): one CTA owns 32 rows of B (in place);
+// 128 threads, each a 4x4 register tile (8 shared loads per 16 products).
+__global__ void __launch_bounds__(128) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp) {
+  __shared__ uint32_t Bs[32][TR_BASE + 4];
+  __shared__ uint32_t Ui[TR_BASE][TR_BASE + 4];
+  const int w = b.n, r0 = blockIdx.x * 32, rows = min(32, b.m - r0);
+  {
+    // all staging loads issued back to back (32 + 16 per thread), then stored
+    uint32_t u[32], bb[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int cc = c0 + q;
-    // X[rr][cc] = sum_{t<=cc} B[rr][t] Uinv[t][cc]
-    res[q] = (rr < rows && cc < w) ? acc_dot(&Bs[rr][0], 1, &Ui[0][cc], TR_BASE + 1, cc + 1, mp) : 0u;
+    for (int q = 0; q < 32; ++q) {
+      const int idx = threadIdx.x + q * 128, i = idx >> 6, j = idx & 63;
+      u[q] = (i < w && j < w) ? __ldg(uinv + i * TR_BASE + j) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = (threadIdx.x >> 5) + 4 * (q >> 1), j = (threadIdx.x & 31) + 32 * (q & 1);
+      bb[q] = (i < rows && j < w) ? b.at(r0 + i, j) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = threadIdx.x + q * 128;
+      Ui[idx >> 6][idx & 63] = u[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Bs[(threadIdx.x >> 5) + 4 * (q >> 1)][(threadIdx.x & 31) + 32 * (q & 1)] = bb[q];
   }
   __syncthreads();
-  if (rr < rows)
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;  // rows 4*ty.., cols 4*tx..
+  uint64_t acc[4][4] = {};
+  const bool fast = mp.kchunk >= TR_BASE;
+  for (int t = 0; t < w; ++t) {
+    uint32_t av[4], bv[4];
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
-      if (c0 + q < w) b.at(r0 + rr, c0 + q) = res[q];
+    for (int q = 0; q < 4; ++q) { av[q] = Bs[4 * ty + q][t]; bv[q] = Ui[t][4 * tx + q]; }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        acc[x][y] += (uint64_t)av[x] * bv[y];
+        if (!fast) acc[x][y] = reduce64(acc[x][y], mp);
+      }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int rr = 4 * ty + x, cc = 4 * tx + y;
+      if (rr < rows && cc < w) b.at(r0 + rr, cc) = reduce64(acc[x][y], mp);
+    }
 }
 
-// B <- Linv * B for a w-row block (w <= 64): one CTA owns 64 columns of B (in place).
-__global__ void __launch_bounds__(256) trsm_apply_left_kernel(const uint32_t* linv, View b, ModP mp) {
-  __shared__ uint32_t Bs[TR_BASE][64 + 1];
-  __shared__ uint32_t Li[TR_BASE][TR_BASE + 1];
-  const int w = b.m, c0 = blockIdx.x * 64, cols = min(64, b.n - c0);
-  for (int idx = threadIdx.x; idx < w * w; idx += 256) Li[idx / w][idx % w] = linv[(idx / w) * TR_BASE + idx % w];
-  for (int idx = threadIdx.x; idx < w * 64; idx += 256) {
-    int i = idx / 64, j = idx % 64;
-    Bs[i][j] = j < cols ? b.at(i, c0 + j) : 0u;
+// B <- Linv * B for a w-row block (w <= 64): one CTA owns 32 columns of B (in place).
+__global__ void __launch_bounds__(128) trsm_apply_left_kernel(const uint32_t* linv, View b, ModP mp) {
+  __shared__ uint32_t Bs[TR_BASE][32 + 4];
+  __shared__ uint32_t Li[TR_BASE][TR_BASE + 4];
+  const int w = b.m, c0 = blockIdx.x * 32, cols = min(32, b.n - c0);
+  {
+    uint32_t u[32], bb[16];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = threadIdx.x + q * 128, i = idx >> 6, j = idx & 63;
+      u[q] = (i < w && j < w) ? __ldg(linv + i * TR_BASE + j) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = (threadIdx.x >> 5) + 4 * q, j = threadIdx.x & 31;
+      bb[q] = (i < w && j < cols) ? b.at(i, c0 + j) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = threadIdx.x + q * 128;
+      Li[idx >> 6][idx & 63] = u[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Bs[(threadIdx.x >> 5) + 4 * q][threadIdx.x & 31] = bb[q];
   }
   __syncthreads();
-  const int cc = threadIdx.x & 63, r0 = (threadIdx.x >> 6) * 16;
-  uint32_t res[16];
+  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;  // rows 4*ty.. (64), cols 4*tx.. (32)
+  uint64_t acc[4][4] = {};
+  const bool fast = mp.kchunk >= TR_BASE;
+  for (int t = 0; t < w; ++t) {
+    uint32_t av[4], bv[4];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int rr = r0 + q;
-    // X[rr][cc] = sum_{t<=rr} Linv[rr][t] B[t][cc]
-    res[q] = (rr < w && cc < cols) ? acc_dot(&Li[rr][0], 1, &Bs[0][cc], 65, rr + 1, mp) : 0u;
+    for (int q = 0; q < 4; ++q) { av[q] = Li[4 * ty + q][t]; bv[q] = Bs[t][4 * tx + q]; }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        acc[x][y] += (uint64_t)av[x] * bv[y];
+        if (!fast) acc[x][y] = reduce64(acc[x][y], mp);
+      }
   }
-  __syncthreads();
-  if (cc < cols)
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
-      if (r0 + q < w) b.at(r0 + q, c0 + cc) = res[q];
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int rr = 4 * ty + x, cc = 4 * tx + y;
+      if (rr < w && cc < cols) b.at(rr, c0 + cc) = reduce64(acc[x][y], mp);
+    }
 }
 
 // flag <- 1 if any diagonal entry of U is zero (kernels.py:93-95).

@@ -96,25 +96,32 @@ __device__ void cta_gather_cols(const View v, const int* g, int* scratch, BcShar
   __syncthreads();
 }
 
-// C <- C - A B mod p (kernels.py:38-55), outputs spread over the CTA.
+// C <- C - A B mod p (kernels.py:38-55), outputs spread over the CTA
+// (C column lanes x R row lanes, no integer division in the index math).
 __device__ void cta_mm_sub(const View c, const View a, const View b, const ModP mp) {
   const int m = c.m, n = c.n, k = a.n;
   if (m == 0 || n == 0 || k == 0) return;
+  const int nt = blockDim.x;
+  int C = 1;
+  while (C < n && C < nt) C <<= 1;
+  const int R = nt / C, tc = threadIdx.x & (C - 1), tr = threadIdx.x / C;
   const bool fast = (uint64_t)k <= mp.kchunk;
-  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
-    int i = idx / n, j = idx - i * n;
+  for (int i = tr; i < m; i += R) {
     const uint32_t* ar = a.row(i);
-    uint64_t acc = 0;
-    if (fast) {
-      for (int t = 0; t < k; ++t) acc += (uint64_t)ar[t] * b.at(t, j);
-    } else {
-      uint64_t cntk = 0;
-      for (int t = 0; t < k; ++t) {
-        acc += (uint64_t)ar[t] * b.at(t, j);
-        if (++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+    uint32_t* cr = c.row(i);
+    for (int j = tc; j < n; j += C) {
+      uint64_t acc = 0;
+      if (fast) {
+        for (int t = 0; t < k; ++t) acc += (uint64_t)ar[t] * b.at(t, j);
+      } else {
+        uint64_t cntk = 0;
+        for (int t = 0; t < k; ++t) {
+          acc += (uint64_t)ar[t] * b.at(t, j);
+          if (++cntk == mp.kchunk) { acc = reduce64(acc, mp); cntk = 0; }
+        }
       }
+      cr[j] = submod(cr[j], reduce64(acc, mp), mp);
     }
-    c.at(i, j) = submod(c.at(i, j), reduce64(acc, mp), mp);
   }
   __syncthreads();
 }
