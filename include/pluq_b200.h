@@ -109,6 +109,10 @@ int pluq_modgemm_sub_tc(pluq_ctx* ctx, uint32_t* dC, int64_t ldc, const uint32_t
                         int64_t lda, const uint32_t* dB, int64_t ldb, int64_t m, int64_t n,
                         int64_t k, int64_t p);
 
+/* OpCounts the reference charges on an m x n matrix with a GENERIC rank profile of rank
+ * `rank` (leading principal minors 1..rank nonzero), where P = Q = I.  Host-only. */
+int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, int64_t* counts);
+
 /* Device-side statistics of the last pluq_factor call (kernel launches, host syncs,
  * nodes, tensor-core GEMM launches and their summed device time in ms). */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);

@@ -28,6 +28,7 @@ SIGNATURES = {
     "pluq_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i64]),
     "pluq_last_error": (ctypes.c_char_p, [_p]),
     "pluq_last_stats": (ctypes.c_int, [_p, _pi64, _i64]),
+    "pluq_generic_counts": (ctypes.c_int, [_i64, _i64, _i64, _i64, _pi64]),
     "pluq_factor": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_iterative": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_batched": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p]),
@@ -115,10 +116,10 @@ class Context:
         raise_for(self.lib.pluq_set_option(self.handle, key.encode(), int(value)), self, f"option {key}")
 
     def stats(self) -> dict:
-        buf = (ctypes.c_int64 * 8)()
-        self.lib.pluq_last_stats(self.handle, buf, 8)
+        buf = (ctypes.c_int64 * 9)()
+        self.lib.pluq_last_stats(self.handle, buf, 9)
         keys = ["launches", "host_syncs", "nodes", "small_node_kernels", "basecase_kernels",
-                "tc_gemms", "simt_gemms", "zero_skips"]
+                "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves"]
         return dict(zip(keys, list(buf)))
 
     def __del__(self):

@@ -363,6 +363,8 @@ __device__ int basecase_ff(const View x, int* psig, int* qsig, const BcScratch s
           c_mul += br; c_add += br; c_red += br;
         }
       }
+      if (pr >= 0)  // snapshot of the pivot column (rows straddling update chunks read it)
+        for (int rho = pr + 1 + lane; rho < m; rho += 32) bcol[rho] = prow[rho] ? 0u : A[rho * ld + pc];
       if (lane == 0) { sh->pr = pr; sh->pc = pc; }
     }
     __syncthreads();
@@ -372,10 +374,8 @@ __device__ int basecase_ff(const View x, int* psig, int* qsig, const BcScratch s
     const uint32_t a = A[pr * ld + pc];
     const uint32_t spr = S[pr];
     const uint32_t* __restrict__ prw = A + pr * ld;
-    // snapshot the pivot column; afterwards every element is read and written by the
-    // same thread (only the snapshot, the untouched pivot row and the flags are shared)
-    for (int rho = pr + 1 + tid; rho < m; rho += nt) bcol[rho] = prow[rho] ? 0u : A[rho * ld + pc];
-    __syncthreads();
+    // every element is read and written by the same thread (only the bcol snapshot, the
+    // untouched pivot row and the flags are shared), so no read/write phase split
     if (n <= nt) {
       for (int rho = pr + 1 + tr; rho < m; rho += R) {
         const uint32_t b = bcol[rho];

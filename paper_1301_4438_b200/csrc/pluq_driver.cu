@@ -90,9 +90,10 @@ struct pluq_ctx {
   int64_t use_tc = 1;
   int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
   int64_t tc_min_k = 32;
+  int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
-          st_simt = 0, st_zero_skips = 0;
+          st_simt = 0, st_zero_skips = 0, st_generic = 0;
   TcGemm tc;
   uint16_t* d_invtab = nullptr;  // inverse table for invtab_p (p < 2^16)
   uint32_t invtab_p = 0;
@@ -109,7 +110,7 @@ struct pluq_ctx {
     return d_invtab;
   }
 
-  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = 0; }
+  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = 0; }
 
   void sync() {
     CU(cudaStreamSynchronize(stream));
@@ -314,6 +315,63 @@ struct Ops {
   }
 };
 
+// OpCounts of the reference recursion on a matrix with a GENERIC rank profile (leading
+// principal minors of orders 1..rho nonzero, Schur complement after rho pivots zero).
+// On such inputs every node is again generic with rank min(rows, cols, remaining
+// rank), pivots sit on the diagonal and P = Q = I, so the reference's charges
+// (kernels.py:1-16, iterative.py:63-75) are a function of (m, n, rho, threshold).
+static void generic_counts_rec(int64_t m, int64_t n, int64_t rho, int64_t thr, Counts& c) {
+  if (m == 0 || n == 0) return;
+  const int64_t rr = std::min(std::min(m, n), rho);
+  if (m == 1 || n == 1 || std::min(m, n) <= thr) {
+    for (int64_t t = 0; t < rr; ++t) {
+      const long long below = m - 1 - t, right = n - 1 - t;
+      if (below > 0) {
+        c.inv += 1; c.mul += below; c.red += below;
+        if (right > 0) { c.mul += below * right; c.add += below * right; c.red += below * right; }
+      }
+    }
+    return;
+  }
+  const int64_t kr = m / 2, kc = n / 2;
+  const int64_t r1 = std::min(std::min(kr, kc), rho);
+  generic_counts_rec(kr, kc, rho, thr, c);
+  charge_trsm_l(c, r1, n - kc);
+  charge_trsm_u(c, m - kr, r1);
+  charge_mm(c, kr - r1, n - kc, r1);
+  charge_mm(c, m - kr, kc - r1, r1);
+  charge_mm(c, m - kr, n - kc, r1);
+  const int64_t r2 = std::min(std::min(kr - r1, n - kc), rho - r1);
+  generic_counts_rec(kr - r1, n - kc, rho - r1, thr, c);
+  const int64_t r3 = std::min(std::min(m - kr, kc - r1), rho - r1 - r2);
+  generic_counts_rec(m - kr, kc - r1, rho - r1 - r2, thr, c);
+  const int64_t m4 = m - kr - r3, n4 = n - kc - r2;
+  charge_trsm_u(c, r3, r2);
+  charge_trsm_l(c, r3, r2);
+  charge_trsm_u(c, m4, r2);
+  charge_trsm_l(c, r3, n4);
+  charge_mm(c, r3, n4, r2);
+  charge_mm(c, m4, n4, r2);
+  charge_mm(c, m4, n4, r3);
+  generic_counts_rec(m4, n4, rho - r1 - r2 - r3, thr, c);
+}
+
+
+// Per-rank table of generic-profile charges, uploaded for the batched kernel.
+static unsigned long long* upload_generic_counts(pluq_ctx* c, int64_t m, int64_t n, int64_t thr) {
+  const int64_t mn = std::min(m, n);
+  std::vector<unsigned long long> tab((size_t)(mn + 1) * 4);
+  for (int64_t r = 0; r <= mn; ++r) {
+    Counts g{0, 0, 0, 0};
+    generic_counts_rec(m, n, r, thr, g);
+    tab[4 * r] = g.mul; tab[4 * r + 1] = g.add; tab[4 * r + 2] = g.inv; tab[4 * r + 3] = g.red;
+  }
+  unsigned long long* dt = c->dalloc<unsigned long long>(tab.size());
+  void* h = c->stage(tab.data(), tab.size() * sizeof(unsigned long long));
+  CU(cudaMemcpyAsync(dt, h, tab.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+  return dt;
+}
+
 struct NodeRes {
   Perm P, Q;
   int r;
@@ -336,8 +394,8 @@ struct Driver {
   int flagged_depth = -1;   // deepest ancestor slot with a zero test in flight
   bool zero_known[pluq_ctx::kMaxDepth] = {};
 
-  NodeRes readback(int m, int n) {
-    CU(cudaMemcpyAsync(c->h_res, c->d_res, (size_t)(m + n + 1) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  NodeRes readback(int m, int n, int extra = 0) {
+    CU(cudaMemcpyAsync(c->h_res, c->d_res, (size_t)(m + n + 1 + extra) * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (flagged_depth >= 0)
       CU(cudaMemcpyAsync(c->h_zflags, c->d_zflags, (size_t)(flagged_depth + 1) * sizeof(int),
                          cudaMemcpyDeviceToHost, c->stream));
@@ -351,18 +409,26 @@ struct Driver {
   }
 
   NodeRes leaf_small(const View& x) {
-    c->ensure_res((size_t)x.m + x.n + 1);
+    c->ensure_res((size_t)x.m + x.n + 2);
     SmallArgs a;
     a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
     a.p_out = c->d_res; a.q_out = c->d_res + x.m; a.r_out = c->d_res + x.m + x.n;
     a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
     a.invtab = c->invtab(mp.p);
+    a.try_generic = (int)c->try_generic;
+    a.generic_counts = nullptr;           // charged on the host from the readback below
+    a.generic_flag = c->d_res + x.m + x.n + 1;
     size_t smem = small_smem_bytes(x.m, x.n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
     c->check_launch();
     ++c->st_small;
-    return readback(x.m, x.n);
+    NodeRes res = readback(x.m, x.n, 1);
+    if (a.try_generic && c->h_res[x.m + x.n + 1]) {  // generic leaf: charges in closed form
+      generic_counts_rec(x.m, x.n, res.r, threshold, host_counts);
+      ++c->st_generic;
+    }
+    return res;
   }
 
   NodeRes leaf_global(const View& x) {
@@ -655,16 +721,25 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_min_dim") c->tc_min_dim = value;
   else if (k == "tc_min_k") c->tc_min_k = value;
   else if (k == "tc_k_pass") c->tc.k_pass_override = value;
+  else if (k == "try_generic") c->try_generic = value;
   else return kInvalid;
   return kOk;
 }
 
 const char* pluq_last_error(pluq_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, int64_t* counts) {
+  if (m < 0 || n < 0 || rank < 0 || rank > std::min(m, n) || threshold < 1 || !counts) return kInvalid;
+  Counts c{0, 0, 0, 0};
+  generic_counts_rec(m, n, rank, threshold, c);
+  counts[0] = (int64_t)c.mul; counts[1] = (int64_t)c.add; counts[2] = (int64_t)c.inv; counts[3] = (int64_t)c.red;
+  return kOk;
+}
+
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[8] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt, c->st_zero_skips};
-  for (int64_t i = 0; i < nout && i < 8; ++i) out[i] = v[i];
+  int64_t v[9] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt, c->st_zero_skips, c->st_generic};
+  for (int64_t i = 0; i < nout && i < 9; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -704,6 +779,11 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     if (!cnt) cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
     a.cnt_out = cnt; a.cnt_accumulate = 0;
     a.invtab = c->invtab((uint32_t)p);
+    a.try_generic = (int)c->try_generic;
+    a.generic_flag = nullptr;
+    unsigned long long* gtab = nullptr;
+    if (a.try_generic) gtab = upload_generic_counts(c, m, n, threshold);
+    a.generic_counts = gtab;
     size_t smem = small_smem_bytes(m, n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int64_t b0 = 0; b0 < batch; b0 += 2147483647ll) {
@@ -711,6 +791,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       c->check_launch();
     }
     if (!d_counts) c->dfree(cnt);
+    if (gtab) c->dfree(gtab);
   });
 }
 
@@ -789,6 +870,10 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     a.lda = n; a.bstride = mn; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
     a.mp = mp; a.invtab = c->invtab((uint32_t)p);
+    a.try_generic = (int)c->try_generic;
+    a.generic_flag = nullptr;
+    unsigned long long* gtab = a.try_generic ? upload_generic_counts(c, m, n, threshold) : nullptr;
+    a.generic_counts = gtab;
     unsigned long long* cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
     a.cnt_accumulate = 0;
     const size_t smem = small_smem_bytes(m, n, threshold);
@@ -823,6 +908,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     cudaStreamDestroy(sin);
     cudaStreamDestroy(sout);
     c->dfree(cnt);
+    if (gtab) c->dfree(gtab);
     c->dfree(dp);
     c->dfree(dA);
     c->dfree(raw);

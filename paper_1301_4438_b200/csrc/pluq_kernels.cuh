@@ -19,6 +19,9 @@ struct SmallArgs {
   unsigned long long* cnt_out;  // batch x 4 (or 4 if cnt_accumulate)
   int cnt_accumulate;
   const uint16_t* invtab;       // inverse table when p < 2^16 (else nullptr)
+  int try_generic;              // attempt the no-pivot generic-profile path first
+  const unsigned long long* generic_counts;  // (min(m,n)+1) x 4 charges by rank, or nullptr
+  int* generic_flag;            // per block: 1 if the generic path produced the result (or nullptr)
 };
 
 __global__ void small_pluq_kernel(SmallArgs args) {
@@ -47,7 +50,26 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   SmallCtx c{args.mp, args.threshold, &cnt, &sh, args.invtab};
   View x{sa, lds, m, n};
   int* P = stk; int* Q = P + m; int* top = Q + n;
-  const int r = rec_smem(x, P, Q, top, c);
+  int r = -1;
+  if (args.try_generic) {
+    r = crout_generic(x, args.mp, args.invtab, &sh);
+    if (r >= 0) {
+      for (int t = threadIdx.x; t < m; t += blockDim.x) P[t] = t;
+      for (int t = threadIdx.x; t < n; t += blockDim.x) Q[t] = t;
+      if (threadIdx.x == 0 && args.generic_counts) {
+        const unsigned long long* g = args.generic_counts + 4 * r;
+        cnt.mul = g[0]; cnt.add = g[1]; cnt.inv = g[2]; cnt.red = g[3];
+      }
+    } else {
+      // not generic: restore the block from global memory and run the exact recursion
+      const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      for (int i = w; i < m; i += nw)
+        for (int j = ln; j < n; j += 32) sa[i * lds + j] = ga[(int64_t)i * args.lda + j];
+      __syncthreads();
+    }
+  }
+  if (args.generic_flag && threadIdx.x == 0) args.generic_flag[blockIdx.x] = r >= 0;
+  if (r < 0) r = rec_smem(x, P, Q, top, c);
   {
     const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     for (int i = w; i < m; i += nw)
