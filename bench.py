@@ -274,18 +274,10 @@ def main():
             e2e_t.append(time.perf_counter() - t0)
         w_e2e = float(sum(work(M, N, int(r)) for r in r2.ranks))
 
-    t_dev = sum(step_ms) / 1e3
-    t_e2e = sum(e2e_t)
-    if world > 1:
-        v = torch.tensor([t_dev, t_e2e, w_step, w_e2e], dtype=torch.float64, device=dev)
-        tmax = v[:2].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        wsum = v[2:].clone()
-        dist.all_reduce(wsum, op=dist.ReduceOp.SUM)
-        t_dev, t_e2e = float(tmax[0]), float(tmax[1])
-        w_all, w_e2e_all = float(wsum[0]), float(wsum[1])
-    else:
-        w_all, w_e2e_all = w_step, w_e2e
+    from paper_1301_4438_b200.sharding import reduce_timing
+
+    t_dev, w_all = reduce_timing(sum(step_ms) / 1e3, w_step, dev)        # max time, summed work
+    t_e2e, w_e2e_all = reduce_timing(sum(e2e_t), w_e2e, dev)
     value = w_all * args.steps / t_dev / 1e9
     e2e_value = w_e2e_all * len(e2e_t) / t_e2e / 1e9
 

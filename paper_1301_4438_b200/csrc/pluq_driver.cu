@@ -80,20 +80,25 @@ struct pluq_ctx {
   unsigned long long* h_counts = nullptr;
   int* d_flag = nullptr;
   int* h_flag = nullptr;
+  int* d_stop = nullptr;     // [stop, k0, t] of the speculative no-pivot path
+  int* h_stop = nullptr;
+  int64_t spec_block = 128;  // panel width of the speculative blocked LU
+  int64_t spec_check = 16;   // host checks the stop flag every this many panels
+  int64_t spec_panel = 1024; // outer panel width of the two-level speculative LU
   int* d_zflags = nullptr;   // per-depth "node is nonzero" flags (deferred zero test)
   int* h_zflags = nullptr;
   static constexpr int kMaxDepth = 96;
   // options
   int64_t small_cap = 128 * 128;   // max m*n of a node factored whole by one CTA
   int64_t small_threads = 256;    // CTA size of a host-recursion leaf node
-  int64_t batch_threads = 64;     // CTA size of the batched kernel (one matrix per CTA)
+  int64_t batch_threads = 128;    // CTA size of the batched kernels (one matrix per CTA)
   int64_t use_tc = 1;
   int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
   int64_t tc_min_k = 32;
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
-          st_simt = 0, st_zero_skips = 0, st_generic = 0;
+          st_simt = 0, st_zero_skips = 0, st_generic = 0, st_spec_ok = 0, st_spec_fail = 0;
   TcGemm tc;
   uint16_t* d_invtab = nullptr;  // inverse table for invtab_p (p < 2^16)
   uint32_t invtab_p = 0;
@@ -110,7 +115,7 @@ struct pluq_ctx {
     return d_invtab;
   }
 
-  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = 0; }
+  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok = st_spec_fail = 0; }
 
   void sync() {
     CU(cudaStreamSynchronize(stream));
@@ -166,12 +171,13 @@ inline int grid_rows(int64_t rows) { return (int)std::max<int64_t>(1, std::min<i
 struct Ops {
   pluq_ctx* c;
   ModP mp;
+  const int* stop = nullptr;  // device stop flag of the speculative path (nullptr: none)
 
   // ---- modular GEMM: C <- C - A B  (kernels.py:38-55) ------------------------------
   void gemm(const View& cv, const View& av, const View& bv) {
     if (cv.m == 0 || cv.n == 0 || av.n == 0) return;
     if (c->use_tc && cv.m >= c->tc_min_dim && cv.n >= c->tc_min_dim && av.n >= c->tc_min_k) {
-      int st = c->tc.run(cv, av, bv, mp, c->stream);
+      int st = c->tc.run(cv, av, bv, mp, c->stream, stop);
       if (st == kOk) { ++c->st_tc; c->st_launch += 3; return; }
       if (st != kUnsupported) throw PluqError(st, "tensor-core GEMM failed: " + c->tc.last_error);
     }
@@ -184,9 +190,9 @@ struct Ops {
       return;
     }
     if (mp.kchunk < 2 * SG_BK)
-      simt_gemm_kernel<true><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp);
+      simt_gemm_kernel<true><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp, stop);
     else
-      simt_gemm_kernel<false><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp);
+      simt_gemm_kernel<false><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp, stop);
     ++c->st_simt;
     c->check_launch();
   }
@@ -203,7 +209,7 @@ struct Ops {
     if (r == 0 || b.n == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_lower_unit_kernel<<<nb, 256, 0, c->stream>>>(l, inv, mp);
+    trinv_lower_unit_kernel<<<nb, 256, 0, c->stream>>>(l, inv, mp, stop);
     c->check_launch();
     trsm_l_rec(l, b, inv);
     c->dfree(inv);
@@ -211,7 +217,7 @@ struct Ops {
   void trsm_l_rec(const View& l, const View& b, const uint32_t* inv) {
     const int r = l.m;
     if (r <= TR_BASE) {
-      trsm_apply_left_kernel<<<(b.n + 31) / 32, 128, 0, c->stream>>>(inv, b, mp);
+      trsm_apply_left_kernel<<<(b.n + 31) / 32, 128, 0, c->stream>>>(inv, b, mp, stop);
       c->check_launch();
       return;
     }
@@ -227,7 +233,7 @@ struct Ops {
     if (r == 0 || b.m == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_upper_kernel<<<nb, 256, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p));
+    trinv_upper_kernel<<<nb, 256, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p), stop);
     c->check_launch();
     trsm_u_rec(b, u, inv);
     c->dfree(inv);
@@ -235,7 +241,7 @@ struct Ops {
   void trsm_u_rec(const View& b, const View& u, const uint32_t* inv) {
     const int r = u.m;
     if (r <= TR_BASE) {
-      trsm_apply_right_kernel<<<(b.m + 31) / 32, 128, 0, c->stream>>>(b, inv, mp);
+      trsm_apply_right_kernel<<<(b.m + 31) / 32, 128, 0, c->stream>>>(b, inv, mp, stop);
       c->check_launch();
       return;
     }
@@ -417,7 +423,13 @@ struct Driver {
     a.invtab = c->invtab(mp.p);
     a.try_generic = (int)c->try_generic;
     a.generic_counts = nullptr;           // charged on the host from the readback below
-    a.generic_flag = c->d_res + x.m + x.n + 1;
+    a.generic_flag = a.try_generic ? c->d_res + x.m + x.n + 1 : nullptr;
+    if (a.try_generic) {
+      const size_t cs = crout_smem_bytes(x.m, x.n);
+      CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+      crout_fast_kernel<<<1, (unsigned)c->small_threads, cs, c->stream>>>(a);
+      c->check_launch();
+    }
     size_t smem = small_smem_bytes(x.m, x.n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
@@ -455,6 +467,90 @@ struct Driver {
     return readback(m, n);
   }
 
+  // ---- speculative no-pivot LU of a whole node (generic rank profile) ----------------
+  // Blocked right-looking LU with Crout diagonal blocks, fully asynchronous under the
+  // device stop flag.  Success conditions are exactly those of crout_generic (pinned
+  // against the oracle): no zero pivot, or a first zero pivot at global g after which
+  // the whole Schur complement is zero (rank g).  On success P = Q = I and the node
+  // holds the unique factors; otherwise the node is restored and the caller recurses.
+  bool speculative_lu(const View& x, int& rank) {
+    const int m = x.m, n = x.n, mn = std::min(m, n);
+    const int BS = (int)c->spec_block;
+    const int W = std::max(BS, (int)(c->spec_panel / BS) * BS);
+    uint32_t* backup = c->dalloc<uint32_t>((size_t)m * n);
+    View bk{backup, n, m, n};
+    ops.copy(bk, x);
+    CU(cudaMemsetAsync(c->d_stop, 0, 4 * sizeof(int), c->stream));
+    Ops sops = ops;
+    sops.stop = c->d_stop;
+    const uint16_t* itab = c->invtab(mp.p);
+    const size_t dsm = diag_fast_smem(BS, itab != nullptr);
+    CU(cudaFuncSetAttribute(diag_crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    bool stopped_early = false;
+    int blk = 0;
+    for (int ps = 0; ps < mn && !stopped_early; ps += W) {
+      const int pe = std::min(ps + W, mn);
+      // inner right-looking LU of the panel columns [ps, pe)
+      for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
+        const int bs = std::min(BS, pe - k0);
+        diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
+                                                            c->d_stop + 1, k0);
+        c->check_launch();
+        const View b11 = x.sub(k0, k0, bs, bs);
+        sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                       // L21
+        sops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                      // U12 (panel)
+        sops.gemm(x.sub(k0 + bs, k0 + bs, m - k0 - bs, pe - k0 - bs), x.sub(k0 + bs, k0, m - k0 - bs, bs),
+                  x.sub(k0, k0 + bs, bs, pe - k0 - bs));
+        if (blk == 0 || (blk + 1) % c->spec_check == 0) {  // abort early on non-generic input
+          CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+          c->sync();
+          if (c->h_stop[0]) { stopped_early = true; break; }
+        }
+      }
+      if (stopped_early) break;
+      // outer step: U rows [ps, pe) right of the panel, then the K = W trailing update
+      const View l11 = x.sub(ps, ps, pe - ps, pe - ps);
+      sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+      sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, n - pe));
+    }
+    if (!stopped_early) {
+      CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+    }
+    bool ok = true;
+    rank = mn;
+    if (c->h_stop[0]) {
+      // first zero pivot at global g = k0 + t inside panel [ps, pe): finish the pivots
+      // [k0, g) inside the panel, then [ps, g) for the columns right of it, and require
+      // the whole Schur complement A[g:, g:] to vanish
+      const int k0 = c->h_stop[1], t = c->h_stop[2], g = k0 + t;
+      const int ps = (k0 / W) * W, pe = std::min(ps + W, mn);
+      const int bs = std::min(BS, pe - k0);
+      if (t > 0) {
+        const View b11 = x.sub(k0, k0, t, t);
+        ops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, t), b11);
+        ops.trsm_l(b11, x.sub(k0, k0 + bs, t, pe - k0 - bs));
+        ops.gemm(x.sub(g, g, m - g, pe - g), x.sub(g, k0, m - g, t), x.sub(k0, g, t, pe - g));
+      }
+      if (g > ps) {
+        ops.trsm_l(x.sub(ps, ps, g - ps, g - ps), x.sub(ps, pe, g - ps, n - pe));
+        ops.gemm(x.sub(g, pe, m - g, n - pe), x.sub(g, ps, m - g, g - ps), x.sub(ps, pe, g - ps, n - pe));
+      }
+      ok = !ops.nonzero(x.sub(g, g, m - g, n - g));
+      rank = g;
+    }
+    if (ok) {
+      ++c->st_spec_ok;
+    } else {
+      ops.copy(x, bk);
+      ++c->st_spec_fail;
+    }
+    c->dfree(backup);
+    return ok;
+  }
+
+  bool spec_disabled = false;
+
   NodeRes rec(const View& x) {
     const int m = x.m, n = x.n;
     ++c->st_nodes;
@@ -462,6 +558,22 @@ struct Driver {
     const bool base = m == 1 || n == 1 || std::min(m, n) <= threshold;
     if (fits_small(m, n)) return leaf_small(x);
     if (base) return leaf_global(x);
+    if (c->try_generic && !spec_disabled) {
+      int rk = 0;
+      if (speculative_lu(x, rk)) {
+        generic_counts_rec(m, n, rk, threshold, host_counts);
+        return NodeRes{ident(m), ident(n), rk};
+      }
+      spec_disabled = true;  // non-generic node: do not speculate again inside its subtree
+      NodeRes res = rec_exact(x);
+      spec_disabled = false;
+      return res;
+    }
+    return rec_exact(x);
+  }
+
+  NodeRes rec_exact(const View& x) {
+    const int m = x.m, n = x.n;
     // Zero-block short-circuit without a dedicated sync: the test result travels back
     // with the next leaf readback (inside A1's subtree).  Factoring A1 of a zero block
     // is exact (identity, r=0, data untouched), so only the left spine is spent.
@@ -664,6 +776,8 @@ int pluq_create(pluq_ctx** out, int device, void* stream) {
     CU(cudaHostAlloc((void**)&c->h_counts, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_flag, sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault));
+    CU(cudaMalloc((void**)&c->d_stop, 4 * sizeof(int)));
+    CU(cudaHostAlloc((void**)&c->h_stop, 4 * sizeof(int), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_zflags, pluq_ctx::kMaxDepth * sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_zflags, pluq_ctx::kMaxDepth * sizeof(int), cudaHostAllocDefault));
     cudaMemPool_t pool;
@@ -699,6 +813,8 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->d_zflags) cudaFree(c->d_zflags);
+  if (c->d_stop) cudaFree(c->d_stop);
+  if (c->h_stop) cudaFreeHost(c->h_stop);
   if (c->h_zflags) cudaFreeHost(c->h_zflags);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   delete c;
@@ -722,6 +838,9 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_min_k") c->tc_min_k = value;
   else if (k == "tc_k_pass") c->tc.k_pass_override = value;
   else if (k == "try_generic") c->try_generic = value;
+  else if (k == "spec_block") c->spec_block = value;
+  else if (k == "spec_check") c->spec_check = value;
+  else if (k == "spec_panel") c->spec_panel = value;
   else return kInvalid;
   return kOk;
 }
@@ -738,8 +857,9 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[9] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt, c->st_zero_skips, c->st_generic};
-  for (int64_t i = 0; i < nout && i < 9; ++i) out[i] = v[i];
+  int64_t v[11] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+                   c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail};
+  for (int64_t i = 0; i < nout && i < 11; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -784,14 +904,22 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     unsigned long long* gtab = nullptr;
     if (a.try_generic) gtab = upload_generic_counts(c, m, n, threshold);
     a.generic_counts = gtab;
-    size_t smem = small_smem_bytes(m, n, threshold);
-    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (int64_t b0 = 0; b0 < batch; b0 += 2147483647ll) {
-      small_pluq_kernel<<<(unsigned)std::min<int64_t>(batch - b0, 2147483647ll), (unsigned)c->batch_threads, smem, c->stream>>>(a);
+    int* flags = nullptr;
+    if (a.try_generic) {
+      flags = c->dalloc<int>((size_t)batch);
+      a.generic_flag = flags;
+      const size_t cs = crout_smem_bytes(m, n);
+      CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+      crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
       c->check_launch();
     }
+    size_t smem = small_smem_bytes(m, n, threshold);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    small_pluq_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, smem, c->stream>>>(a);
+    c->check_launch();
     if (!d_counts) c->dfree(cnt);
     if (gtab) c->dfree(gtab);
+    if (flags) c->dfree(flags);
   });
 }
 
@@ -878,6 +1006,9 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     a.cnt_accumulate = 0;
     const size_t smem = small_smem_bytes(m, n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t cs = crout_smem_bytes(m, n);
+    CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+    int* flags = a.try_generic ? c->dalloc<int>((size_t)batch) : nullptr;
     for (int64_t k = 0; k < nchunks; ++k) {
       const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
       if (nb <= 0) break;
@@ -891,6 +1022,11 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       a.a = dA + b0 * mn;
       a.p_out = dp + b0 * m; a.q_out = dp + batch * m + b0 * n; a.r_out = dp + batch * (m + n) + b0;
       a.cnt_out = cnt + 4 * b0;
+      if (flags) {
+        a.generic_flag = flags + b0;
+        crout_fast_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, cs, c->stream>>>(a);
+        c->check_launch();
+      }
       small_pluq_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, smem, c->stream>>>(a);
       c->check_launch();
       to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA + b0 * mn, raw + b0 * mn, cntk);
@@ -909,6 +1045,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     cudaStreamDestroy(sout);
     c->dfree(cnt);
     if (gtab) c->dfree(gtab);
+    if (flags) c->dfree(flags);
     c->dfree(dp);
     c->dfree(dA);
     c->dfree(raw);

@@ -4,6 +4,11 @@
 
 namespace pluq {
 
+// Speculative-path predication: kernels launched under a stop flag do nothing once it is set.
+__device__ __forceinline__ bool stopped(const int* stop) {
+  return stop && *reinterpret_cast<const volatile int*>(stop);
+}
+
 // ---------------------------------------------------------------------------------
 // Small-node / batched PLUQ: one CTA per block, block staged through shared memory.
 // ---------------------------------------------------------------------------------
@@ -28,6 +33,7 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   __shared__ BcShared sh;
   __shared__ Counts cnt;
+  if (args.generic_flag && args.generic_flag[blockIdx.x]) return;  // done by crout_fast_kernel
   const int m = args.m, n = args.n;
   const int lds = n | 1;
   uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
@@ -50,26 +56,7 @@ __global__ void small_pluq_kernel(SmallArgs args) {
   SmallCtx c{args.mp, args.threshold, &cnt, &sh, args.invtab};
   View x{sa, lds, m, n};
   int* P = stk; int* Q = P + m; int* top = Q + n;
-  int r = -1;
-  if (args.try_generic) {
-    r = crout_generic(x, args.mp, args.invtab, &sh);
-    if (r >= 0) {
-      for (int t = threadIdx.x; t < m; t += blockDim.x) P[t] = t;
-      for (int t = threadIdx.x; t < n; t += blockDim.x) Q[t] = t;
-      if (threadIdx.x == 0 && args.generic_counts) {
-        const unsigned long long* g = args.generic_counts + 4 * r;
-        cnt.mul = g[0]; cnt.add = g[1]; cnt.inv = g[2]; cnt.red = g[3];
-      }
-    } else {
-      // not generic: restore the block from global memory and run the exact recursion
-      const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-      for (int i = w; i < m; i += nw)
-        for (int j = ln; j < n; j += 32) sa[i * lds + j] = ga[(int64_t)i * args.lda + j];
-      __syncthreads();
-    }
-  }
-  if (args.generic_flag && threadIdx.x == 0) args.generic_flag[blockIdx.x] = r >= 0;
-  if (r < 0) r = rec_smem(x, P, Q, top, c);
+  const int r = rec_smem(x, P, Q, top, c);
   {
     const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     for (int i = w; i < m; i += nw)
@@ -92,6 +79,53 @@ __global__ void small_pluq_kernel(SmallArgs args) {
 }
 
 // Dynamic shared memory of small_pluq_kernel: block (odd pitch) + P/Q + recursion stack.
+// Lean generic-profile kernel (no recursion compiled in, so few registers and many
+// CTAs per SM): Crout LU + exact genericity check per block.  Successful blocks are
+// written back with P = Q = I; failed blocks are left untouched in global memory and
+// flagged for small_pluq_kernel, which then runs the exact recursion on them only.
+__global__ void crout_fast_kernel(SmallArgs args) {
+  extern __shared__ __align__(16) uint32_t smem_dyn[];
+  __shared__ BcShared sh;
+  const int m = args.m, n = args.n;
+  const int lds = n | 1;
+  uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
+  uint32_t* sa = smem_dyn;
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i0 = 4 * w; i0 < m; i0 += 4 * nw)
+    for (int j = ln; j < n; j += 32) {
+      uint32_t v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = i0 + q < m ? ga[(int64_t)(i0 + q) * args.lda + j] : 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) if (i0 + q < m) sa[(i0 + q) * lds + j] = v[q];
+    }
+  __syncthreads();
+  View x{sa, lds, m, n};
+  const int r = crout_generic<true>(x, args.mp, args.invtab, &sh);
+  if (threadIdx.x == 0) args.generic_flag[blockIdx.x] = r >= 0;
+  if (r < 0) return;
+  for (int i = w; i < m; i += nw)
+    for (int j = ln; j < n; j += 32) ga[(int64_t)i * args.lda + j] = sa[i * lds + j];
+  int* po = args.p_out + (int64_t)blockIdx.x * m;
+  int* qo = args.q_out + (int64_t)blockIdx.x * n;
+  for (int t = threadIdx.x; t < m; t += blockDim.x) po[t] = t;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) qo[t] = t;
+  if (threadIdx.x == 0) {
+    args.r_out[blockIdx.x] = r;
+    if (args.generic_counts) {
+      const unsigned long long* g = args.generic_counts + 4 * r;
+      unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);
+      if (args.cnt_accumulate) {
+        atomicAdd(co + 0, g[0]); atomicAdd(co + 1, g[1]); atomicAdd(co + 2, g[2]); atomicAdd(co + 3, g[3]);
+      } else {
+        co[0] = g[0]; co[1] = g[1]; co[2] = g[2]; co[3] = g[3];
+      }
+    }
+  }
+}
+
+inline size_t crout_smem_bytes(int64_t m, int64_t n) { return (size_t)(m * (n | 1) + 4) * 4; }
+
 inline size_t small_smem_bytes(int64_t m, int64_t n, int64_t thr) {
   int64_t lds = n | 1;
   return (size_t)((((m * lds) + 3) & ~3ll) + m + n + small_stack_words(m, n, thr) + 64) * 4;
@@ -161,7 +195,8 @@ __global__ void __launch_bounds__(1024) basecase_global_kernel(BaseArgs args) {
 constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 32;
 
 template <bool kSlow>
-__global__ void __launch_bounds__(256) simt_gemm_kernel(View c, View a, View b, ModP mp) {
+__global__ void __launch_bounds__(256) simt_gemm_kernel(View c, View a, View b, ModP mp, const int* stop) {
+  if (stopped(stop)) return;
   __shared__ uint32_t As[SG_BK][SG_BM + 4];
   __shared__ uint32_t Bs[SG_BK][SG_BN + 4];
   const int m = c.m, n = c.n, k = a.n;
@@ -358,7 +393,9 @@ __device__ void trinv_block_slow(uint32_t (*M)[TR_BASE + 1], uint32_t (*X)[TR_BA
 }
 
 // out[b] = inverse of the b-th 64x64 diagonal block of U (upper, nonzero diagonal).
-__global__ void __launch_bounds__(256) trinv_upper_kernel(View u, uint32_t* out, ModP mp, const uint16_t* invtab) {
+__global__ void __launch_bounds__(256) trinv_upper_kernel(View u, uint32_t* out, ModP mp, const uint16_t* invtab,
+                                                          const int* stop) {
+  if (stopped(stop)) return;
   __shared__ uint32_t Us[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t T[32][33];
@@ -389,7 +426,8 @@ __global__ void __launch_bounds__(256) trinv_upper_kernel(View u, uint32_t* out,
 }
 
 // out[b] = inverse of the b-th diagonal block of unit-lower L (diagonal implicit 1).
-__global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t* out, ModP mp) {
+__global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t* out, ModP mp, const int* stop) {
+  if (stopped(stop)) return;
   __shared__ uint32_t Ls[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t X[TR_BASE][TR_BASE + 1];
   __shared__ uint32_t T[32][33];
@@ -417,7 +455,9 @@ __global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t*
 
 // B <- B * Uinv for a w-column block (w <= 64): one CTA owns 32 rows of B (in place);
 // 128 threads, each a 4x4 register tile (8 shared loads per 16 products).
-__global__ void __launch_bounds__(128) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp) {
+__global__ void __launch_bounds__(128) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp,
+                                                               const int* stop) {
+  if (stopped(stop)) return;
   __shared__ uint32_t Bs[32][TR_BASE + 4];
   __shared__ uint32_t Ui[TR_BASE][TR_BASE + 4];
   const int w = b.n, r0 = blockIdx.x * 32, rows = min(32, b.m - r0);
@@ -468,7 +508,9 @@ __global__ void __launch_bounds__(128) trsm_apply_right_kernel(View b, const uin
 }
 
 // B <- Linv * B for a w-row block (w <= 64): one CTA owns 32 columns of B (in place).
-__global__ void __launch_bounds__(128) trsm_apply_left_kernel(const uint32_t* linv, View b, ModP mp) {
+__global__ void __launch_bounds__(128) trsm_apply_left_kernel(const uint32_t* linv, View b, ModP mp,
+                                                              const int* stop) {
+  if (stopped(stop)) return;
   __shared__ uint32_t Bs[TR_BASE][32 + 4];
   __shared__ uint32_t Li[TR_BASE][TR_BASE + 4];
   const int w = b.m, c0 = blockIdx.x * 32, cols = min(32, b.n - c0);
@@ -575,6 +617,118 @@ __global__ void copy_view_kernel(View dst, View src) {
 __global__ void invtab_kernel(uint16_t* tab, ModP mp) {
   for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < mp.p; a += gridDim.x * blockDim.x)
     tab[a] = a ? (uint16_t)invmod(a, mp) : 0;
+}
+
+// Diagonal block of the speculative no-pivot LU: Crout in shared memory until the
+// first zero pivot.  A zero pivot raises the stop flag (every later kernel of the
+// speculative schedule becomes a no-op) and records (k0, t) for the host.
+__global__ void __launch_bounds__(256) diag_crout_kernel(View blk, ModP mp, const uint16_t* invtab, int* stop,
+                                                         int* status, int k0) {
+  if (stopped(stop)) return;
+  extern __shared__ __align__(16) uint32_t smem_dyn[];
+  __shared__ BcShared sh;
+  const int m = blk.m, n = blk.n, lds = n | 1;
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i = w; i < m; i += nw)
+    for (int j = ln; j < n; j += 32) smem_dyn[i * lds + j] = blk.at(i, j);
+  __syncthreads();
+  View x{smem_dyn, lds, m, n};
+  const int t = crout_generic<false>(x, mp, invtab, &sh);
+  for (int i = w; i < m; i += nw)
+    for (int j = ln; j < n; j += 32) blk.at(i, j) = smem_dyn[i * lds + j];
+  if (threadIdx.x == 0 && t < min(m, n)) {
+    status[0] = k0;
+    status[1] = t;
+    __threadfence();
+    atomicExch(stop, 1);
+  }
+}
+
+// Diagonal block of the speculative LU, latency-optimised (one CTA of 1024 threads,
+// block <= 128 x 128): Crout with every dot product split over 4 threads (shuffle
+// reduction), the pivot settled first (a zero pivot leaves row/column t untouched for
+// the host finish), and the pivot inverse from a shared-memory copy of the inverse
+// table when p < 2^16.
+__global__ void __launch_bounds__(1024) diag_crout_fast_kernel(View blk, ModP mp, const uint16_t* invtab, int* stop,
+                                                              int* status, int k0) {
+  if (stopped(stop)) return;
+  extern __shared__ __align__(16) uint32_t smem_dyn[];
+  __shared__ uint32_t piv_sh;
+  const int m = blk.m, n = blk.n, mn = min(m, n), lds = n | 1;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  uint32_t* A = smem_dyn;
+  uint16_t* tab = reinterpret_cast<uint16_t*>(smem_dyn + ((m * lds + 3) & ~3));
+  const bool use_tab = invtab != nullptr;
+  if (use_tab)
+    for (int q = tid; q < (int)(mp.p + 1) / 2; q += nt)
+      reinterpret_cast<uint32_t*>(tab)[q] = reinterpret_cast<const uint32_t*>(invtab)[q];
+  for (int idx = tid; idx < m * n; idx += nt) {
+    const int i = idx / n, j = idx - (idx / n) * n;
+    A[i * lds + j] = blk.at(i, j);
+  }
+  __syncthreads();
+  const int sub = tid & 3, item0 = tid >> 2, nitems_par = nt >> 2;
+  const bool fast = mp.kchunk >= 40;  // <= 32 products per partial sum without reduction
+  int stop_t = mn;
+  for (int t = 0; t < mn; ++t) {
+    // settle the pivot: warp 0 computes U[t][t] (4 partial sums per lane group)
+    if (tid < 32) {
+      uint64_t acc = 0;
+      for (int k = tid; k < t; k += 32) {
+        acc += (uint64_t)A[t * lds + k] * A[k * lds + t];
+        if (!fast) acc = reduce64(acc, mp);
+      }
+      uint32_t v = reduce64(acc, mp);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = addmod(v, __shfl_xor_sync(0xffffffffu, v, o), mp);
+      if (tid == 0) piv_sh = submod(A[t * lds + t], v, mp);
+    }
+    __syncthreads();
+    const uint32_t piv = piv_sh;
+    if (piv == 0u) { stop_t = t; break; }
+    const uint32_t inv = use_tab ? (uint32_t)tab[piv] : invmod(piv, mp);
+    // U row t (j > t) and L column t (i > t): 4 threads per dot product
+    const int nu = n - t - 1, nl = m - t - 1;
+    for (int q0 = 0; q0 < nu + nl; q0 += nitems_par) {
+      const int q = q0 + item0;
+      const bool live = q < nu + nl;
+      const int i = q < nu ? t : t + 1 + (q - nu);
+      const int j = q < nu ? t + 1 + q : t;
+      uint64_t acc = 0;
+      if (live) {
+        const uint32_t* li = A + i * lds;
+        if (fast) {
+          for (int k = sub; k < t; k += 4) acc += (uint64_t)li[k] * A[k * lds + j];
+        } else {
+          for (int k = sub; k < t; k += 4) acc = reduce64(acc + (uint64_t)li[k] * A[k * lds + j], mp);
+        }
+      }
+      uint32_t v = reduce64(acc, mp);
+      v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 1), mp);
+      v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 2), mp);
+      if (live && sub == 0) {
+        uint32_t w = submod(A[i * lds + j], v, mp);
+        if (q >= nu) w = mulmod(w, inv, mp);  // L entry
+        A[i * lds + j] = w;
+      }
+    }
+    if (tid == 0) A[t * lds + t] = piv;
+    __syncthreads();
+  }
+  for (int idx = tid; idx < m * n; idx += nt) {
+    const int i = idx / n, j = idx - (idx / n) * n;
+    blk.at(i, j) = A[i * lds + j];
+  }
+  if (tid == 0 && stop_t < mn) {
+    status[0] = k0;
+    status[1] = stop_t;
+    __threadfence();
+    atomicExch(stop, 1);
+  }
+}
+
+inline size_t diag_fast_smem(int64_t bs, bool tab) {
+  return (size_t)(((bs * (bs | 1)) + 3) & ~3ll) * 4 + (tab ? 65536 * 2 : 0);
 }
 
 // Host-format conversion: float64 / int64 residues <-> uint32 device storage.

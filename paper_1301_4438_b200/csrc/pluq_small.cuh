@@ -438,6 +438,7 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c) {
 // exact recursion).  Each L/U entry is one dot product with a single delayed
 // reduction, two barriers per pivot.
 // ------------------------------------------------------------------------------------
+template <bool kCheckTrailing = true>
 __device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab, BcShared* sh) {
   const int m = x.m, n = x.n, mn = min(m, n);
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -445,6 +446,21 @@ __device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab
   const int ld = (int)x.ld;
   const bool fast = (uint64_t)mn <= mp.kchunk;
   for (int t = 0; t < mn; ++t) {
+    if (!kCheckTrailing) {
+      // speculative panel mode: settle the pivot first, so a zero pivot leaves row t and
+      // column t untouched for the host-side finish (exact Schur complement check)
+      if (tid == 0) {
+        uint64_t acc = 0;
+        const uint32_t* lt = A + t * ld;
+        for (int k = 0; k < t; ++k) acc = fast ? acc + (uint64_t)lt[k] * A[k * ld + t]
+                                               : reduce64(acc + (uint64_t)lt[k] * A[k * ld + t], mp);
+        sh->minv = (int)submod(A[t * ld + t], reduce64(acc, mp), mp);
+      }
+      __syncthreads();
+      const uint32_t pv = (uint32_t)sh->minv;
+      __syncthreads();
+      if (pv == 0u) return t;
+    }
     // U row t: A[t][j] -= sum_{k<t} L[t][k] U[k][j]      (j >= t)
     // L col t numerators: A[i][t] -= sum_{k<t} L[i][k] U[k][t]   (i > t)
     const int nu = n - t, nl = m - t - 1;
@@ -462,6 +478,7 @@ __device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab
     }
     __syncthreads();
     const uint32_t piv = A[t * ld + t];
+    if (piv == 0u && !kCheckTrailing) return t;  // caller verifies the global Schur complement
     if (piv == 0u) {
       // generic only if the whole Schur complement S[t:, t:] is zero (row t is done)
       bool nz = false;

@@ -124,7 +124,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 template <int L>
 __global__ void __launch_bounds__(256, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
-                      int m_pad, int n_pad, int kblocks, ModP mp) {
+                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   constexpr int BN = TcCfg<L>::BN, STAGES = TcCfg<L>::STAGES;
   constexpr int NPOS = 2 * L - 1;
   constexpr int ACC_COLS = NPOS * BN;               // one accumulator set
@@ -255,7 +256,8 @@ __global__ void __launch_bounds__(256, 1)
 
 // Limb planes of a row-major view (K-major operand): out[l][i][kk] = limb_l(v[i][kk]),
 // zero-padded to rows_pad x k_pad.  4 consecutive bytes per thread.
-__global__ void limb_rows_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad) {
+__global__ void limb_rows_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   const int64_t plane = (int64_t)rows_pad * k_pad;
   const int kq = k_pad / 4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rows_pad * kq;
@@ -278,7 +280,8 @@ __global__ void limb_rows_kernel(View v, uint8_t* out, int L, int rows_pad, int 
 
 // Limb planes of B^T (B is k x n row-major): out[l][j][kk] = limb_l(B[kk][j]),
 // zero-padded to n_pad x k_pad; 32x32 tiles transposed through shared memory.
-__global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_pad) {
+__global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_pad, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   __shared__ uint32_t tile[32][33];
   const int64_t plane = (int64_t)n_pad * k_pad;
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -364,7 +367,7 @@ struct TcGemm {
   }
 
   template <int L>
-  int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st) {
+  int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop) {
     constexpr int BN = TcCfg<L>::BN;
     const int m = c.m, n = c.n, k = a.n;
     const int m_pad = (m + TC_BM - 1) / TC_BM * TC_BM;
@@ -397,11 +400,11 @@ struct TcGemm {
       {
         int64_t work = (int64_t)m_pad * (k_pad / 4);
         int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 32);
-        limb_rows_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad);
+        limb_rows_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad, stop);
       }
       {
         dim3 grid(n_pad / 32, k_pad / 32);
-        limb_cols_kernel<<<grid, 256, 0, st>>>(bs, db, L, n_pad, k_pad);
+        limb_cols_kernel<<<grid, 256, 0, st>>>(bs, db, L, n_pad, k_pad, stop);
       }
       CUtensorMap ta, tb;
       if (!make_map(&ta, da, k_pad, (int64_t)L * m_pad, TC_BM) || !make_map(&tb, db, k_pad, (int64_t)L * n_pad, BN)) {
@@ -410,7 +413,7 @@ struct TcGemm {
         return kCuda;
       }
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
-      tc_modgemm_kernel<L><<<std::min(tiles, num_sms()), 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp);
+      tc_modgemm_kernel<L><<<std::min(tiles, num_sms()), 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);
@@ -424,15 +427,15 @@ struct TcGemm {
     return kOk;
   }
 
-  int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st) {
+  int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop = nullptr) {
     if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
     if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
     if (!load()) return kUnsupported;
     switch (limbs(mp.p)) {
-      case 1: return launch<1>(c, a, b, mp, st);
-      case 2: return launch<2>(c, a, b, mp, st);
-      case 3: return launch<3>(c, a, b, mp, st);
-      case 4: return launch<4>(c, a, b, mp, st);
+      case 1: return launch<1>(c, a, b, mp, st, stop);
+      case 2: return launch<2>(c, a, b, mp, st, stop);
+      case 3: return launch<3>(c, a, b, mp, st, stop);
+      case 4: return launch<4>(c, a, b, mp, st, stop);
     }
     return kUnsupported;
   }

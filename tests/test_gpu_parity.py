@@ -433,3 +433,56 @@ def test_full_scale_cfg3_invariants(pb):
     bad = verify.freivalds(orig, pb.PluqFactors(f.p_perm, f.q_perm, f.rank,
                                                 pb.DenseMatrix(pb.PrimeField(p), (a.data + 1) % p)), probes=1)
     assert not bad
+
+
+# ---------------------------------------------------------------------------------------
+# speculative no-pivot path (generic rank profile) on large nodes
+# ---------------------------------------------------------------------------------------
+
+SPEC_CASES = [
+    ("full", 200, 200, None, 65521),
+    ("full_tall", 300, 120, None, 65521),
+    ("full_wide", 120, 300, None, 65521),
+    ("xy_rank97", 200, 180, 97, 65521),      # zero pivot mid-block: finish with t > 0
+    ("xy_rank64", 192, 192, 64, 65521),      # zero pivot at a block boundary: t = 0
+    ("xy_rank5", 150, 170, 5, 1009),
+    ("full_p23", 160, 160, None, 8388593),   # 3-limb tensor-core GEMM inside
+    ("profile", 200, 240, 60, 8388593),      # non-generic (prescribed profiles): restore + recursion
+    ("zero", 130, 140, 0, 101),
+]
+
+
+@pytest.mark.parametrize("name,m,n,r,p", SPEC_CASES)
+def test_speculative_path_vs_oracle(pb, name, m, n, r, p):
+    from paper_1301_4438_b200 import _native
+
+    rng = np.random.default_rng(m * n + 7)
+    if name == "profile":
+        a0, _, _ = orc.gen_cfg4(seed=3, m=m, n=n, r=r, p=p)
+    elif name == "zero":
+        a0 = np.zeros((m, n), dtype=np.int64)
+    elif r is None:
+        a0 = rng.integers(0, p, (m, n))
+    else:
+        a0 = orc.gen_xy_rank(m, n, r, p, 11)
+    P, Q, R, packed, cnt = _oracle(a0, p)
+    ctx = _native.context()
+    ctx.set_option("small_cap", 1)       # every node is "large": the speculative path runs
+    ctx.set_option("spec_block", 16)
+    ctx.set_option("spec_panel", 48)     # several panels with inner blocks
+    ctx.set_option("spec_check", 3)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0)
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        ctx.set_option("small_cap", 128 * 128)
+        ctx.set_option("spec_block", 128)
+        ctx.set_option("spec_panel", 1024)
+        ctx.set_option("spec_check", 16)
+    _check(f, a.data, P, Q, R, packed, cnt, c)
+    if name in ("profile",):
+        assert st["speculative_fail"] >= 1
+    else:
+        assert st["speculative_ok"] >= 1
