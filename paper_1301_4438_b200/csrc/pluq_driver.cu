@@ -415,7 +415,7 @@ struct Driver {
   }
 
   NodeRes leaf_small(const View& x) {
-    c->ensure_res((size_t)x.m + x.n + 2);
+    c->ensure_res((size_t)x.m + x.n + 4);
     SmallArgs a;
     a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
     a.p_out = c->d_res; a.q_out = c->d_res + x.m; a.r_out = c->d_res + x.m + x.n;
@@ -424,6 +424,12 @@ struct Driver {
     a.try_generic = (int)c->try_generic;
     a.generic_counts = nullptr;           // charged on the host from the readback below
     a.generic_flag = a.try_generic ? c->d_res + x.m + x.n + 1 : nullptr;
+    a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
+    if (a.try_generic) {
+      a.fail_count = c->d_res + x.m + x.n + 2;
+      a.fail_list = c->d_res + x.m + x.n + 3;
+      CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+    }
     if (a.try_generic) {
       const size_t cs = crout_smem_bytes(x.m, x.n);
       CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
@@ -432,7 +438,7 @@ struct Driver {
     }
     size_t smem = small_smem_bytes(x.m, x.n, threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a);
+    small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a, a.fail_list, a.fail_count);
     c->check_launch();
     ++c->st_small;
     NodeRes res = readback(x.m, x.n, 1);
@@ -905,17 +911,25 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     if (a.try_generic) gtab = upload_generic_counts(c, m, n, threshold);
     a.generic_counts = gtab;
     int* flags = nullptr;
+    a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
+    size_t smem = small_smem_bytes(m, n, threshold);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (a.try_generic) {
-      flags = c->dalloc<int>((size_t)batch);
+      flags = c->dalloc<int>((size_t)batch + 1 + (size_t)batch);
       a.generic_flag = flags;
+      a.fail_count = flags + batch;
+      a.fail_list = flags + batch + 1;
+      CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
       const size_t cs = crout_smem_bytes(m, n);
       CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
       crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
       c->check_launch();
+      // exact recursion only for the blocks that are not generic (persistent grid)
+      const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 2);
+      small_pluq_kernel<<<grid, (unsigned)c->batch_threads, smem, c->stream>>>(a, a.fail_list, a.fail_count);
+    } else {
+      small_pluq_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, smem, c->stream>>>(a, nullptr, nullptr);
     }
-    size_t smem = small_smem_bytes(m, n, threshold);
-    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    small_pluq_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, smem, c->stream>>>(a);
     c->check_launch();
     if (!d_counts) c->dfree(cnt);
     if (gtab) c->dfree(gtab);
@@ -1008,7 +1022,13 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const size_t cs = crout_smem_bytes(m, n);
     CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-    int* flags = a.try_generic ? c->dalloc<int>((size_t)batch) : nullptr;
+    int* flags = a.try_generic ? c->dalloc<int>(2 * (size_t)batch + 1) : nullptr;
+    a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
+    if (flags) {
+      a.fail_count = flags + batch;
+      a.fail_list = flags + batch + 1;
+      CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+    }
     for (int64_t k = 0; k < nchunks; ++k) {
       const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
       if (nb <= 0) break;
@@ -1024,10 +1044,19 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       a.cnt_out = cnt + 4 * b0;
       if (flags) {
         a.generic_flag = flags + b0;
+        a.fail_base = (int)b0;
         crout_fast_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, cs, c->stream>>>(a);
         c->check_launch();
+        // failures are listed with global indices: run them with the chunk base at 0
+        SmallArgs g = a;
+        g.a = dA; g.p_out = dp; g.q_out = dp + batch * m; g.r_out = dp + batch * (m + n);
+        g.cnt_out = cnt; g.generic_flag = nullptr;
+        small_pluq_kernel<<<(unsigned)std::min<int64_t>(nb, 148 * 2), (unsigned)c->batch_threads, smem, c->stream>>>(
+            g, a.fail_list, a.fail_count);
+        CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+      } else {
+        small_pluq_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, smem, c->stream>>>(a, nullptr, nullptr);
       }
-      small_pluq_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, smem, c->stream>>>(a);
       c->check_launch();
       to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA + b0 * mn, raw + b0 * mn, cntk);
       c->check_launch();

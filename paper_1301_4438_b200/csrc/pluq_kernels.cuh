@@ -27,16 +27,34 @@ struct SmallArgs {
   int try_generic;              // attempt the no-pivot generic-profile path first
   const unsigned long long* generic_counts;  // (min(m,n)+1) x 4 charges by rank, or nullptr
   int* generic_flag;            // per block: 1 if the generic path produced the result (or nullptr)
+  int* fail_list;               // compacted indices of blocks needing the exact recursion
+  int* fail_count;
+  int fail_base;                // index offset of this launch's first block in the list
 };
 
-__global__ void small_pluq_kernel(SmallArgs args) {
+__device__ void small_pluq_block(const SmallArgs& args, int blk);
+
+// One CTA per block (grid = batch), or - when fail_list is given - a persistent grid
+// walking the compacted list of blocks the generic kernel could not finish.
+__global__ void small_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+  if (fail_list) {
+    const int cnt = *fail_count;
+    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+      small_pluq_block(args, fail_list[q]);
+      __syncthreads();
+    }
+    return;
+  }
+  small_pluq_block(args, blockIdx.x);
+}
+
+__device__ void small_pluq_block(const SmallArgs& args, int blk) {
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   __shared__ BcShared sh;
   __shared__ Counts cnt;
-  if (args.generic_flag && args.generic_flag[blockIdx.x]) return;  // done by crout_fast_kernel
   const int m = args.m, n = args.n;
   const int lds = n | 1;
-  uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
+  uint32_t* ga = args.a + (int64_t)blk * args.bstride;
   uint32_t* sa = smem_dyn;
   int* stk = reinterpret_cast<int*>(sa + (((int64_t)m * lds + 3) & ~3ll));
   {
@@ -62,13 +80,13 @@ __global__ void small_pluq_kernel(SmallArgs args) {
     for (int i = w; i < m; i += nw)
       for (int j = ln; j < n; j += 32) ga[(int64_t)i * args.lda + j] = sa[i * lds + j];
   }
-  int* po = args.p_out + (int64_t)blockIdx.x * m;
-  int* qo = args.q_out + (int64_t)blockIdx.x * n;
+  int* po = args.p_out + (int64_t)blk * m;
+  int* qo = args.q_out + (int64_t)blk * n;
   for (int t = threadIdx.x; t < m; t += blockDim.x) po[t] = P[t];
   for (int t = threadIdx.x; t < n; t += blockDim.x) qo[t] = Q[t];
   if (threadIdx.x == 0) {
-    args.r_out[blockIdx.x] = r;
-    unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);
+    args.r_out[blk] = r;
+    unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blk);
     if (args.cnt_accumulate) {
       atomicAdd(co + 0, cnt.mul); atomicAdd(co + 1, cnt.add);
       atomicAdd(co + 2, cnt.inv); atomicAdd(co + 3, cnt.red);
@@ -102,7 +120,10 @@ __global__ void crout_fast_kernel(SmallArgs args) {
   __syncthreads();
   View x{sa, lds, m, n};
   const int r = crout_generic<true>(x, args.mp, args.invtab, &sh);
-  if (threadIdx.x == 0) args.generic_flag[blockIdx.x] = r >= 0;
+  if (threadIdx.x == 0) {
+    args.generic_flag[blockIdx.x] = r >= 0;
+    if (r < 0 && args.fail_list) args.fail_list[atomicAdd(args.fail_count, 1)] = args.fail_base + blockIdx.x;
+  }
   if (r < 0) return;
   for (int i = w; i < m; i += nw)
     for (int j = ln; j < n; j += 32) ga[(int64_t)i * args.lda + j] = sa[i * lds + j];
@@ -653,68 +674,68 @@ __global__ void __launch_bounds__(1024) diag_crout_fast_kernel(View blk, ModP mp
                                                               int* status, int k0) {
   if (stopped(stop)) return;
   extern __shared__ __align__(16) uint32_t smem_dyn[];
-  __shared__ uint32_t piv_sh;
   const int m = blk.m, n = blk.n, mn = min(m, n), lds = n | 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   uint32_t* A = smem_dyn;
   uint16_t* tab = reinterpret_cast<uint16_t*>(smem_dyn + ((m * lds + 3) & ~3));
   const bool use_tab = invtab != nullptr;
-  if (use_tab)
-    for (int q = tid; q < (int)(mp.p + 1) / 2; q += nt)
-      reinterpret_cast<uint32_t*>(tab)[q] = reinterpret_cast<const uint32_t*>(invtab)[q];
+  if (use_tab) {
+    const int words = (int)(mp.p + 1) / 2;
+    const uint4* src = reinterpret_cast<const uint4*>(invtab);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (int q = tid; q < (words + 3) / 4; q += nt) dst[q] = __ldg(src + q);
+  }
   for (int idx = tid; idx < m * n; idx += nt) {
     const int i = idx / n, j = idx - (idx / n) * n;
     A[i * lds + j] = blk.at(i, j);
   }
   __syncthreads();
-  const int sub = tid & 3, item0 = tid >> 2, nitems_par = nt >> 2;
+  const int sub = tid & 3, item0 = tid >> 2;
   const bool fast = mp.kchunk >= 40;  // <= 32 products per partial sum without reduction
   int stop_t = mn;
   for (int t = 0; t < mn; ++t) {
-    // settle the pivot: warp 0 computes U[t][t] (4 partial sums per lane group)
-    if (tid < 32) {
-      uint64_t acc = 0;
-      for (int k = tid; k < t; k += 32) {
-        acc += (uint64_t)A[t * lds + k] * A[k * lds + t];
-        if (!fast) acc = reduce64(acc, mp);
-      }
-      uint32_t v = reduce64(acc, mp);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) v = addmod(v, __shfl_xor_sync(0xffffffffu, v, o), mp);
-      if (tid == 0) piv_sh = submod(A[t * lds + t], v, mp);
-    }
-    __syncthreads();
-    const uint32_t piv = piv_sh;
-    if (piv == 0u) { stop_t = t; break; }
-    const uint32_t inv = use_tab ? (uint32_t)tab[piv] : invmod(piv, mp);
-    // U row t (j > t) and L column t (i > t): 4 threads per dot product
-    const int nu = n - t - 1, nl = m - t - 1;
-    for (int q0 = 0; q0 < nu + nl; q0 += nitems_par) {
-      const int q = q0 + item0;
-      const bool live = q < nu + nl;
-      const int i = q < nu ? t : t + 1 + (q - nu);
-      const int j = q < nu ? t + 1 + q : t;
-      uint64_t acc = 0;
-      if (live) {
-        const uint32_t* li = A + i * lds;
-        if (fast) {
-          for (int k = sub; k < t; k += 4) acc += (uint64_t)li[k] * A[k * lds + j];
-        } else {
-          for (int k = sub; k < t; k += 4) acc = reduce64(acc + (uint64_t)li[k] * A[k * lds + j], mp);
+    // phase A: U row t (j >= t, incl. the pivot) and L column t numerators (i > t),
+    // 4 threads per dot product; each writer keeps its dot product to undo on a zero pivot
+    const int nu = n - t, nl = m - t - 1;
+    const int q = item0;  // nu + nl <= 255 < 256 items per pass
+    const bool live = q < nu + nl;
+    const int i = q < nu ? t : t + 1 + (q - nu);
+    const int j = q < nu ? t + q : t;
+    uint64_t acc = 0;
+    if (live) {
+      const uint32_t* li = A + i * lds;
+      if (fast) {
+        int kk = sub;
+        for (; kk + 12 < t; kk += 16) {
+          acc += (uint64_t)li[kk] * A[kk * lds + j];
+          acc += (uint64_t)li[kk + 4] * A[(kk + 4) * lds + j];
+          acc += (uint64_t)li[kk + 8] * A[(kk + 8) * lds + j];
+          acc += (uint64_t)li[kk + 12] * A[(kk + 12) * lds + j];
         }
-      }
-      uint32_t v = reduce64(acc, mp);
-      v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 1), mp);
-      v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 2), mp);
-      if (live && sub == 0) {
-        uint32_t w = submod(A[i * lds + j], v, mp);
-        if (q >= nu) w = mulmod(w, inv, mp);  // L entry
-        A[i * lds + j] = w;
+        for (; kk < t; kk += 4) acc += (uint64_t)li[kk] * A[kk * lds + j];
+      } else {
+        for (int kk = sub; kk < t; kk += 4) acc = reduce64(acc + (uint64_t)li[kk] * A[kk * lds + j], mp);
       }
     }
-    if (tid == 0) A[t * lds + t] = piv;
+    uint32_t v = reduce64(acc, mp);
+    v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 1), mp);
+    v = addmod(v, __shfl_xor_sync(0xffffffffu, v, 2), mp);
+    const bool writer = live && sub == 0;
+    if (writer) A[i * lds + j] = submod(A[i * lds + j], v, mp);
+    __syncthreads();
+    const uint32_t piv = A[t * lds + t];
+    if (piv == 0u) {
+      // zero pivot: undo phase A so row t / column t are untouched for the host finish
+      if (writer) A[i * lds + j] = addmod(A[i * lds + j], v, mp);
+      stop_t = t;
+      break;
+    }
+    // phase B: scale the L column by the pivot inverse
+    const uint32_t inv = use_tab ? (uint32_t)tab[piv] : invmod(piv, mp);
+    if (writer && q >= nu) A[i * lds + j] = mulmod(A[i * lds + j], inv, mp);
     __syncthreads();
   }
+  __syncthreads();
   for (int idx = tid; idx < m * n; idx += nt) {
     const int i = idx / n, j = idx - (idx / n) * n;
     blk.at(i, j) = A[i * lds + j];

@@ -467,10 +467,19 @@ __device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab
     for (int q = tid; q < nu + nl; q += nt) {
       const int i = q < nu ? t : t + 1 + (q - nu);
       const int j = q < nu ? t + q : t;
-      uint64_t acc = 0;
+      uint64_t acc = 0, acc2 = 0;
       const uint32_t* li = A + i * ld;
+      const uint32_t* cj = A + j;
       if (fast) {
-        for (int k = 0; k < t; ++k) acc += (uint64_t)li[k] * A[k * ld + j];
+        int k = 0;
+        for (; k + 3 < t; k += 4) {
+          acc += (uint64_t)li[k] * cj[k * ld];
+          acc2 += (uint64_t)li[k + 1] * cj[(k + 1) * ld];
+          acc += (uint64_t)li[k + 2] * cj[(k + 2) * ld];
+          acc2 += (uint64_t)li[k + 3] * cj[(k + 3) * ld];
+        }
+        for (; k < t; ++k) acc += (uint64_t)li[k] * cj[k * ld];
+        acc = reduce64(acc, mp) + (uint64_t)reduce64(acc2, mp);
       } else {
         for (int k = 0; k < t; ++k) acc = reduce64(acc + (uint64_t)li[k] * A[k * ld + j], mp);
       }
