@@ -422,6 +422,7 @@ struct Driver {
     a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
     a.invtab = c->invtab(mp.p);
     a.try_generic = (int)c->try_generic;
+    a.try_depth = 1;
     a.generic_counts = nullptr;           // charged on the host from the readback below
     a.generic_flag = a.try_generic ? c->d_res + x.m + x.n + 1 : nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
@@ -906,6 +907,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     a.cnt_out = cnt; a.cnt_accumulate = 0;
     a.invtab = c->invtab((uint32_t)p);
     a.try_generic = (int)c->try_generic;
+    a.try_depth = 1;  // depth 0 was attempted by crout_fast_kernel
     a.generic_flag = nullptr;
     unsigned long long* gtab = nullptr;
     if (a.try_generic) gtab = upload_generic_counts(c, m, n, threshold);
@@ -1013,6 +1015,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
     a.mp = mp; a.invtab = c->invtab((uint32_t)p);
     a.try_generic = (int)c->try_generic;
+    a.try_depth = 1;
     a.generic_flag = nullptr;
     unsigned long long* gtab = a.try_generic ? upload_generic_counts(c, m, n, threshold) : nullptr;
     a.generic_counts = gtab;

@@ -25,6 +25,7 @@ struct SmallArgs {
   int cnt_accumulate;
   const uint16_t* invtab;       // inverse table when p < 2^16 (else nullptr)
   int try_generic;              // attempt the no-pivot generic-profile path first
+  int try_depth;                // smallest recursion depth at which small_pluq_kernel attempts it
   const unsigned long long* generic_counts;  // (min(m,n)+1) x 4 charges by rank, or nullptr
   int* generic_flag;            // per block: 1 if the generic path produced the result (or nullptr)
   int* fail_list;               // compacted indices of blocks needing the exact recursion
@@ -71,7 +72,7 @@ __device__ void small_pluq_block(const SmallArgs& args, int blk) {
   }
   if (threadIdx.x == 0) { cnt.mul = cnt.add = cnt.inv = cnt.red = 0; }
   __syncthreads();
-  SmallCtx c{args.mp, args.threshold, &cnt, &sh, args.invtab};
+  SmallCtx c{args.mp, args.threshold, &cnt, &sh, args.invtab, args.try_generic, args.try_depth};
   View x{sa, lds, m, n};
   int* P = stk; int* Q = P + m; int* top = Q + n;
   const int r = rec_smem(x, P, Q, top, c);

@@ -22,7 +22,46 @@ struct SmallCtx {
   Counts* cnt;      // shared, touched by thread 0 only
   BcShared* sh;
   const uint16_t* invtab;  // inverses mod p when p < 2^16, else nullptr
+  int try_generic;         // attempt the generic-profile Crout at internal nodes (depth >= try_depth)
+  int try_depth;
 };
+
+// OpCounts of the reference recursion on a generic-profile block (see pluq_driver.cu).
+PLUQ_HD void generic_counts_dev(int64_t m, int64_t n, int64_t rho, int64_t thr, Counts& c) {
+  if (m == 0 || n == 0) return;
+  const int64_t rr = (m < n ? m : n) < rho ? (m < n ? m : n) : rho;
+  if (m == 1 || n == 1 || (m < n ? m : n) <= thr) {
+    for (int64_t t = 0; t < rr; ++t) {
+      const long long below = m - 1 - t, right = n - 1 - t;
+      if (below > 0) {
+        c.inv += 1; c.mul += below; c.red += below;
+        if (right > 0) { c.mul += below * right; c.add += below * right; c.red += below * right; }
+      }
+    }
+    return;
+  }
+  const int64_t kr = m / 2, kc = n / 2;
+  int64_t r1 = kr < kc ? kr : kc; r1 = r1 < rho ? r1 : rho;
+  generic_counts_dev(kr, kc, rho, thr, c);
+  charge_trsm_l(c, r1, n - kc);
+  charge_trsm_u(c, m - kr, r1);
+  charge_mm(c, kr - r1, n - kc, r1);
+  charge_mm(c, m - kr, kc - r1, r1);
+  charge_mm(c, m - kr, n - kc, r1);
+  int64_t r2 = (kr - r1) < (n - kc) ? (kr - r1) : (n - kc); r2 = r2 < rho - r1 ? r2 : rho - r1;
+  generic_counts_dev(kr - r1, n - kc, rho - r1, thr, c);
+  int64_t r3 = (m - kr) < (kc - r1) ? (m - kr) : (kc - r1); r3 = r3 < rho - r1 - r2 ? r3 : rho - r1 - r2;
+  generic_counts_dev(m - kr, kc - r1, rho - r1 - r2, thr, c);
+  const int64_t m4 = m - kr - r3, n4 = n - kc - r2;
+  charge_trsm_u(c, r3, r2);
+  charge_trsm_l(c, r3, r2);
+  charge_trsm_u(c, m4, r2);
+  charge_trsm_l(c, r3, n4);
+  charge_mm(c, r3, n4, r2);
+  charge_mm(c, m4, n4, r2);
+  charge_mm(c, m4, n4, r3);
+  generic_counts_dev(m4, n4, rho - r1 - r2 - r3, thr, c);
+}
 
 __device__ __forceinline__ void cta_ident(int* a, int n) {
   for (int t = threadIdx.x; t < n; t += blockDim.x) a[t] = t;
@@ -321,7 +360,10 @@ __device__ __forceinline__ int t_sigma(int x, int r1, int r2, int r3, int r4, in
   return x;
 }
 
-__device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c) {
+template <bool kCheckTrailing>
+__device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab, BcShared* sh);
+
+__device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int depth = 0) {
   const int m = x.m, n = x.n;
   BcShared* sh = c.sh;
   if (m == 0 || n == 0) {
@@ -329,12 +371,27 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c) {
     return 0;
   }
   if (m == 1 || n == 1 || min(m, n) <= c.threshold) return base_smem(x, P, Q, stk, c);
+  if (c.try_generic && depth >= c.try_depth) {
+    // generic-profile shortcut for the whole subtree (exact; see crout_generic)
+    uint32_t* bk = reinterpret_cast<uint32_t*>(stk);
+    for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) bk[idx] = x.at(idx / n, idx % n);
+    __syncthreads();
+    const int rg = crout_generic<true>(x, c.mp, c.invtab, sh);
+    if (rg >= 0) {
+      cta_ident(P, m); cta_ident(Q, n);
+      if (threadIdx.x == 0) generic_counts_dev(m, n, rg, c.threshold, *c.cnt);
+      __syncthreads();
+      return rg;
+    }
+    for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) x.at(idx / n, idx % n) = bk[idx];
+    __syncthreads();
+  }
   const int kr = m / 2, kc = n / 2;
   const ModP mp = c.mp;
   const bool t0 = threadIdx.x == 0;
 
   int* P1 = stk; int* Q1 = P1 + kr; int* top = Q1 + kc;
-  const int r1 = rec_smem(x.sub(0, 0, kr, kc), P1, Q1, top, c);
+  const int r1 = rec_smem(x.sub(0, 0, kr, kc), P1, Q1, top, c, depth + 1);
   {
     int* g = top; int* scr = g + max(m, n);
     cta_inverse(P1, g, kr);
@@ -355,9 +412,9 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c) {
   cta_mm_sub(x.sub(kr, r1, m - kr, n - r1), x.sub(kr, 0, m - kr, r1), x.sub(0, r1, r1, n - r1), mp);
 
   int* P2 = top; int* Q2 = P2 + (kr - r1); top = Q2 + (n - kc);
-  const int r2 = rec_smem(x.sub(r1, kc, kr - r1, n - kc), P2, Q2, top, c);
+  const int r2 = rec_smem(x.sub(r1, kc, kr - r1, n - kc), P2, Q2, top, c, depth + 1);
   int* P3 = top; int* Q3 = P3 + (m - kr); top = Q3 + (kc - r1);
-  const int r3 = rec_smem(x.sub(kr, r1, m - kr, kc - r1), P3, Q3, top, c);
+  const int r3 = rec_smem(x.sub(kr, r1, m - kr, kc - r1), P3, Q3, top, c, depth + 1);
   {
     int* ip3 = top; int* ip2 = ip3 + (m - kr); int* scr = ip2 + (kr - r1);
     cta_inverse(P3, ip3, m - kr);
@@ -393,7 +450,7 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c) {
   }
 
   int* P4 = top; int* Q4 = P4 + m4; top = Q4 + n4;
-  const int r4 = rec_smem(x.sub(kr + r3, kc + r2, m4, n4), P4, Q4, top, c);
+  const int r4 = rec_smem(x.sub(kr + r3, kc + r2, m4, n4), P4, Q4, top, c, depth + 1);
   {
     int* ip4 = top; int* scr = ip4 + m4;
     cta_inverse(P4, ip4, m4);
@@ -532,6 +589,7 @@ inline int64_t small_stack_words(int64_t m, int64_t n, int64_t thr) {
   int64_t jbuf = hm * hn + 1 + 17 * mx + 300;    // J scratch + TRSM block-inverse scratch
   int64_t child = small_stack_words(hm, hn, thr);
   int64_t t = own > jbuf ? own : jbuf;
+  t = t > m * n ? t : m * n;  // generic-attempt backup of the node (at the frame base)
   return 2 * (m + n) + (t > child ? t : child) + 8;
 }
 

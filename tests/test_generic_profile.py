@@ -33,7 +33,7 @@ def test_generic_profile_claim_and_counts():
         m, n = (int(x) for x in rng.integers(1, 60, 2))
         r = int(rng.integers(0, min(m, n) + 1))
         a = rng.integers(0, p, (m, n)) if trial % 3 == 0 else orc.gen_xy_rank(m, n, r, p, trial, permute=trial % 3 == 2)
-        thr = int(rng.choice([1, 2, 4, 30]))
+        thr = int(rng.choice([1, 2, 4, 30, 10**9]))  # 10**9: Algorithm 2 on the whole matrix
         ok, rr, packed = _unpivoted(a, p)
         if not ok:
             continue
