@@ -33,6 +33,9 @@ M = N = 64
 BATCH = 4096
 THRESHOLD = 30
 METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
+# dram__bytes_read.sum + dram__bytes_write.sum of crout_fast_kernel per launch from the committed
+# ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
+TRAFFIC = None
 UNIT = "Gfield-op/s"
 
 
@@ -256,6 +259,16 @@ def main():
         step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
         ranks = res.ranks.to(torch.int64).cpu().numpy()
         w_step = float(sum(work(M, N, int(r)) for r in ranks))
+        # per-kernel device times of one extra (untimed) step, CUDA events inside the library
+        from paper_1301_4438_b200 import _native
+
+        kctx = _native.context(local)
+        kctx.set_option("time_kernels", 1)
+        work_buf.copy_(pristine)
+        flush.fill_(7)
+        step()
+        kst = kctx.stats()
+        kctx.set_option("time_kernels", 0)
 
         # ---- e2e through the public API with pinned host buffers (H2D + D2H inside) ----
         pinned = torch.empty((BATCH, M, N), dtype=torch.float64, pin_memory=True)
@@ -287,6 +300,7 @@ def main():
         return
 
     avg_launch = t_dev / args.steps
+    t_gen = kst["t_generic_ns"] / 1e9 if kst["t_generic_ns"] > 0 else avg_launch
     alg_bytes = BATCH * M * N * 4 * 2 + BATCH * (M + N + 1) * 4
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -298,11 +312,13 @@ def main():
                 "path": "pluq_batched(pinned float64 numpy batch) -> C ABI pluq_factor_batched_host_f64",
                 "ms_per_step": 1e3 * t_e2e / len(e2e_t)},
         "gpu_launches": args.steps,
-        "roofline": {"bound": "hbm", "kernel": "small_pluq_kernel", "achieved": alg_bytes / avg_launch / 1e9,
-                     "peak": hbm, "unit": "GB/s", "frac": alg_bytes / avg_launch / 1e9 / hbm, "traffic": None,
-                     "peak_kind": peak_kind,
-                     "note": "algorithmic bytes = read+write of 4096 int32 64x64 blocks + P/Q/rank; "
-                             "the kernel is latency-bound (serial pivot chain per matrix), see DESIGN.md"},
+        "roofline": {"bound": "hbm", "kernel": "crout_fast_kernel", "achieved": alg_bytes / t_gen / 1e9,
+                     "peak": hbm, "unit": "GB/s", "frac": alg_bytes / t_gen / 1e9 / hbm, "traffic": TRAFFIC,
+                     "peak_kind": peak_kind, "kernel_ms": t_gen * 1e3,
+                     "fallback_kernel_ms": kst["t_fallback_ns"] / 1e6,
+                     "note": "algorithmic bytes = read+write of 4096 int32 64x64 blocks + P/Q/rank; the "
+                             "generic-profile Crout kernel is latency/issue bound (64-pivot chain per matrix); "
+                             "small_pluq_kernel handles the few non-generic matrices; see DESIGN.md"},
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
     }

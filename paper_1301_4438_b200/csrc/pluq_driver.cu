@@ -96,6 +96,9 @@ struct pluq_ctx {
   int64_t tc_min_dim = 128;        // smallest m, n for the tensor-core GEMM
   int64_t tc_min_k = 32;
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
+  int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
+  int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
+  float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
           st_simt = 0, st_zero_skips = 0, st_generic = 0, st_spec_ok = 0, st_spec_fail = 0;
@@ -845,6 +848,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_min_k") c->tc_min_k = value;
   else if (k == "tc_k_pass") c->tc.k_pass_override = value;
   else if (k == "try_generic") c->try_generic = value;
+  else if (k == "time_kernels") c->time_kernels = value;
+  else if (k == "fixed_kernels") c->fixed_kernels = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;
   else if (k == "spec_panel") c->spec_panel = value;
@@ -864,9 +869,10 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[11] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
-                   c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail};
-  for (int64_t i = 0; i < nout && i < 11; ++i) out[i] = v[i];
+  int64_t v[13] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+                   c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail,
+                   (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f)};
+  for (int64_t i = 0; i < nout && i < 13; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -924,11 +930,24 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
       const size_t cs = crout_smem_bytes(m, n);
       CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-      crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
+      cudaEvent_t ev[3];
+      if (c->time_kernels)
+        for (auto& e : ev) { CU(cudaEventCreate(&e)); }
+      if (c->time_kernels) CU(cudaEventRecord(ev[0], c->stream));
+      if (!(c->fixed_kernels && launch_crout_fixed(a, batch, c->stream)))
+        crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
       c->check_launch();
+      if (c->time_kernels) CU(cudaEventRecord(ev[1], c->stream));
       // exact recursion only for the blocks that are not generic (persistent grid)
       const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 2);
       small_pluq_kernel<<<grid, (unsigned)c->batch_threads, smem, c->stream>>>(a, a.fail_list, a.fail_count);
+      if (c->time_kernels) {
+        CU(cudaEventRecord(ev[2], c->stream));
+        CU(cudaEventSynchronize(ev[2]));
+        CU(cudaEventElapsedTime(&c->t_generic_ms, ev[0], ev[1]));
+        CU(cudaEventElapsedTime(&c->t_fallback_ms, ev[1], ev[2]));
+        for (auto& e : ev) cudaEventDestroy(e);
+      }
     } else {
       small_pluq_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, smem, c->stream>>>(a, nullptr, nullptr);
     }
@@ -1048,7 +1067,8 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       if (flags) {
         a.generic_flag = flags + b0;
         a.fail_base = (int)b0;
-        crout_fast_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, cs, c->stream>>>(a);
+        if (!(c->fixed_kernels && launch_crout_fixed(a, nb, c->stream)))
+          crout_fast_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, cs, c->stream>>>(a);
         c->check_launch();
         // failures are listed with global indices: run them with the chunk base at 0
         SmallArgs g = a;

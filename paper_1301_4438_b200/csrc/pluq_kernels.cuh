@@ -146,6 +146,152 @@ __global__ void crout_fast_kernel(SmallArgs args) {
   }
 }
 
+// Shape-specialised generic-profile kernel (compile-time M x N, M + N - 1 <= NT): Crout
+// with ONE barrier per pivot.  Each thread owns one item per step (a U-row entry or an
+// L-column numerator).  The L column of step t is published unscaled in a
+// double-buffered vector and scaled by its owner during step t+1, while readers apply
+// inv(U[t][t]) to that single term themselves; the owner of the pivot publishes its
+// inverse before the barrier.  Static shared arrays give immediate-offset LDS.
+template <int M, int N, int NT, bool kFast>
+__global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
+  static_assert(M + N - 1 <= NT, "one item per thread per step");
+  constexpr int MN = M < N ? M : N;
+  constexpr int LD = N | 1;
+  __shared__ uint32_t A[M * LD];
+  __shared__ uint32_t Ncol[2][M];
+  __shared__ uint32_t invs[2];
+  __shared__ int zero_at;
+  __shared__ BcShared sh;
+  const int tid = threadIdx.x;
+  const ModP mp = args.mp;
+  const uint16_t* tab = args.invtab;
+  uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
+  {
+    const int w = tid >> 5, ln = tid & 31;
+#pragma unroll 4
+    for (int i = w; i < M; i += NT / 32)
+      for (int j = ln; j < N; j += 32) A[i * LD + j] = ga[(int64_t)i * args.lda + j];
+  }
+  if (tid == 0) zero_at = -1;
+  __syncthreads();
+  int own_i = -1;          // L item row owned at the previous step
+  uint32_t own_num = 0;    // its unscaled numerator
+  uint32_t inv_prev = 0;
+  int t = 0;
+  for (; t < MN; ++t) {
+    const int nu = N - t;
+    const bool is_u = tid < nu;
+    const bool is_l = !is_u && tid - nu < M - t - 1;
+    const int row = is_u ? t : t + 1 + (tid - nu);
+    const int col = is_u ? t + tid : t;
+    // scale the L entry of the previous step (nobody reads A[.][t-1] during this step)
+    if (own_i >= 0) A[own_i * LD + t - 1] = mulmod(own_num, inv_prev, mp);
+    own_i = -1;
+    if (is_u || is_l) {
+      uint64_t acc = 0, acc2 = 0;
+      const uint32_t* ri = A + row * LD;
+      const uint32_t* cj = A + col;
+      const int kend = t - 1;  // terms k < t-1 read final values; k = t-1 is the deferred one
+      int kk = 0;
+      if (kFast) {
+#pragma unroll 4
+        for (; kk + 1 < kend; kk += 2) {
+          acc += (uint64_t)ri[kk] * cj[kk * LD];
+          acc2 += (uint64_t)ri[kk + 1] * cj[(kk + 1) * LD];
+        }
+        for (; kk < kend; ++kk) acc += (uint64_t)ri[kk] * cj[kk * LD];
+        acc = (uint64_t)reduce64(acc, mp) + reduce64(acc2, mp);
+      } else {
+        for (; kk < kend; ++kk) acc = reduce64(acc + (uint64_t)ri[kk] * cj[kk * LD], mp);
+      }
+      if (t > 0) {
+        const uint32_t lt = mulmod(Ncol[(t - 1) & 1][row], inv_prev, mp);  // L[row][t-1]
+        acc += (uint64_t)lt * cj[(t - 1) * LD];
+      }
+      const uint32_t v = submod(A[row * LD + col], reduce64(acc, mp), mp);
+      if (is_u) {
+        A[row * LD + col] = v;
+        if (col == t) {
+          if (v == 0u) zero_at = t;
+          else invs[t & 1] = tab ? (uint32_t)tab[v] : invmod(v, mp);
+        }
+      } else {
+        Ncol[t & 1][row] = v;
+        own_i = row;
+        own_num = v;
+      }
+    }
+    __syncthreads();
+    if (zero_at >= 0) break;
+    inv_prev = invs[t & 1];
+  }
+  int r = MN;
+  if (zero_at >= 0) {
+    // zero pivot at t: column t's Schur values are the unscaled numerators; the
+    // previous column's owners already wrote their scaled entries in this step
+    for (int i = t + 1 + tid; i < M; i += NT) A[i * LD + t] = Ncol[t & 1][i];
+    __syncthreads();
+    bool nz = false;
+    for (int j = t + tid; j < N; j += NT) nz |= A[t * LD + j] != 0u;
+    const int rows = M - t - 1, cols = N - t;
+    for (int q = tid; q < rows * cols; q += NT) {
+      const int i = t + 1 + q / cols, j = t + q % cols;
+      if (j == t) { nz |= A[i * LD + j] != 0u; continue; }
+      uint64_t acc = 0;
+      for (int kk = 0; kk < t; ++kk) {
+        acc += (uint64_t)A[i * LD + kk] * A[kk * LD + j];
+        if (!kFast) acc = reduce64(acc, mp);
+      }
+      nz |= submod(A[i * LD + j], reduce64(acc, mp), mp) != 0u;
+    }
+    if (__syncthreads_or(nz)) {
+      if (tid == 0) {
+        args.generic_flag[blockIdx.x] = 0;
+        if (args.fail_list) args.fail_list[atomicAdd(args.fail_count, 1)] = args.fail_base + blockIdx.x;
+      }
+      return;
+    }
+    for (int q = tid; q < (M - t) * (N - t); q += NT) A[(t + q / (N - t)) * LD + t + q % (N - t)] = 0u;
+    r = t;
+  } else if (own_i >= 0) {
+    A[own_i * LD + MN - 1] = mulmod(own_num, inv_prev, mp);  // last L column
+  }
+  __syncthreads();
+  {
+    const int w = tid >> 5, ln = tid & 31;
+    for (int i = w; i < M; i += NT / 32)
+      for (int j = ln; j < N; j += 32) ga[(int64_t)i * args.lda + j] = A[i * LD + j];
+  }
+  int* po = args.p_out + (int64_t)blockIdx.x * M;
+  int* qo = args.q_out + (int64_t)blockIdx.x * N;
+  for (int q = tid; q < M; q += NT) po[q] = q;
+  for (int q = tid; q < N; q += NT) qo[q] = q;
+  if (tid == 0) {
+    args.generic_flag[blockIdx.x] = 1;
+    args.r_out[blockIdx.x] = r;
+    if (args.generic_counts) {
+      const unsigned long long* g = args.generic_counts + 4 * r;
+      unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);
+      if (args.cnt_accumulate) {
+        atomicAdd(co + 0, g[0]); atomicAdd(co + 1, g[1]); atomicAdd(co + 2, g[2]); atomicAdd(co + 3, g[3]);
+      } else {
+        co[0] = g[0]; co[1] = g[1]; co[2] = g[2]; co[3] = g[3];
+      }
+    }
+  }
+}
+
+// Launch the generic-profile kernel for a batch: the specialised 64x64 instance when it
+// applies, otherwise the runtime-shape kernel.
+inline bool launch_crout_fixed(const SmallArgs& a, int64_t batch, cudaStream_t st) {
+  if (a.m == 64 && a.n == 64) {
+    if (a.mp.kchunk >= 64) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    else crout_fixed_kernel<64, 64, 128, false><<<(unsigned)batch, 128, 0, st>>>(a);
+    return true;
+  }
+  return false;
+}
+
 inline size_t crout_smem_bytes(int64_t m, int64_t n) { return (size_t)(m * (n | 1) + 4) * 4; }
 
 inline size_t small_smem_bytes(int64_t m, int64_t n, int64_t thr) {
