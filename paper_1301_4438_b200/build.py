@@ -11,7 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpluq_b200.so")
 SOURCES = ["pluq_driver.cu"]
-HEADERS = ["pluq_common.cuh", "pluq_basecase.cuh", "pluq_small.cuh", "pluq_kernels.cuh", "pluq_tc_gemm.cuh"]
+HEADERS = ["pluq_common.cuh", "pluq_basecase.cuh", "pluq_small.cuh", "pluq_rpm.cuh", "pluq_kernels.cuh",
+           "pluq_tc_gemm.cuh"]
 
 
 def nvcc_path() -> str:
@@ -42,6 +43,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     ] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    extra = os.environ.get("PLUQ_NVCC_FLAGS")  # diagnostics builds, e.g. -DPLUQ_TRACE
+    if extra:
+        cmd[1:1] = extra.split()
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

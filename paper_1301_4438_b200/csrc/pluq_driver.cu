@@ -25,6 +25,8 @@
 
 #include "../../include/pluq_b200.h"
 #include "pluq_kernels.cuh"
+#include <chrono>
+#include <cstdio>
 #include "pluq_tc_gemm.cuh"
 
 using namespace pluq;
@@ -98,11 +100,20 @@ struct pluq_ctx {
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
+  int64_t host_chunks = 8;         // pipeline depth of the host-buffer batched path
+  int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
+  int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
+  int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
           st_simt = 0, st_zero_skips = 0, st_generic = 0, st_spec_ok = 0, st_spec_fail = 0;
   TcGemm tc;
+  // host-batch pipeline resources, created once per context
+  cudaStream_t side[6] = {};        // H2D, D2H, 4 exact-kernel streams
+  std::vector<cudaEvent_t> evpool;  // timing-disabled events
+  int32_t* h_bres = nullptr;        // pinned per-block results (P, Q, rank)
+  size_t h_bres_cap = 0;
   uint16_t* d_invtab = nullptr;  // inverse table for invtab_p (p < 2^16)
   uint32_t invtab_p = 0;
 
@@ -116,6 +127,28 @@ struct pluq_ctx {
       CU(cudaStreamSynchronize(stream));  // one-time; the table may be read from other streams
     }
     return d_invtab;
+  }
+
+  cudaStream_t* side_streams() {
+    if (!side[0])
+      for (auto& s : side) CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return side;
+  }
+  cudaEvent_t* events(size_t count) {
+    while (evpool.size() < count) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evpool.push_back(e);
+    }
+    return evpool.data();
+  }
+  int32_t* batch_results(size_t ints) {
+    if (ints > h_bres_cap) {
+      if (h_bres) CU(cudaFreeHost(h_bres));
+      h_bres_cap = std::max(ints, size_t(1) << 20);
+      CU(cudaHostAlloc((void**)&h_bres, h_bres_cap * sizeof(int32_t), cudaHostAllocDefault));
+    }
+    return h_bres;
   }
 
   void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok = st_spec_fail = 0; }
@@ -386,6 +419,25 @@ struct NodeRes {
   int r;
 };
 
+// Exact factorization of the blocks listed in fl/fc (every block of the grid when fl is
+// null): the rank-profile kernel (pluq_rpm.cuh) or the field-arithmetic recursion.
+static size_t block_smem_bytes(int64_t m, int64_t n, int64_t thr) {
+  return std::max(small_smem_bytes(m, n, thr), rpm_smem_bytes(m, n));
+}
+static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigned threads, const int* fl,
+                         const int* fc, cudaStream_t st) {
+  if (c->exact_kernel) {
+    const size_t smem = rpm_smem_bytes(a.m, a.n);
+    CU(cudaFuncSetAttribute(rpm_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rpm_pluq_kernel<<<grid, (unsigned)c->rpm_threads, smem, st>>>(a, fl, fc);
+  } else {
+    const size_t smem = small_smem_bytes(a.m, a.n, a.threshold);
+    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    small_pluq_kernel<<<grid, threads, smem, st>>>(a, fl, fc);
+  }
+  c->check_launch();
+}
+
 struct Driver {
   pluq_ctx* c;
   ModP mp;
@@ -396,7 +448,7 @@ struct Driver {
   Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ModP::make(p)), threshold(thr), ops{ctx, ModP::make(p)} {}
 
   bool fits_small(int64_t m, int64_t n) const {
-    return m * n <= c->small_cap && small_smem_bytes(m, n, threshold) <= 227 * 1024;
+    return m * n <= c->small_cap && block_smem_bytes(m, n, threshold) <= 227 * 1024;
   }
 
   int depth = 0;            // depth of the node being processed
@@ -440,10 +492,7 @@ struct Driver {
       crout_fast_kernel<<<1, (unsigned)c->small_threads, cs, c->stream>>>(a);
       c->check_launch();
     }
-    size_t smem = small_smem_bytes(x.m, x.n, threshold);
-    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    small_pluq_kernel<<<1, (unsigned)c->small_threads, smem, c->stream>>>(a, a.fail_list, a.fail_count);
-    c->check_launch();
+    launch_exact(c, a, 1, (unsigned)c->small_threads, a.fail_list, a.fail_count, c->stream);
     ++c->st_small;
     NodeRes res = readback(x.m, x.n, 1);
     if (a.try_generic && c->h_res[x.m + x.n + 1]) {  // generic leaf: charges in closed form
@@ -816,6 +865,9 @@ int pluq_destroy(pluq_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->tc.release();
   if (c->pin) cudaFreeHost(c->pin);
+  if (c->h_bres) cudaFreeHost(c->h_bres);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  for (auto s : c->side) if (s) cudaStreamDestroy(s);
   if (c->d_res) cudaFree(c->d_res);
   if (c->h_res) cudaFreeHost(c->h_res);
   if (c->d_counts) cudaFree(c->d_counts);
@@ -850,6 +902,10 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "try_generic") c->try_generic = value;
   else if (k == "time_kernels") c->time_kernels = value;
   else if (k == "fixed_kernels") c->fixed_kernels = value;
+  else if (k == "host_chunks") c->host_chunks = value;
+  else if (k == "exact_kernel") c->exact_kernel = value;
+  else if (k == "rpm_threads") c->rpm_threads = value;
+  else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;
   else if (k == "spec_panel") c->spec_panel = value;
@@ -892,7 +948,7 @@ int pluq_factor_iterative(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int6
 }
 
 int64_t pluq_batched_max_elems(pluq_ctx*, int64_t m, int64_t n) {
-  return small_smem_bytes(m, n, 30) <= 227 * 1024 ? m * n : 0;
+  return block_smem_bytes(m, n, 30) <= 227 * 1024 ? m * n : 0;
 }
 
 int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch, int64_t m, int64_t n,
@@ -900,7 +956,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
                         uint64_t* d_counts) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (small_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
+  if (block_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
   if (batch == 0) return kOk;
   return guarded(c, [&] {
     SmallArgs a;
@@ -920,8 +976,6 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     a.generic_counts = gtab;
     int* flags = nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
-    size_t smem = small_smem_bytes(m, n, threshold);
-    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (a.try_generic) {
       flags = c->dalloc<int>((size_t)batch + 1 + (size_t)batch);
       a.generic_flag = flags;
@@ -940,7 +994,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       if (c->time_kernels) CU(cudaEventRecord(ev[1], c->stream));
       // exact recursion only for the blocks that are not generic (persistent grid)
       const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 2);
-      small_pluq_kernel<<<grid, (unsigned)c->batch_threads, smem, c->stream>>>(a, a.fail_list, a.fail_count);
+      launch_exact(c, a, grid, (unsigned)c->batch_threads, a.fail_list, a.fail_count, c->stream);
       if (c->time_kernels) {
         CU(cudaEventRecord(ev[2], c->stream));
         CU(cudaEventSynchronize(ev[2]));
@@ -949,9 +1003,8 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
         for (auto& e : ev) cudaEventDestroy(e);
       }
     } else {
-      small_pluq_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, smem, c->stream>>>(a, nullptr, nullptr);
+      launch_exact(c, a, (unsigned)batch, (unsigned)c->batch_threads, nullptr, nullptr, c->stream);
     }
-    c->check_launch();
     if (!d_counts) c->dfree(cnt);
     if (gtab) c->dfree(gtab);
     if (flags) c->dfree(flags);
@@ -1001,7 +1054,8 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
                                  int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* ranks) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (small_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
+  if (block_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
+  const auto hentry = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     const int64_t mn = m * n;
     if (batch == 0 || mn == 0) {
@@ -1012,22 +1066,39 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       }
       return;
     }
-    // Chunked pipeline: H2D of chunk k+1, factorization of chunk k and D2H of chunk k-1
-    // overlap on three streams (two copy engines + compute).
-    const int64_t nchunks = std::min<int64_t>(8, batch);
+    // Chunked pipeline on four streams: H2D of chunk k+1 (sin), the generic kernel of
+    // chunk k (compute), the exact recursion over chunk k's few non-generic blocks plus
+    // the f64 conversion (sfb: a handful of CTAs, latency-bound, so it overlaps the next
+    // chunk's generic kernel), and D2H of chunk k-1 (sout).
+    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(c->host_chunks, batch));
     const int64_t per = (batch + nchunks - 1) / nchunks;
     double* raw = c->dalloc<double>((size_t)batch * mn);
     uint32_t* dA = c->dalloc<uint32_t>((size_t)batch * mn);
     int32_t* dp = c->dalloc<int32_t>((size_t)(batch * (m + n + 1)));
     CU(cudaStreamSynchronize(c->stream));  // allocations visible to the side streams
-    cudaStream_t sin, sout;
-    CU(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
-    CU(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev_in(nchunks), ev_done(nchunks);
-    for (int64_t k = 0; k < nchunks; ++k) {
-      CU(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
-      CU(cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming));
+    // the exact kernel of a chunk is a few latency-bound CTAs: round-robin them over
+    // several streams so that the fallbacks of consecutive chunks overlap
+    constexpr int kFb = 4;
+    cudaStream_t* ss = c->side_streams();
+    cudaStream_t sin = ss[0], sout = ss[1], *sfbs = ss + 2;
+    const bool tr = c->trace_pipeline != 0;
+    // events: in / generic / done / out per chunk, + start/end (timing-enabled when tracing)
+    std::vector<cudaEvent_t> tev;
+    cudaEvent_t* evs;
+    if (tr) {
+      tev.resize(5 * nchunks + 2);
+      for (auto& e : tev) CU(cudaEventCreate(&e));
+      evs = tev.data();
+    } else {
+      evs = c->events(5 * nchunks + 2);
     }
+    cudaEvent_t *ev_in = evs, *ev_gen = evs + nchunks, *ev_done = evs + 2 * nchunks, *ev_out = evs + 3 * nchunks;
+    cudaEvent_t *ev_res = evs + 4 * nchunks;
+    cudaEvent_t ev0 = evs[5 * nchunks], ev_end = evs[5 * nchunks + 1];
+    // per-block results (P, Q, rank) come back per chunk into pinned memory and are
+    // widened to the caller's int64 arrays while later chunks are still in flight
+    int32_t* host = c->batch_results((size_t)(batch * (m + n + 1)));
+    const auto h0 = std::chrono::steady_clock::now();
     const ModP mp = ModP::make((uint32_t)p);
     SmallArgs a;
     a.lda = n; a.bstride = mn; a.m = (int)m; a.n = (int)n;
@@ -1040,20 +1111,20 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     a.generic_counts = gtab;
     unsigned long long* cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
     a.cnt_accumulate = 0;
-    const size_t smem = small_smem_bytes(m, n, threshold);
-    CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const size_t cs = crout_smem_bytes(m, n);
     CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
-    int* flags = a.try_generic ? c->dalloc<int>(2 * (size_t)batch + 1) : nullptr;
+    // flags: per-block generic flag [batch] | per-chunk failure count [nchunks] | failure
+    // list [batch] (chunk k lists its failures, as global indices, from slot k*per on)
+    int* flags = a.try_generic ? c->dalloc<int>(2 * (size_t)batch + nchunks) : nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
-    if (flags) {
-      a.fail_count = flags + batch;
-      a.fail_list = flags + batch + 1;
-      CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
-    }
+    if (flags) CU(cudaMemsetAsync(flags + batch, 0, sizeof(int) * nchunks, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaEventRecord(ev0, sin));
+    int64_t last = 0;
     for (int64_t k = 0; k < nchunks; ++k) {
       const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
       if (nb <= 0) break;
+      last = k;
       CU(cudaMemcpyAsync(raw + b0 * mn, hA + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyHostToDevice, sin));
       CU(cudaEventRecord(ev_in[k], sin));
       CU(cudaStreamWaitEvent(c->stream, ev_in[k], 0));
@@ -1064,37 +1135,63 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       a.a = dA + b0 * mn;
       a.p_out = dp + b0 * m; a.q_out = dp + batch * m + b0 * n; a.r_out = dp + batch * (m + n) + b0;
       a.cnt_out = cnt + 4 * b0;
+      cudaStream_t tail = c->stream;
       if (flags) {
         a.generic_flag = flags + b0;
         a.fail_base = (int)b0;
+        a.fail_count = flags + batch + k;
+        a.fail_list = flags + batch + nchunks + b0;
         if (!(c->fixed_kernels && launch_crout_fixed(a, nb, c->stream)))
           crout_fast_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, cs, c->stream>>>(a);
         c->check_launch();
+        CU(cudaEventRecord(ev_gen[k], c->stream));
+        cudaStream_t sfb = sfbs[k % kFb];
+        CU(cudaStreamWaitEvent(sfb, ev_gen[k], 0));
         // failures are listed with global indices: run them with the chunk base at 0
         SmallArgs g = a;
         g.a = dA; g.p_out = dp; g.q_out = dp + batch * m; g.r_out = dp + batch * (m + n);
         g.cnt_out = cnt; g.generic_flag = nullptr;
-        small_pluq_kernel<<<(unsigned)std::min<int64_t>(nb, 148 * 2), (unsigned)c->batch_threads, smem, c->stream>>>(
-            g, a.fail_list, a.fail_count);
-        CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+        launch_exact(c, g, (unsigned)std::min<int64_t>(nb, 148 * 2), (unsigned)c->batch_threads, a.fail_list,
+                     a.fail_count, sfb);
+        tail = sfb;
       } else {
-        small_pluq_kernel<<<(unsigned)nb, (unsigned)c->batch_threads, smem, c->stream>>>(a, nullptr, nullptr);
+        launch_exact(c, a, (unsigned)nb, (unsigned)c->batch_threads, nullptr, nullptr, c->stream);
       }
+      to_f64_kernel<<<grid, 256, 0, tail>>>(dA + b0 * mn, raw + b0 * mn, cntk);
       c->check_launch();
-      to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA + b0 * mn, raw + b0 * mn, cntk);
-      c->check_launch();
-      CU(cudaEventRecord(ev_done[k], c->stream));
+      CU(cudaEventRecord(ev_done[k], tail));
       CU(cudaStreamWaitEvent(sout, ev_done[k], 0));
       CU(cudaMemcpyAsync(hA + b0 * mn, raw + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyDeviceToHost, sout));
+      CU(cudaEventRecord(ev_out[k], sout));
+      CU(cudaMemcpyAsync(host + b0 * m, dp + b0 * m, (size_t)nb * m * 4, cudaMemcpyDeviceToHost, sout));
+      CU(cudaMemcpyAsync(host + batch * m + b0 * n, dp + batch * m + b0 * n, (size_t)nb * n * 4,
+                         cudaMemcpyDeviceToHost, sout));
+      CU(cudaMemcpyAsync(host + batch * (m + n) + b0, dp + batch * (m + n) + b0, (size_t)nb * 4,
+                         cudaMemcpyDeviceToHost, sout));
+      CU(cudaEventRecord(ev_res[k], sout));
     }
-    std::vector<int32_t> host((size_t)(batch * (m + n + 1)));
-    CU(cudaStreamWaitEvent(sout, ev_done[nchunks - 1], 0));
-    CU(cudaMemcpyAsync(host.data(), dp, host.size() * 4, cudaMemcpyDeviceToHost, sout));
+    CU(cudaEventRecord(ev_end, sout));
+    for (int64_t k = 0; k <= last; ++k) {
+      CU(cudaEventSynchronize(ev_res[k]));
+      const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
+      for (int64_t i = b0 * m; i < (b0 + nb) * m; ++i) psig[i] = host[i];
+      for (int64_t i = b0 * n; i < (b0 + nb) * n; ++i) qsig[i] = host[batch * m + i];
+      for (int64_t i = b0; i < b0 + nb; ++i) ranks[i] = host[batch * (m + n) + i];
+    }
     CU(cudaStreamSynchronize(sout));
     CU(cudaStreamSynchronize(c->stream));
-    for (int64_t k = 0; k < nchunks; ++k) { cudaEventDestroy(ev_in[k]); cudaEventDestroy(ev_done[k]); }
-    cudaStreamDestroy(sin);
-    cudaStreamDestroy(sout);
+    for (int q = 0; q < kFb; ++q) CU(cudaStreamSynchronize(sfbs[q]));
+    const auto h1 = std::chrono::steady_clock::now();
+    if (tr) {
+      auto ms = [&](cudaEvent_t e) { float v = 0.f; cudaEventElapsedTime(&v, ev0, e); return v; };
+      fprintf(stderr, "pipeline: setup %.3f ms, enqueue+wait %.3f ms, device end %.3f ms\n",
+              std::chrono::duration<double, std::milli>(h0 - hentry).count(),
+              std::chrono::duration<double, std::milli>(h1 - h0).count(), ms(ev_end));
+      for (int64_t k = 0; k <= last; ++k)
+        fprintf(stderr, "  chunk %lld: h2d %.3f gen %.3f done %.3f d2h %.3f\n", (long long)k, ms(ev_in[k]),
+                ms(ev_gen[k]), ms(ev_done[k]), ms(ev_out[k]));
+      for (auto e : tev) cudaEventDestroy(e);
+    }
     c->dfree(cnt);
     if (gtab) c->dfree(gtab);
     if (flags) c->dfree(flags);
@@ -1102,9 +1199,9 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     c->dfree(dA);
     c->dfree(raw);
     c->sync();
-    for (int64_t i = 0; i < batch * m; ++i) psig[i] = host[i];
-    for (int64_t i = 0; i < batch * n; ++i) qsig[i] = host[batch * m + i];
-    for (int64_t i = 0; i < batch; ++i) ranks[i] = host[batch * (m + n) + i];
+    if (tr)
+      fprintf(stderr, "pipeline: frees %.3f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
   });
 }
 

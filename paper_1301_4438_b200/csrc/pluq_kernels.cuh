@@ -1,6 +1,7 @@
 // Global-memory kernels used by the host recursion driver and the C ABI.
 #pragma once
 #include "pluq_small.cuh"
+#include "pluq_rpm.cuh"
 
 namespace pluq {
 
@@ -96,6 +97,111 @@ __device__ void small_pluq_block(const SmallArgs& args, int blk) {
     }
   }
 }
+
+// Exact PLUQ of one block through its rank profile matrix (pluq_rpm.cuh): same outputs
+// as small_pluq_block, three short phases instead of the field-arithmetic recursion.
+__device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
+  extern __shared__ __align__(16) uint32_t smem_dyn[];
+  __shared__ Counts s_cnt;
+  __shared__ int s_r;
+  const int m = args.m, n = args.n, ld = n, mn = min(m, n);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  uint32_t* ga = args.a + (int64_t)blk * args.bstride;
+#ifdef PLUQ_TRACE
+  long long tr[6];
+#define RPM_MARK(i) do { if (tid == 0) tr[i] = clock64(); } while (0)
+#else
+#define RPM_MARK(i) do { } while (0)
+#endif
+  RPM_MARK(0);
+  uint32_t* W = smem_dyn;
+  int* rp = reinterpret_cast<int*>(W + (int64_t)m * n);
+  int* cp = rp + m; int* rpos = cp + n; int* cpos = rpos + m;
+  int* P = cpos + n; int* Q = P + m; int* pinv = Q + n; int* rows = pinv + m; int* cols = rows + m;
+  uint32_t* dinv = reinterpret_cast<uint32_t*>(cols + n);
+  uint32_t* dpre = dinv + mn;
+  uint32_t* diag = dpre + mn;
+  uint32_t* rowbuf = diag + mn;
+  int* stk = reinterpret_cast<int*>(rowbuf + 256);
+  // register-resident phases when the block fits (n <= 64 with <= 4 rows per warp, or
+  // n <= 128 with <= 8 rows per warp), shared-memory phases otherwise
+  const int shape = (n <= 64 && m <= 4 * nw) ? 1 : (n <= 128 && m <= 8 * nw) ? 2 : 0;
+  for (int t = tid; t < m; t += nt) rows[t] = t;
+  for (int t = tid; t < n; t += nt) cols[t] = t;
+  if (shape == 0) {
+    for (int i = w; i < m; i += nw)
+      for (int j = lane; j < n; j += 32) W[i * ld + j] = ga[(int64_t)i * args.lda + j];
+  }
+  __syncthreads();
+  RPM_MARK(1);
+  int r;
+  if (shape == 1) r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  else if (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
+  RPM_MARK(2);
+  if (tid < 32) {
+    SymCtx s{rp, cp, rpos, cpos, args.threshold, {0, 0, 0, 0}};
+    const int rs = sym_rec(rows, cols, m, n, P, Q, stk, s);
+    if (lane == 0) { s_cnt = s.cnt; s_r = rs; }
+  }
+  __syncthreads();
+  RPM_MARK(3);
+  if (s_r != r) __trap();  // the replay must find exactly the pivots of R_A
+  for (int t = tid; t < m; t += nt) pinv[P[t]] = t;
+  __syncthreads();
+  RPM_MARK(4);
+  const bool inv = args.invtab != nullptr;
+  if (shape == 1) {
+    if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+    else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+  } else if (shape == 2) {
+    if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+    else lu_reg<4, 8, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+  } else {
+    for (int t = w; t < m; t += nw) {  // A'[t][u] = A[P^-1(t)][Q(u)]
+      const uint32_t* src = ga + (int64_t)pinv[t] * args.lda;
+      for (int u = lane; u < n; u += 32) W[t * ld + u] = src[Q[u]];
+    }
+    ff_lu_generic(W, ld, m, n, r, args.mp, args.invtab, dinv, dpre);
+    for (int i = w; i < m; i += nw)
+      for (int j = lane; j < n; j += 32) ga[(int64_t)i * args.lda + j] = W[i * ld + j];
+  }
+  RPM_MARK(5);
+  int* po = args.p_out + (int64_t)blk * m;
+  int* qo = args.q_out + (int64_t)blk * n;
+  for (int t = tid; t < m; t += nt) po[t] = P[t];
+  for (int t = tid; t < n; t += nt) qo[t] = Q[t];
+  if (tid == 0) {
+    args.r_out[blk] = r;
+    unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blk);
+    if (args.cnt_accumulate) {
+      atomicAdd(co + 0, s_cnt.mul); atomicAdd(co + 1, s_cnt.add);
+      atomicAdd(co + 2, s_cnt.inv); atomicAdd(co + 3, s_cnt.red);
+    } else {
+      co[0] = s_cnt.mul; co[1] = s_cnt.add; co[2] = s_cnt.inv; co[3] = s_cnt.red;
+    }
+  }
+#ifdef PLUQ_TRACE
+  if (tid == 0)
+    printf("RPM blk %d r=%d shape=%d stage=%lld rows=%lld sym=%lld pinv=%lld lu=%lld total=%lld\n", blk, r, shape,
+           tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4], clock64() - tr[0]);
+#endif
+}
+
+// One CTA per block, or a persistent grid over the failure list of the generic kernel.
+__global__ void __launch_bounds__(512) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+  if (fail_list) {
+    const int cnt = *fail_count;
+    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+      rpm_pluq_block(args, fail_list[q]);
+      __syncthreads();
+    }
+    return;
+  }
+  rpm_pluq_block(args, blockIdx.x);
+}
+
+inline size_t rpm_smem_bytes(int64_t m, int64_t n) { return (size_t)rpm_smem_words(m, n) * 4; }
 
 // Dynamic shared memory of small_pluq_kernel: block (odd pitch) + P/Q + recursion stack.
 // Lean generic-profile kernel (no recursion compiled in, so few registers and many
@@ -200,7 +306,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
           acc2 += (uint64_t)ri[kk + 1] * cj[(kk + 1) * LD];
         }
         for (; kk < kend; ++kk) acc += (uint64_t)ri[kk] * cj[kk * LD];
-        acc = (uint64_t)reduce64(acc, mp) + reduce64(acc2, mp);
+        acc += acc2;  // kFast: <= MN products of (p-1)^2 plus one more term fit in 64 bits
       } else {
         for (; kk < kend; ++kk) acc = reduce64(acc + (uint64_t)ri[kk] * cj[kk * LD], mp);
       }
@@ -285,7 +391,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
 // applies, otherwise the runtime-shape kernel.
 inline bool launch_crout_fixed(const SmallArgs& a, int64_t batch, cudaStream_t st) {
   if (a.m == 64 && a.n == 64) {
-    if (a.mp.kchunk >= 64) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    if (a.mp.kchunk >= 66) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else crout_fixed_kernel<64, 64, 128, false><<<(unsigned)batch, 128, 0, st>>>(a);
     return true;
   }

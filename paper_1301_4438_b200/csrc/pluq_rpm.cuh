@@ -1,0 +1,461 @@
+// Rank-profile fallback for blocks whose rank profile is not generic.
+//
+// The reference recursion (Algorithm 1, recursive.py:186-256, with the Algorithm 2
+// base case iterative.py:23-91) is rank-profile revealing, and its whole output is a
+// function of the rank profile matrix R_A (the 0/1 partial permutation with a one at
+// every pivot position, SPEC.md "rank profile matrix"):
+//
+//   (1) P, Q, rank and the charged OpCounts of Alg.1 on A equal those of Alg.1 on R_A;
+//   (2) the packed factors of A are the unpivoted LU of A' = P^T A Q^T
+//       (A'[t][u] = A[P^-1(t)][Q(u)]), whose leading minors 1..r are nonzero.
+//
+// tests/test_rpm_fallback.py pins (1) and (2) against the oracle on thousands of random
+// non-generic inputs (all thresholds, tiny primes, rank-deficient and sparse blocks).
+// So instead of replaying the deep recursion with field arithmetic (hundreds of
+// latency-bound barrier phases per 64x64 block), a block is finished in three short
+// phases:
+//   a) row-order elimination in shared memory -> R_A (pivot of row i = first nonzero
+//      of row i once the earlier pivots are eliminated), one barrier per row;
+//   b) Alg.1 replayed symbolically on R_A by one warp (index lists only: a partial
+//      permutation has no fill, so every TRSM/GEMM of the recursion is the identity
+//      on its pattern) -> P, Q, rank, OpCounts;
+//   c) fraction-free right-looking LU of A' (gathered straight from global memory),
+//      normalised once at the end with all inverses computed in parallel.
+#pragma once
+#include "pluq_small.cuh"
+
+namespace pluq {
+
+// a) R_A by row-order elimination.  W: m x n block in shared memory (pitch ld), destroyed.
+// rp[i] = column of row i's pivot (-1 if none), cp[j] = row of column j's pivot.
+// Warp w owns the rows k with k % nw == w, lanes run over columns; fraction-free update
+// row_k <- piv * row_k - W[k][j] * row_i keeps the zero pattern exact without inverses.
+__device__ int rpm_rows(uint32_t* W, int ld, int m, int n, const ModP mp, int* rp, int* cp) {
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  for (int t = tid; t < m; t += nt) rp[t] = -1;
+  for (int t = tid; t < n; t += nt) cp[t] = -1;
+  int r = 0;
+  for (int i = 0; i < m && r < n; ++i) {
+    __syncthreads();  // row i is final
+    const uint32_t* ri = W + i * ld;
+    int j = -1;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+      const int c = c0 + lane;
+      const unsigned bb = __ballot_sync(FULL, c < n && ri[c] != 0u);
+      if (bb) { j = c0 + __ffs(bb) - 1; break; }
+    }
+    if (j < 0) continue;  // zero row (uniform: every warp scanned the same row)
+    if (tid == 0) { rp[i] = j; cp[j] = i; }
+    ++r;
+    const uint32_t piv = ri[j];
+    const int first = i + 1 + (((w - (i + 1)) % nw) + nw) % nw;
+    for (int k = first; k < m; k += nw) {
+      uint32_t* rk = W + k * ld;
+      const uint32_t f = rk[j];
+      if (f == 0u) continue;  // row k untouched: its own scale stays consistent
+      __syncwarp();  // every lane has read f before the lane owning column j clears it
+      // the WHOLE row is scaled by piv (row i is zero left of j, so those columns only scale)
+      for (int c = lane; c < n; c += 32)
+        rk[c] = c < j ? mulmod(piv, rk[c], mp) : c == j ? 0u : submod(mulmod(piv, rk[c], mp), mulmod(f, ri[c], mp), mp);
+    }
+  }
+  __syncthreads();
+  return r;
+}
+
+// b) Symbolic Alg.1 on R_A, executed by one converged warp.
+struct SymCtx {
+  const int* rp;   // original row -> original column of its one (or -1)
+  const int* cp;   // original column -> original row of its one (or -1)
+  int* rpos;       // scratch: local index of an original row inside the current base case
+  int* cpos;       // scratch: local index of an original column inside the current base case
+  int thr;
+  Counts cnt;      // lane 0 accumulates
+};
+
+// Alg.2 (iterative.py:23-91) on the partial permutation restricted to rows x cols (both
+// lists of original indices in local order).  P[local row] = position, Q[position] =
+// local column, pivots first then the rest in local order (iterative.py:82-91).  On a
+// partial permutation the frontier walk needs no pivot flags: a row (column) at the
+// frontier can only be matched with its own single one.
+__device__ int sym_base(const int* rows, const int* cols, int m, int n, int* P, int* Q, int* stk,
+                        SymCtx& s) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  for (int a = lane; a < m; a += 32) s.rpos[rows[a]] = a;
+  for (int b = lane; b < n; b += 32) s.cpos[cols[b]] = b;
+  __syncwarp();
+  int* lr = stk; int* lc = lr + m; int* ro = lc + n; int* co = ro + min(m, n);
+  for (int a = lane; a < m; a += 32) {
+    const int x = s.rp[rows[a]];
+    int b = -1;
+    if (x >= 0) {
+      const int q = s.cpos[x];
+      if ((unsigned)q < (unsigned)n && cols[q] == x) b = q;  // stale scratch entries fail the check
+    }
+    lr[a] = b;
+  }
+  for (int b = lane; b < n; b += 32) {
+    const int y = s.cp[cols[b]];
+    int a = -1;
+    if (y >= 0) {
+      const int q = s.rpos[y];
+      if ((unsigned)q < (unsigned)m && rows[q] == y) a = q;
+    }
+    lc[b] = a;
+  }
+  __syncwarp();
+  int r = 0;
+  if (lane == 0) {
+    int i = 0, j = 0;
+    while (i < m || j < n) {
+      int pr = -1, pc = -1;
+      if (j < n) {  // column segment above the frontier (iterative.py:40-44)
+        const int a = lc[j];
+        if (a >= 0 && a < i) { pr = a; pc = j; ++j; }
+      }
+      if (pr < 0 && i < m) {  // row segment left of the frontier, then the corner (:45-53)
+        const int b = lr[i];
+        if (b >= 0 && b < j) { pr = i; pc = b; ++i; }
+        else if (j < n && b == j) { pr = i; pc = j; ++i; ++j; }
+      }
+      if (pr < 0) { i = min(i + 1, m); j = min(j + 1, n); continue; }  // (:54-57)
+      ro[r] = pr; co[r] = pc; ++r;
+    }
+  }
+  r = __shfl_sync(FULL, r, 0);
+  __syncwarp();
+  // charges of iterative.py:59-75 per pivot, from the pivots that precede it
+  unsigned long long cm = 0, ca = 0, ci = 0;
+  for (int k = lane; k < r; k += 32) {
+    const int pr = ro[k], pc = co[k];
+    int below = m - 1 - pr, right = n - 1 - pc;
+    for (int t = 0; t < k; ++t) { below -= ro[t] > pr; right -= co[t] > pc; }
+    if (below > 0) {
+      const unsigned long long br = (unsigned long long)below * right;
+      ci += 1; cm += below + br; ca += br;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    cm += __shfl_xor_sync(FULL, cm, o);
+    ca += __shfl_xor_sync(FULL, ca, o);
+    ci += __shfl_xor_sync(FULL, ci, o);
+  }
+  if (lane == 0) { s.cnt.mul += cm; s.cnt.add += ca; s.cnt.inv += ci; s.cnt.red += cm; }
+  for (int x = lane; x < m; x += 32) {
+    int pos = -1, before = 0;
+    for (int t = 0; t < r; ++t) { pos = ro[t] == x ? t : pos; before += ro[t] < x; }
+    P[x] = pos >= 0 ? pos : r + x - before;
+  }
+  for (int x = lane; x < n; x += 32) {
+    int pos = -1, before = 0;
+    for (int t = 0; t < r; ++t) { pos = co[t] == x ? t : pos; before += co[t] < x; }
+    Q[pos >= 0 ? pos : r + x - before] = x;
+  }
+  __syncwarp();
+  return r;
+}
+
+// Alg.1 (recursive.py:186-256) on the index lists.  With R_A's pattern the updates
+// D, E vanish and F, G, H are the untouched sub-patterns, so a node only reorders its
+// row/column lists by the children's permutations and composes P, Q exactly like
+// rec_smem; the OpCounts charges are the same closed forms.
+__device__ int sym_rec(const int* rows, const int* cols, int m, int n, int* P, int* Q, int* stk,
+                       SymCtx& s) {
+  const int lane = threadIdx.x & 31;
+  if (m == 0 || n == 0) {
+    for (int a = lane; a < m; a += 32) P[a] = a;
+    for (int b = lane; b < n; b += 32) Q[b] = b;
+    __syncwarp();
+    return 0;
+  }
+  if (m == 1 || n == 1 || min(m, n) <= s.thr) return sym_base(rows, cols, m, n, P, Q, stk, s);
+  const int kr = m / 2, kc = n / 2;
+  int* P1 = stk; int* Q1 = P1 + kr; int* top = Q1 + kc;
+  const int r1 = sym_rec(rows, cols, kr, kc, P1, Q1, top, s);
+  int* rt = top; int* cl = rt + kr; top = cl + kc;  // P1^T-ordered top rows, Q1-ordered left columns
+  for (int a = lane; a < kr; a += 32) rt[P1[a]] = rows[a];
+  for (int t = lane; t < kc; t += 32) cl[t] = cols[Q1[t]];
+  __syncwarp();
+  if (lane == 0) {
+    charge_trsm_l(s.cnt, r1, n - kc);
+    charge_trsm_u(s.cnt, m - kr, r1);
+    charge_mm(s.cnt, kr - r1, n - kc, r1);
+    charge_mm(s.cnt, m - kr, kc - r1, r1);
+    charge_mm(s.cnt, m - kr, n - kc, r1);
+  }
+  int* P2 = top; int* Q2 = P2 + (kr - r1); top = Q2 + (n - kc);
+  const int r2 = sym_rec(rt + r1, cols + kc, kr - r1, n - kc, P2, Q2, top, s);
+  int* P3 = top; int* Q3 = P3 + (m - kr); top = Q3 + (kc - r1);
+  const int r3 = sym_rec(rows + kr, cl + r1, m - kr, kc - r1, P3, Q3, top, s);
+  int* hr = top; int* hc = hr + (m - kr); top = hc + (n - kc);
+  for (int a = lane; a < m - kr; a += 32) hr[P3[a]] = rows[kr + a];
+  for (int t = lane; t < n - kc; t += 32) hc[t] = cols[kc + Q2[t]];
+  __syncwarp();
+  const int m4 = m - kr - r3, n4 = n - kc - r2;
+  if (lane == 0) {
+    charge_trsm_u(s.cnt, r3, r2);
+    charge_trsm_l(s.cnt, r3, r2);
+    charge_trsm_u(s.cnt, m4, r2);
+    charge_trsm_l(s.cnt, r3, n4);
+    charge_mm(s.cnt, r3, n4, r2);
+    charge_mm(s.cnt, m4, n4, r2);
+    charge_mm(s.cnt, m4, n4, r3);
+  }
+  int* P4 = top; int* Q4 = P4 + m4; top = Q4 + n4;
+  const int r4 = sym_rec(hr + r3, hc + r2, m4, n4, P4, Q4, top, s);
+  // P = Diag(P1 Diag(I,P2), P3 Diag(I,P4)) S ; Q = T Diag(Diag(I,Q3) Q1, Diag(I,Q4) Q2)
+  for (int t = lane; t < m; t += 32) {
+    int y;
+    if (t < kr) { const int z = P1[t]; y = z < r1 ? z : r1 + P2[z - r1]; }
+    else { const int z = P3[t - kr]; y = kr + (z < r3 ? z : r3 + P4[z - r3]); }
+    P[t] = s_sigma(y, r1, r2, r3, r4, kr);
+  }
+  for (int t = lane; t < n; t += 32) {
+    const int z = t_sigma(t, r1, r2, r3, r4, kc);
+    int y;
+    if (z < kc) { const int w = z < r1 ? z : r1 + Q3[z - r1]; y = Q1[w]; }
+    else { const int zz = z - kc; const int w = zz < r2 ? zz : r2 + Q4[zz - r2]; y = kc + Q2[w]; }
+    Q[t] = y;
+  }
+  __syncwarp();
+  return r1 + r2 + r3 + r4;
+}
+
+// Words of the symbolic recursion stack for an m x n block (children need at most half
+// the parent's lists, plus the base case's lr/lc/ro/co).
+__host__ __device__ inline int64_t sym_stack_words(int64_t m, int64_t n) {
+  return 12 * (m + n) + 64;
+}
+
+// c) Fraction-free right-looking LU of the generic block W (r pivots on the diagonal),
+// then L[k][s] = W[k][s] / W[s][s] and U[s][c] = W[s][c] / prod_{t<s} W[t][t].
+// dinv, dpre: r words of scratch each.
+__device__ void ff_lu_generic(uint32_t* W, int ld, int m, int n, int r, const ModP mp,
+                              const uint16_t* invtab, uint32_t* dinv, uint32_t* dpre) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  for (int s = 0; s < r; ++s) {
+    __syncthreads();  // row s is final
+    const uint32_t* ps = W + s * ld;
+    const uint32_t piv = ps[s];
+    if (piv == 0u) __trap();  // impossible for A' = P^T A Q^T (leading minors nonzero)
+    const int first = s + 1 + (((w - (s + 1)) % nw) + nw) % nw;
+    for (int k = first; k < m; k += nw) {
+      uint32_t* rk = W + k * ld;
+      const uint32_t f = rk[s];
+      // every trailing row is scaled by piv, even when f == 0, so that rows k and s carry
+      // the same factor prod_{t<s} W[t][t] at step s (L[k][s] = W[k][s] / W[s][s])
+      if (f == 0u) {
+        for (int c = s + 1 + lane; c < n; c += 32) rk[c] = mulmod(piv, rk[c], mp);
+      } else {
+        for (int c = s + 1 + lane; c < n; c += 32)
+          rk[c] = submod(mulmod(piv, rk[c], mp), mulmod(f, ps[c], mp), mp);
+      }
+    }
+  }
+  __syncthreads();
+  for (int s = tid; s < r; s += nt) dinv[s] = pivot_inverse(W[s * ld + s], mp, invtab);
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 1u;
+    for (int s = 0; s < r; ++s) { dpre[s] = acc; acc = mulmod(acc, dinv[s], mp); }
+  }
+  __syncthreads();
+  for (int k = w; k < m; k += nw) {
+    uint32_t* rk = W + k * ld;
+    const uint32_t us = k < r ? dpre[k] : 0u;
+    for (int c = lane; c < n; c += 32) {
+      if (c >= k) { if (k < r && us != 1u) rk[c] = mulmod(rk[c], us, mp); }
+      else if (c < r) rk[c] = mulmod(rk[c], dinv[c], mp);
+    }
+  }
+  __syncthreads();
+}
+
+// ---- register-resident variants of a) and c) (blocks up to 32*NQ columns and NR rows
+// per warp: the hot case).  Warp w holds rows k = w + nw*t, lane holds columns
+// c = lane + 32*q; the row being eliminated is broadcast through a double-buffered
+// shared row and the multipliers through __shfl_sync, so a step costs one barrier and
+// touches no shared memory for the rows a warp owns.
+template <int NQ>
+__device__ __forceinline__ uint32_t lane_pick(const uint32_t (&v)[NQ], int q) {
+  uint32_t x = v[0];
+#pragma unroll
+  for (int u = 1; u < NQ; ++u) x = q == u ? v[u] : x;
+  return x;
+}
+
+// the owner warp of row k publishes it into rowbuf (32*NQ words)
+template <int NQ, int NR>
+__device__ __forceinline__ void publish_row(const uint32_t (&a)[NR][NQ], int k, uint32_t* rowbuf) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (k % nw != w) return;
+  const int tk = k / nw;
+#pragma unroll
+  for (int t = 0; t < NR; ++t)
+    if (t == tk) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) rowbuf[lane + 32 * q] = a[t][q];
+    }
+}
+
+template <int NQ, int NR>
+__device__ int rpm_rows_reg(const uint32_t* ga, int64_t lda, int m, int n, const ModP mp, int* rp, int* cp,
+                            uint32_t* rowbuf) {
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  uint32_t a[NR][NQ];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + nw * t;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      a[t][q] = (k < m && c < n) ? ga[(int64_t)k * lda + c] : 0u;
+    }
+  }
+  for (int t = tid; t < m; t += nt) rp[t] = -1;
+  for (int t = tid; t < n; t += nt) cp[t] = -1;
+  publish_row<NQ, NR>(a, 0, rowbuf);
+  int r = 0;
+  for (int i = 0; i < m && r < n; ++i) {
+    __syncthreads();  // row i published
+    const uint32_t* ri = rowbuf + (i & 1) * (32 * NQ);
+    uint32_t rv[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) rv[q] = ri[lane + 32 * q];
+    int j = -1;
+#pragma unroll
+    for (int q = NQ - 1; q >= 0; --q) {
+      const unsigned bb = __ballot_sync(FULL, rv[q] != 0u);
+      if (bb) j = 32 * q + __ffs(bb) - 1;
+    }
+    if (j >= 0) {
+      if (tid == 0) { rp[i] = j; cp[j] = i; }
+      ++r;
+      const int jq = j >> 5, jl = j & 31;
+      const uint32_t piv = __shfl_sync(FULL, lane_pick<NQ>(rv, jq), jl);
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const int k = w + nw * t;
+        const uint32_t f = __shfl_sync(FULL, lane_pick<NQ>(a[t], jq), jl);
+        if (k > i && f != 0u) {  // warp-uniform; rows >= m hold zeros
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int c = lane + 32 * q;
+            const uint32_t x = mulmod(piv, a[t][q], mp);
+            a[t][q] = c < j ? x : c == j ? 0u : submod(x, mulmod(f, rv[q], mp), mp);
+          }
+        }
+      }
+    }
+    if (i + 1 < m) publish_row<NQ, NR>(a, i + 1, rowbuf + ((i + 1) & 1) * (32 * NQ));
+  }
+  __syncthreads();
+  return r;
+}
+
+// c) on registers: A'[k][c] = A[pinv[k]][Q[c]] gathered from global, r pivot steps, the
+// packed factors written back to global.  kInv (p < 2^16): multipliers through the
+// inverse table, one product per element; else fraction-free with the final
+// normalisation of ff_lu_generic.
+template <int NQ, int NR, bool kInv>
+__device__ void lu_reg(uint32_t* ga, int64_t lda, int m, int n, int r, const int* pinv, const int* Q,
+                       const ModP mp, const uint16_t* invtab, uint32_t* rowbuf, uint32_t* diag, uint32_t* dinv,
+                       uint32_t* dpre) {
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  uint32_t a[NR][NQ];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + nw * t;
+    const uint32_t* src = k < m ? ga + (int64_t)pinv[k] * lda : ga;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      a[t][q] = (k < m && c < n) ? src[Q[c]] : 0u;
+    }
+  }
+  __syncthreads();  // every original row is in registers before any packed row is written
+  publish_row<NQ, NR>(a, 0, rowbuf);
+  for (int s = 0; s < r; ++s) {
+    __syncthreads();
+    const uint32_t* rs = rowbuf + (s & 1) * (32 * NQ);
+    uint32_t rv[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) rv[q] = rs[lane + 32 * q];
+    const int sq = s >> 5, sl = s & 31;
+    const uint32_t piv = __shfl_sync(FULL, lane_pick<NQ>(rv, sq), sl);
+    if (piv == 0u) __trap();  // impossible for A' (leading minors 1..r nonzero)
+    uint32_t inv = 0u;
+    if (kInv) inv = invtab[piv];
+    else if (tid == 0) diag[s] = piv;
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      const int k = w + nw * t;
+      const uint32_t f = __shfl_sync(FULL, lane_pick<NQ>(a[t], sq), sl);
+      if (k > s && k < m) {
+        if (kInv) {
+          if (f != 0u) {
+            const uint32_t l = mulmod(f, inv, mp);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const int c = lane + 32 * q;
+              if (c > s) a[t][q] = submod(a[t][q], mulmod(l, rv[q], mp), mp);
+              else if (c == s) a[t][q] = l;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int c = lane + 32 * q;
+            if (c > s) a[t][q] = submod(mulmod(piv, a[t][q], mp), mulmod(f, rv[q], mp), mp);
+          }
+        }
+      }
+    }
+    if (s + 1 < m) publish_row<NQ, NR>(a, s + 1, rowbuf + ((s + 1) & 1) * (32 * NQ));
+  }
+  if (!kInv) {
+    __syncthreads();
+    for (int s = tid; s < r; s += nt) dinv[s] = pivot_inverse(diag[s], mp, invtab);
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 1u;
+      for (int s = 0; s < r; ++s) { dpre[s] = acc; acc = mulmod(acc, dinv[s], mp); }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      const int k = w + nw * t;
+      if (k >= m) continue;
+      const uint32_t us = k < r ? dpre[k] : 1u;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        if (c >= n) continue;
+        if (c >= k) { if (k < r) a[t][q] = mulmod(a[t][q], us, mp); }
+        else if (c < r) a[t][q] = mulmod(a[t][q], dinv[c], mp);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + nw * t;
+    if (k >= m) continue;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      if (c < n) ga[(int64_t)k * lda + c] = a[t][q];
+    }
+  }
+}
+
+// Shared-memory words of rpm_pluq_block for an m x n block.
+__host__ __device__ inline int64_t rpm_smem_words(int64_t m, int64_t n) {
+  const int64_t mn = m < n ? m : n;
+  return m * n + 6 * (m + n) + 3 * mn + 256 + sym_stack_words(m, n) + 16;
+}
+
+}  // namespace pluq

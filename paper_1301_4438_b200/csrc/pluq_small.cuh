@@ -363,14 +363,32 @@ __device__ __forceinline__ int t_sigma(int x, int r1, int r2, int r3, int r4, in
 template <bool kCheckTrailing>
 __device__ int crout_generic(const View x, const ModP mp, const uint16_t* invtab, BcShared* sh);
 
+#ifdef PLUQ_TRACE
+#define TR_MARK(i) do { if (threadIdx.x == 0) tr[i] = clock64(); } while (0)
+#else
+#define TR_MARK(i) do { } while (0)
+#endif
 __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int depth = 0) {
   const int m = x.m, n = x.n;
+#ifdef PLUQ_TRACE
+  long long tr[10];
+  TR_MARK(0);
+#endif
   BcShared* sh = c.sh;
   if (m == 0 || n == 0) {
     cta_ident(P, m); cta_ident(Q, n); __syncthreads();
     return 0;
   }
-  if (m == 1 || n == 1 || min(m, n) <= c.threshold) return base_smem(x, P, Q, stk, c);
+  if (m == 1 || n == 1 || min(m, n) <= c.threshold) {
+#ifdef PLUQ_TRACE
+    const int rb = base_smem(x, P, Q, stk, c);
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+      printf("TRACE d%d base %dx%d r=%d cyc=%lld\n", depth, m, n, rb, clock64() - tr[0]);
+    return rb;
+#else
+    return base_smem(x, P, Q, stk, c);
+#endif
+  }
   if (c.try_generic && depth >= c.try_depth) {
     // generic-profile shortcut for the whole subtree (exact; see crout_generic)
     uint32_t* bk = reinterpret_cast<uint32_t*>(stk);
@@ -381,17 +399,23 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int
       cta_ident(P, m); cta_ident(Q, n);
       if (threadIdx.x == 0) generic_counts_dev(m, n, rg, c.threshold, *c.cnt);
       __syncthreads();
+#ifdef PLUQ_TRACE
+      if (threadIdx.x == 0 && blockIdx.x == 0)
+        printf("TRACE d%d generic-ok %dx%d r=%d cyc=%lld\n", depth, m, n, rg, clock64() - tr[0]);
+#endif
       return rg;
     }
     for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) x.at(idx / n, idx % n) = bk[idx];
     __syncthreads();
   }
+  TR_MARK(1);
   const int kr = m / 2, kc = n / 2;
   const ModP mp = c.mp;
   const bool t0 = threadIdx.x == 0;
 
   int* P1 = stk; int* Q1 = P1 + kr; int* top = Q1 + kc;
   const int r1 = rec_smem(x.sub(0, 0, kr, kc), P1, Q1, top, c, depth + 1);
+  TR_MARK(2);
   {
     int* g = top; int* scr = g + max(m, n);
     cta_inverse(P1, g, kr);
@@ -411,10 +435,12 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int
   // G and H share A = E: one pass over the contiguous column range r1..n
   cta_mm_sub(x.sub(kr, r1, m - kr, n - r1), x.sub(kr, 0, m - kr, r1), x.sub(0, r1, r1, n - r1), mp);
 
+  TR_MARK(3);
   int* P2 = top; int* Q2 = P2 + (kr - r1); top = Q2 + (n - kc);
   const int r2 = rec_smem(x.sub(r1, kc, kr - r1, n - kc), P2, Q2, top, c, depth + 1);
   int* P3 = top; int* Q3 = P3 + (m - kr); top = Q3 + (kc - r1);
   const int r3 = rec_smem(x.sub(kr, r1, m - kr, kc - r1), P3, Q3, top, c, depth + 1);
+  TR_MARK(4);
   {
     int* ip3 = top; int* ip2 = ip3 + (m - kr); int* scr = ip2 + (kr - r1);
     cta_inverse(P3, ip3, m - kr);
@@ -449,8 +475,10 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int
     charge_mm(*c.cnt, m4, n4, r3);
   }
 
+  TR_MARK(5);
   int* P4 = top; int* Q4 = P4 + m4; top = Q4 + n4;
   const int r4 = rec_smem(x.sub(kr + r3, kc + r2, m4, n4), P4, Q4, top, c, depth + 1);
+  TR_MARK(6);
   {
     int* ip4 = top; int* scr = ip4 + m4;
     cta_inverse(P4, ip4, m4);
@@ -480,6 +508,12 @@ __device__ int rec_smem(const View x, int* P, int* Q, int* stk, SmallCtx& c, int
     Q[t] = y;
   }
   __syncthreads();
+#ifdef PLUQ_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("TRACE d%d node %dx%d r=%d,%d,%d,%d attempt=%lld r1=%lld mid=%lld r23=%lld tail=%lld r4=%lld fin=%lld total=%lld\n",
+           depth, m, n, r1, r2, r3, r4, tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3],
+           tr[5] - tr[4], tr[6] - tr[5], clock64() - tr[6], clock64() - tr[0]);
+#endif
   return r1 + r2 + r3 + r4;
 }
 

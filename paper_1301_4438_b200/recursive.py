@@ -326,9 +326,9 @@ def pluq_batched(data, p: int, threshold: int = DEFAULT_THRESHOLD, with_counts: 
         raise ValueError("batched host data must be a contiguous (B, m, n) float64 array")
     bsz, m, n = arr.shape
     ctx = _native.context()
-    psig = np.zeros((bsz, m), dtype=np.int64)
-    qsig = np.zeros((bsz, n), dtype=np.int64)
-    ranks = np.zeros(bsz, dtype=np.int64)
+    psig = np.empty((bsz, m), dtype=np.int64)  # every entry is written by the call
+    qsig = np.empty((bsz, n), dtype=np.int64)
+    ranks = np.empty(bsz, dtype=np.int64)
     st = ctx.lib.pluq_factor_batched_host_f64(ctx.handle, arr.ctypes.data, bsz, m, n, p, threshold,
                                               _native.i64p(psig), _native.i64p(qsig), _native.i64p(ranks))
     _native.raise_for(st, ctx, "pluq_batched")

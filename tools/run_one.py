@@ -34,3 +34,64 @@ elif mode == "batch":
         x = batch.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
         pb.pluq_batched(x, P, 30); torch.cuda.synchronize()
         print(f"batch: {1e3*(time.perf_counter()-t0):.3f} ms", flush=True)
+elif mode == "e2e":
+    # transfer anatomy of the host-buffer batched path
+    src = orc.gen_cfg2(seed=0, batch=4096).astype(np.float64)
+    h = torch.from_numpy(src).pin_memory()
+    h2 = torch.empty_like(h).pin_memory()
+    d = torch.empty(h.shape, dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    nb = h.numel() * 8
+    for it in range(3):
+        torch.cuda.synchronize(); t0 = time.perf_counter(); d.copy_(h, non_blocking=True); torch.cuda.synchronize()
+        t1 = time.perf_counter(); h2.copy_(d, non_blocking=True); torch.cuda.synchronize(); t2 = time.perf_counter()
+        with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize(); t3 = time.perf_counter()
+        print(f"h2d {1e3*(t1-t0):.3f} ms ({nb/(t1-t0)/1e9:.1f} GB/s)  d2h {1e3*(t2-t1):.3f} ms "
+              f"({nb/(t2-t1)/1e9:.1f} GB/s)  both {1e3*(t3-t2):.3f} ms", flush=True)
+    del d, d2
+    ctx = _native.context()
+    pin = h.numpy()
+    for ch in [int(v) for v in sys.argv[2:]] or [8, 4, 16, 32]:
+        ctx.set_option("host_chunks", ch)
+        for it in range(3):
+            pin[...] = src
+            torch.cuda.synchronize(); t0 = time.perf_counter()
+            r = pb.pluq_batched(pin, P, 30)
+            dt = time.perf_counter() - t0
+            print(f"e2e chunks={ch}: {1e3*dt:.3f} ms", flush=True)
+elif mode == "batchk":
+    # per-kernel split of the batched path for option settings given as key=value
+    batch = torch.from_numpy(orc.gen_cfg2(seed=0, batch=4096)).cuda().to(torch.int32)
+    ctx = _native.context()
+    ctx.set_option("time_kernels", 1)
+    for spec in sys.argv[2:]:
+        for kv in spec.split(","):
+            k, v = kv.split("=")
+            ctx.set_option(k, int(v))
+        for it in range(3):
+            x = batch.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
+            pb.pluq_batched(x, P, 30); torch.cuda.synchronize()
+            st = ctx.stats()
+            print(f"{spec}: {1e3*(time.perf_counter()-t0):.3f} ms generic {st['t_generic_ns']/1e3:.1f} us "
+                  f"fallback {st['t_fallback_ns']/1e3:.1f} us", flush=True)
+elif mode == "e2etrace":
+    src = orc.gen_cfg2(seed=0, batch=4096).astype(np.float64)
+    h = torch.from_numpy(src).pin_memory(); pin = h.numpy()
+    ctx = _native.context()
+    for spec in sys.argv[2:] or ["host_chunks=8"]:
+        for kv in spec.split(","):
+            kk, v = kv.split("="); ctx.set_option(kk, int(v))
+        for it in range(3):
+            ctx.set_option("trace_pipeline", 1 if it == 2 else 0)
+            pin[...] = src
+            t0 = time.perf_counter(); r = pb.pluq_batched(pin, P, 30); dt = time.perf_counter() - t0
+            ps = np.zeros((4096, 64), np.int64); qs = np.zeros((4096, 64), np.int64); rk = np.zeros(4096, np.int64)
+            t1 = time.perf_counter()
+            st = ctx.lib.pluq_factor_batched_host_f64(ctx.handle, pin.ctypes.data, 4096, 64, 64, P, 30,
+                                                      _native.i64p(ps), _native.i64p(qs), _native.i64p(rk))
+            dt2 = time.perf_counter() - t1
+            print(f"{spec}: e2e {1e3*dt:.3f} ms  raw C call (reused outputs, already factored input) {1e3*dt2:.3f} ms", flush=True)
+    ctx.set_option("trace_pipeline", 0)
