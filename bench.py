@@ -33,9 +33,9 @@ M = N = 64
 BATCH = 4096
 THRESHOLD = 30
 METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
-# dram__bytes_read.sum + dram__bytes_write.sum of crout_fast_kernel per launch from the committed
+# dram__bytes_read.sum + dram__bytes_write.sum of the generic kernel per launch from the committed
 # ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
-TRAFFIC = None
+TRAFFIC = 78_460_928  # 67.27 MB read + 11.19 MB write (profiles/r1/prof_fixed_raw.txt)
 UNIT = "Gfield-op/s"
 
 
@@ -311,14 +311,16 @@ def main():
                 "d2h_bytes_per_step": BATCH * M * N * 8 + BATCH * (M + N + 1) * 8,
                 "path": "pluq_batched(pinned float64 numpy batch) -> C ABI pluq_factor_batched_host_f64",
                 "ms_per_step": 1e3 * t_e2e / len(e2e_t)},
-        "gpu_launches": args.steps,
-        "roofline": {"bound": "hbm", "kernel": "crout_fast_kernel", "achieved": alg_bytes / t_gen / 1e9,
+        "gpu_launches": args.steps * int(kst["launches"]),
+        "roofline": {"bound": "hbm", "kernel": "crout_fixed_kernel<64,64,128>", "achieved": alg_bytes / t_gen / 1e9,
                      "peak": hbm, "unit": "GB/s", "frac": alg_bytes / t_gen / 1e9 / hbm, "traffic": TRAFFIC,
+                     "traffic_unit": "bytes per launch (ncu --set full, dram read+write; output writes partly still in L2)",
+                     "alg_bytes": alg_bytes,
                      "peak_kind": peak_kind, "kernel_ms": t_gen * 1e3,
                      "fallback_kernel_ms": kst["t_fallback_ns"] / 1e6,
                      "note": "algorithmic bytes = read+write of 4096 int32 64x64 blocks + P/Q/rank; the "
                              "generic-profile Crout kernel is latency/issue bound (64-pivot chain per matrix); "
-                             "small_pluq_kernel handles the few non-generic matrices; see DESIGN.md"},
+                             "rpm_pluq_kernel finishes the few non-generic matrices (rank-profile route); see DESIGN.md"},
         "clocks": clocks.summary(),
         "wall_s_timed_region": wall,
     }

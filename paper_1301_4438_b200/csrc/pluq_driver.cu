@@ -958,6 +958,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
   if (int v = validate(m, n, p)) return v;
   if (block_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
   if (batch == 0) return kOk;
+  c->reset_stats();
   return guarded(c, [&] {
     SmallArgs a;
     a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;

@@ -123,9 +123,9 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   uint32_t* diag = dpre + mn;
   uint32_t* rowbuf = diag + mn;
   int* stk = reinterpret_cast<int*>(rowbuf + 256);
-  // register-resident phases when the block fits (n <= 64 with <= 4 rows per warp, or
-  // n <= 128 with <= 8 rows per warp), shared-memory phases otherwise
-  const int shape = (n <= 64 && m <= 4 * nw) ? 1 : (n <= 128 && m <= 8 * nw) ? 2 : 0;
+  // register-resident phases when the block fits (n <= 64 with <= 4 rows per warp),
+  // shared-memory phases otherwise (one instantiation keeps the kernel's code small)
+  const int shape = (n <= 64 && m <= 4 * nw) ? 1 : 0;
   for (int t = tid; t < m; t += nt) rows[t] = t;
   for (int t = tid; t < n; t += nt) cols[t] = t;
   if (shape == 0) {
@@ -136,7 +136,6 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   RPM_MARK(1);
   int r;
   if (shape == 1) r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
-  else if (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
   RPM_MARK(2);
   if (tid < 32) {
@@ -154,9 +153,6 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   if (shape == 1) {
     if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
-  } else if (shape == 2) {
-    if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
-    else lu_reg<4, 8, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else {
     for (int t = w; t < m; t += nw) {  // A'[t][u] = A[P^-1(t)][Q(u)]
       const uint32_t* src = ga + (int64_t)pinv[t] * args.lda;

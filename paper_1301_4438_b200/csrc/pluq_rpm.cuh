@@ -79,8 +79,86 @@ struct SymCtx {
 // local column, pivots first then the rest in local order (iterative.py:82-91).  On a
 // partial permutation the frontier walk needs no pivot flags: a row (column) at the
 // frontier can only be matched with its own single one.
+// Base cases of at most 32 x 32: lr/lc live in lane registers, the frontier walk runs on
+// all lanes (two independent shuffles per step), and P, Q and the charges come from
+// pivot bitmasks (prefix ORs) instead of per-pivot loops.
+__device__ int sym_base32(const int* rows, const int* cols, int m, int n, int* P, int* Q, int* stk,
+                          SymCtx& s) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  if (lane < m) s.rpos[rows[lane]] = lane;
+  if (lane < n) s.cpos[cols[lane]] = lane;
+  __syncwarp();
+  int lr = -1, lc = -1;
+  if (lane < m) {
+    const int x = s.rp[rows[lane]];
+    if (x >= 0) {
+      const int q = s.cpos[x];
+      if ((unsigned)q < (unsigned)n && cols[q] == x) lr = q;
+    }
+  }
+  if (lane < n) {
+    const int y = s.cp[cols[lane]];
+    if (y >= 0) {
+      const int q = s.rpos[y];
+      if ((unsigned)q < (unsigned)m && rows[q] == y) lc = q;
+    }
+  }
+  int i = 0, j = 0, r = 0, myro = 0, myco = 0;
+  while (i < m || j < n) {
+    const int a = __shfl_sync(FULL, lc, j & 31);
+    const int b = __shfl_sync(FULL, lr, i & 31);
+    int pr, pc;
+    if (j < n && a >= 0 && a < i) { pr = a; pc = j; ++j; }           // column segment
+    else if (i < m && b >= 0 && b < j) { pr = i; pc = b; ++i; }      // row segment
+    else if (i < m && j < n && b == j) { pr = i; pc = j; ++i; ++j; } // corner
+    else { i = min(i + 1, m); j = min(j + 1, n); continue; }
+    if (lane == r) { myro = pr; myco = pc; }
+    ++r;
+  }
+  const bool piv = lane < r;
+  const unsigned rbit = piv ? 1u << myro : 0u, cbit = piv ? 1u << myco : 0u;
+  // prefix ORs over the pivots that precede this one, and the full masks
+  unsigned pre_r = rbit, pre_c = cbit;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned ur = __shfl_up_sync(FULL, pre_r, o), uc = __shfl_up_sync(FULL, pre_c, o);
+    if (lane >= o) { pre_r |= ur; pre_c |= uc; }
+  }
+  const unsigned rmask = __shfl_sync(FULL, pre_r, 31), cmask = __shfl_sync(FULL, pre_c, 31);
+  pre_r &= ~rbit; pre_c &= ~cbit;  // exclusive
+  unsigned long long cm = 0, ca = 0, ci = 0;
+  if (piv) {
+    const int below = m - 1 - myro - __popc((unsigned)((unsigned long long)pre_r >> (myro + 1)));
+    const int right = n - 1 - myco - __popc((unsigned)((unsigned long long)pre_c >> (myco + 1)));
+    if (below > 0) {
+      const unsigned long long br = (unsigned long long)below * right;
+      ci = 1; cm = below + br; ca = br;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    cm += __shfl_xor_sync(FULL, cm, o);
+    ca += __shfl_xor_sync(FULL, ca, o);
+    ci += __shfl_xor_sync(FULL, ci, o);
+  }
+  if (lane == 0) { s.cnt.mul += cm; s.cnt.add += ca; s.cnt.inv += ci; s.cnt.red += cm; }
+  int* at = stk;  // at[row] = pivot index of a pivot row
+  if (piv) at[myro] = lane;
+  __syncwarp();
+  if (lane < m) {
+    const unsigned below_mask = (1u << lane) - 1u;
+    P[lane] = (rmask >> lane) & 1u ? at[lane] : r + lane - __popc(rmask & below_mask);
+  }
+  if (piv) Q[lane] = myco;
+  if (lane < n && !((cmask >> lane) & 1u)) Q[r + lane - __popc(cmask & ((1u << lane) - 1u))] = lane;
+  __syncwarp();
+  return r;
+}
+
 __device__ int sym_base(const int* rows, const int* cols, int m, int n, int* P, int* Q, int* stk,
                         SymCtx& s) {
+  if (m <= 32 && n <= 32) return sym_base32(rows, cols, m, n, P, Q, stk, s);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   for (int a = lane; a < m; a += 32) s.rpos[rows[a]] = a;
