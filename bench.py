@@ -334,7 +334,7 @@ def main():
 
 
 def secondary(pb, orc, dev, hbm, bf16, peak_kind):
-    """cfg3 (8192^2, GEMM-dominated) and the modular GEMM's tensor roofline."""
+    """The modular GEMM's tensor roofline, cfg3 (8192^2), cfg1, and cfg4/cfg5 at full size."""
     import torch
     from paper_1301_4438_b200 import _native
 
@@ -399,6 +399,35 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
         times.append(time.perf_counter() - t0)
     out["cfg1_512"] = {"rank": f1.rank, "s_best": min(times), "value": work(512, 512, f1.rank) / min(times) / 1e9,
                        "unit": UNIT}
+    del x, t3, x1, t1
+    # --- cfg4 / cfg5 at their full BASELINE sizes (device-generated; checked by size-independent
+    # properties: packed structure, Freivalds reconstruction, cfg4's prescribed rank profiles)
+    from paper_1301_4438_b200 import gen, verify
+
+    for name, m_, n_, r_, p_ in (("cfg4_full", 16384, 32768, 8192, 8388593), ("cfg5_full", 65536, 65536, 32768, P)):
+        if name == "cfg4_full":
+            a0, rows, cols = gen.gen_cfg4_device(m_, n_, r_, p_, seed=0)
+        else:
+            a0, rows, cols = gen.gen_xy_rank_device(m_, n_, r_, p_, seed=0), None, None
+        times = []
+        for it in range(2):
+            xa = a0.clone()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            f = pb.pluq(pb.DenseMatrix(pb.PrimeField(p_), xa))
+            torch.cuda.synchronize(dev)
+            times.append(time.perf_counter() - t0)
+            if it == 0:
+                del xa
+        checks = {"structure": bool(verify.structure_ok(f)), "freivalds": bool(verify.freivalds(a0, f, probes=2))}
+        if rows is not None:
+            checks["row_profile"] = pb.row_rank_profile(f) == tuple(int(v) for v in rows)
+            checks["col_profile"] = pb.col_rank_profile(f) == tuple(int(v) for v in cols)
+        out[name] = {"shape": [m_, n_], "p": p_, "rank": f.rank, "s_best": min(times),
+                     "value": work(m_, n_, f.rank) / min(times) / 1e9, "unit": UNIT, "checks": checks,
+                     "stats": pb.last_stats()}
+        del a0, f, xa
+        torch.cuda.empty_cache()
     return out
 
 

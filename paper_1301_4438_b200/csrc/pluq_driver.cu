@@ -100,6 +100,7 @@ struct pluq_ctx {
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
+  int64_t diag_lazy = 1;           // speculative LU: lazy-reduction diagonal-block kernel
   int64_t host_chunks = 8;         // pipeline depth of the host-buffer batched path
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
@@ -543,8 +544,10 @@ struct Driver {
     Ops sops = ops;
     sops.stop = c->d_stop;
     const uint16_t* itab = c->invtab(mp.p);
-    const size_t dsm = diag_fast_smem(BS, itab != nullptr);
-    CU(cudaFuncSetAttribute(diag_crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    const bool lazy = c->diag_lazy && BS <= 128;
+    const size_t dsm = lazy ? diag_lazy_smem(itab != nullptr) : diag_fast_smem(BS, itab != nullptr);
+    if (lazy) CU(cudaFuncSetAttribute(diag_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    else CU(cudaFuncSetAttribute(diag_crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     bool stopped_early = false;
     int blk = 0;
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
@@ -552,8 +555,11 @@ struct Driver {
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
-        diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
-                                                            c->d_stop + 1, k0);
+        if (lazy)
+          diag_lazy_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+        else
+          diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
+                                                              c->d_stop + 1, k0);
         c->check_launch();
         const View b11 = x.sub(k0, k0, bs, bs);
         sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                       // L21
@@ -899,10 +905,12 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_min_dim") c->tc_min_dim = value;
   else if (k == "tc_min_k") c->tc_min_k = value;
   else if (k == "tc_k_pass") c->tc.k_pass_override = value;
+  else if (k == "tc_cfg") c->tc.variant = (int)value;
   else if (k == "try_generic") c->try_generic = value;
   else if (k == "time_kernels") c->time_kernels = value;
   else if (k == "fixed_kernels") c->fixed_kernels = value;
   else if (k == "host_chunks") c->host_chunks = value;
+  else if (k == "diag_lazy") c->diag_lazy = value;
   else if (k == "exact_kernel") c->exact_kernel = value;
   else if (k == "rpm_threads") c->rpm_threads = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;

@@ -997,6 +997,139 @@ __global__ void __launch_bounds__(1024) diag_crout_fast_kernel(View blk, ModP mp
   }
 }
 
+// Right-looking lazy-reduction variant of diag_crout_fast_kernel, same contract: the
+// block (m, n <= 128) is factored in place; on a zero pivot at t the entries with
+// i < t or j < t hold the factors of the first t pivots, the trailing block keeps its
+// original values, and (status, stop) report (k0, t).  Warp w holds rows 4w..4w+3,
+// lane l columns l + 32q (q < 4), every element in a 64-bit register accumulator that
+// takes one IMAD.WIDE per pivot; elements are reduced mod p once, when they become
+// part of pivot row t (U) or column t (L).  For primes where 128 products no longer fit
+// in 64 bits, all accumulators are reduced every kchunk - 1 steps.
+__global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, const uint16_t* invtab, int* stop,
+                                                        int* status, int k0) {
+  if (stopped(stop)) return;
+  extern __shared__ __align__(16) uint32_t smem_dyn[];
+  constexpr int B = 128, LD = B + 1;
+  const int m = blk.m, n = blk.n, mn = min(m, n);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool use_tab = invtab != nullptr;
+  uint16_t* tab = reinterpret_cast<uint16_t*>(smem_dyn);     // inverse table first (16-byte aligned)
+  unsigned long long* mbuf = reinterpret_cast<unsigned long long*>(smem_dyn + (use_tab ? 32768 : 0));  // [32][4]
+  uint32_t* lbuf = reinterpret_cast<uint32_t*>(mbuf + 32 * 4);  // [32][4]
+  uint32_t* pinv = lbuf + 32 * 4;                               // [2]
+  uint32_t* prow = pinv + 2;                                    // [2][B] pivot rows
+  uint32_t* out = prow + 2 * B;                                 // [B][LD] output image
+  if (use_tab) {
+    const int words = (int)(mp.p + 1) / 2;
+    const uint4* src = reinterpret_cast<const uint4*>(invtab);
+    uint4* dst = reinterpret_cast<uint4*>(tab);
+    for (int q = tid; q < (words + 3) / 4; q += 1024) dst[q] = __ldg(src + q);
+  }
+  const int r0 = 4 * w;
+  unsigned long long acc[4][4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = r0 + rr, j = lane + 32 * q;
+      const uint32_t v = (i < m && j < n) ? blk.at(i, j) : 0u;
+      acc[rr][q] = v;
+      if (i < m && j < n) out[i * LD + j] = v;
+    }
+  __syncthreads();  // the table is in shared memory
+  auto pivinv = [&](uint32_t d) -> uint32_t { return d ? (use_tab ? (uint32_t)tab[d] : invmod(d, mp)) : 0u; };
+  if (w == 0) {  // row 0 is final from the start
+#pragma unroll
+    for (int q = 0; q < 4; ++q) prow[lane + 32 * q] = (uint32_t)acc[0][q];
+    if (lane == 0) pinv[0] = mn > 0 ? pivinv((uint32_t)acc[0][0]) : 0u;
+  }
+  const uint64_t kc1 = mp.kchunk > 1 ? mp.kchunk - 1 : 1;
+  const int kred = kc1 > (1u << 20) ? (1 << 20) : (int)kc1;
+  int since = 0, stop_t = mn;
+  for (int t = 0; t < mn; ++t) {
+    __syncthreads();  // pivot row t published
+    const uint32_t iv = pinv[t & 1];
+    if (iv == 0u) { stop_t = t; break; }  // block-uniform
+    uint32_t nrv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t u = prow[(t & 1) * B + lane + 32 * q];
+      nrv[q] = (lane + 32 * q > t && u) ? mp.p - u : 0u;  // columns <= t take no update
+    }
+    if (r0 + 3 > t && r0 < m) {  // warp has rows below the pivot (warp-uniform)
+      const int tq = t >> 5;
+      if (lane == (t & 31)) {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          unsigned long long x = acc[rr][0];
+#pragma unroll
+          for (int q = 1; q < 4; ++q) x = q == tq ? acc[rr][q] : x;
+          mbuf[w * 4 + rr] = x;
+        }
+      }
+      __syncwarp();
+      if (lane < 4) {
+        const int i = r0 + lane;
+        uint32_t l = 0u;
+        if (i > t && i < m) {
+          l = mulmod(reduce64(mbuf[w * 4 + lane], mp), iv, mp);
+          out[i * LD + t] = l;  // L entry, final
+        }
+        lbuf[w * 4 + lane] = l;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const uint32_t l = lbuf[w * 4 + rr];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[rr][q] += (unsigned long long)l * nrv[q];
+      }
+    }
+    if (++since >= kred) {  // large p: keep the accumulators in range (block-uniform)
+      since = 0;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[rr][q] = reduce64(acc[rr][q], mp);
+    }
+    const int t1 = t + 1;  // row t+1 is final: its owner reduces and publishes it
+    if (t1 < mn && (t1 >> 2) == w) {
+      const int rr1 = t1 & 3;
+      uint32_t x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        unsigned long long y = acc[0][q];
+#pragma unroll
+        for (int rr = 1; rr < 4; ++rr) y = rr == rr1 ? acc[rr][q] : y;
+        x[q] = reduce64(y, mp);
+      }
+      const uint32_t d = __shfl_sync(0xffffffffu, lane_pick<4>(x, t1 >> 5), t1 & 31);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = lane + 32 * q;
+        prow[(t1 & 1) * B + c] = c >= t1 && c < n ? x[q] : 0u;
+        if (d != 0u && c >= t1 && c < n) out[t1 * LD + c] = x[q];  // U row (kept original on a zero pivot)
+      }
+      if (lane == 0) pinv[t1 & 1] = pivinv(d);
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < m * n; idx += 1024) {
+    const int i = idx / n, j = idx - (idx / n) * n;
+    blk.at(i, j) = out[i * LD + j];
+  }
+  if (tid == 0 && stop_t < mn) {
+    status[0] = k0;
+    status[1] = stop_t;
+    __threadfence();
+    atomicExch(stop, 1);
+  }
+}
+
+inline size_t diag_lazy_smem(bool tab) {
+  return (size_t)(128 * 129 + 2 * 128 + 2) * 4 + 32 * 4 * 8 + 32 * 4 * 4 + 16 + (tab ? 65536 * 2 : 0);
+}
+
 inline size_t diag_fast_smem(int64_t bs, bool tab) {
   return (size_t)(((bs * (bs | 1)) + 3) & ~3ll) * 4 + (tab ? 65536 * 2 : 0);
 }

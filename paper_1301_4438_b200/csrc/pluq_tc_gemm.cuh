@@ -103,34 +103,45 @@ __host__ __device__ constexpr uint32_t idesc_i8(int n) {
 // Persistent tiling: each CTA (one per SM) walks output tiles; TMEM holds TWO
 // accumulator sets (NPOS positions x BN columns each) so the epilogue of tile t
 // overlaps the MMAs of tile t+1.
-template <int L>
+// V = 0: narrow tiles, two TMEM accumulator sets (epilogue overlapped with the next
+// tile's MMAs).  V = 1: wide tiles with ONE accumulator set: the operand bytes per MAC
+// drop from (BM+BN)/(L*BM*BN) = 0.0117 (L=2, BN=64) to 0.0078 (BN=128), which is what
+// the L2->SM bandwidth (~6.3 KB/cycle chip-wide) allows at >60 % of the int8 MMA rate;
+// the unoverlapped epilogue costs ~1/(K/32) of a K=4096 tile.
+template <int L, int V>
 struct TcCfg;
-template <> struct TcCfg<1> { static constexpr int BN = 256, STAGES = 4; };
-template <> struct TcCfg<2> { static constexpr int BN = 64, STAGES = 4; };
-template <> struct TcCfg<3> { static constexpr int BN = 32, STAGES = 3; };
-template <> struct TcCfg<4> { static constexpr int BN = 32, STAGES = 2; };
+template <> struct TcCfg<1, 0> { static constexpr int BN = 256, STAGES = 4, NBUF = 2; };
+template <> struct TcCfg<2, 0> { static constexpr int BN = 64, STAGES = 4, NBUF = 2; };
+template <> struct TcCfg<3, 0> { static constexpr int BN = 32, STAGES = 3, NBUF = 2; };
+template <> struct TcCfg<4, 0> { static constexpr int BN = 32, STAGES = 2, NBUF = 2; };
+template <> struct TcCfg<1, 1> { static constexpr int BN = 256, STAGES = 4, NBUF = 2; };
+template <> struct TcCfg<2, 1> { static constexpr int BN = 128, STAGES = 3, NBUF = 1; };
+template <> struct TcCfg<3, 1> { static constexpr int BN = 96, STAGES = 2, NBUF = 1; };
+template <> struct TcCfg<4, 1> { static constexpr int BN = 64, STAGES = 2, NBUF = 1; };
 
 constexpr int TC_BM = 128, TC_BK = 128;
 
-template <int L>
+template <int L, int V>
 constexpr size_t tc_smem_bytes() {
-  return 1024 + (size_t)TcCfg<L>::STAGES * L * (TC_BM * TC_BK + TcCfg<L>::BN * TC_BK) + 256;
+  return 1024 + (size_t)TcCfg<L, V>::STAGES * L * (TC_BM * TC_BK + TcCfg<L, V>::BN * TC_BK) + 256;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int L>
-__global__ void __launch_bounds__(256, 1)
+constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warps 4..11 epilogue
+
+template <int L, int V>
+__global__ void __launch_bounds__(TC_THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
                       int m_pad, int n_pad, int kblocks, ModP mp, const int* stop) {
   if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
-  constexpr int BN = TcCfg<L>::BN, STAGES = TcCfg<L>::STAGES;
+  constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
   constexpr int NPOS = 2 * L - 1;
   constexpr int ACC_COLS = NPOS * BN;               // one accumulator set
   constexpr uint32_t TCOLS = 512;
-  static_assert(2 * ACC_COLS <= 512, "two accumulator sets must fit in TMEM");
+  static_assert(NBUF * ACC_COLS <= 512, "the accumulator sets must fit in TMEM");
   constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
   constexpr uint32_t STAGE_BYTES = L * (A_TILE + B_TILE);
   extern __shared__ uint8_t smem_raw[];
@@ -139,16 +150,16 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = smem + (size_t)STAGES * L * A_TILE;    // [STAGES][L][BNx128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)STAGES * L * B_TILE);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + STAGES;   // [NBUF]
+  uint64_t* tempty = tfull + NBUF;    // [NBUF]
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = n_pad / BN, tiles = (m_pad / TC_BM) * tiles_n;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) tmem_alloc(tholder, TCOLS);
@@ -178,7 +189,7 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t idesc = idesc_i8(BN);
     uint32_t g = 0, local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
-      const uint32_t buf = local & 1, use = local >> 1;
+      const uint32_t buf = local % NBUF, use = local / NBUF;
       mbar_wait(&tempty[buf], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t dacc = tbase + buf * ACC_COLS;
@@ -209,10 +220,14 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> recombine mod p -> C ----------------
-    const int q = warp & 3;
+    // 8 warps: TMEM sub-partition q = warp % 4 (lanes 32q..32q+31), column half h.
+    // The limb positions are combined exactly in 64 bits (sum acc_s * 2^(8s) < 2^64 for
+    // L <= 3 since every acc_s < 2^31) and reduced ONCE; L = 4 reduces after position 4.
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    constexpr int HALF = BN / 2;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
-      const uint32_t buf = local & 1, use = local >> 1;
+      const uint32_t buf = local % NBUF, use = local / NBUF;
       const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
       uint32_t* crow = row < c.m ? c.row(row) : nullptr;
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 8) {
+      for (int cc = h * HALF; cc < (h + 1) * HALF; cc += 8) {
         uint32_t acc[NPOS][8];
 #pragma unroll
         for (int s = 0; s < NPOS; ++s) tmem_ld8(lane_base + (uint32_t)(s * BN + cc), acc[s]);
@@ -233,9 +248,21 @@ __global__ void __launch_bounds__(256, 1)
           for (int t = 0; t < 8; ++t) {
             const int col = n0 + cc + t;
             if (col < c.n) {
-              uint32_t v = reduce64(acc[NPOS - 1][t], mp);
+              uint32_t v;
+              if (NPOS <= 5) {
+                uint64_t x = 0;
 #pragma unroll
-              for (int s = NPOS - 2; s >= 0; --s) v = reduce64(((uint64_t)v << 8) + acc[s][t], mp);
+                for (int s = 0; s < NPOS; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+                v = reduce64(x, mp);
+              } else {
+                uint64_t hi = 0;
+#pragma unroll
+                for (int s = 4; s < NPOS; ++s) hi += (uint64_t)acc[s][t] << (8 * (s - 4));
+                uint64_t x = (uint64_t)reduce64(hi, mp) << 32;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+                v = reduce64(x, mp);
+              }
               crow[col] = submod(cur[t], v, mp);
             }
           }
@@ -312,7 +339,8 @@ struct TcGemm {
   PFN_encodeTiled encode = nullptr;
   std::string last_error;
   int64_t k_pass_override = 0;  // tests: force multi-pass K splitting
-  bool attrs_set[5] = {false, false, false, false, false};
+  bool attrs_set[2][5] = {};
+  int variant = 1;              // TcCfg variant (option tc_cfg)
 
   static int limbs(uint32_t p) {
     int bits = 0;
@@ -366,9 +394,9 @@ struct TcGemm {
     return true;
   }
 
-  template <int L>
+  template <int L, int V>
   int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop) {
-    constexpr int BN = TcCfg<L>::BN;
+    constexpr int BN = TcCfg<L, V>::BN;
     const int m = c.m, n = c.n, k = a.n;
     const int m_pad = (m + TC_BM - 1) / TC_BM * TC_BM;
     const int n_pad = (n + BN - 1) / BN * BN;
@@ -383,14 +411,14 @@ struct TcGemm {
       last_error = "workspace allocation failed";
       return kNoMemory;
     }
-    constexpr size_t smem = tc_smem_bytes<L>();
-    if (!attrs_set[L]) {
-      if (cudaFuncSetAttribute(tc_modgemm_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    constexpr size_t smem = tc_smem_bytes<L, V>();
+    if (!attrs_set[V][L]) {
+      if (cudaFuncSetAttribute(tc_modgemm_kernel<L, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess) {
         last_error = "cannot set shared memory size";
         return kCuda;
       }
-      attrs_set[L] = true;
+      attrs_set[V][L] = true;
     }
     for (int64_t k0 = 0; k0 < k; k0 += kp) {
       const int kc = (int)std::min<int64_t>(kp, k - k0);
@@ -413,7 +441,8 @@ struct TcGemm {
         return kCuda;
       }
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
-      tc_modgemm_kernel<L><<<std::min(tiles, num_sms()), 256, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop);
+      tc_modgemm_kernel<L, V><<<std::min(tiles, num_sms()), TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad,
+                                                                                   k_pad / TC_BK, mp, stop);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);
@@ -431,11 +460,21 @@ struct TcGemm {
     if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
     if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
     if (!load()) return kUnsupported;
-    switch (limbs(mp.p)) {
-      case 1: return launch<1>(c, a, b, mp, st, stop);
-      case 2: return launch<2>(c, a, b, mp, st, stop);
-      case 3: return launch<3>(c, a, b, mp, st, stop);
-      case 4: return launch<4>(c, a, b, mp, st, stop);
+    const int L = limbs(mp.p);
+    if (variant == 0) {
+      switch (L) {
+        case 1: return launch<1, 0>(c, a, b, mp, st, stop);
+        case 2: return launch<2, 0>(c, a, b, mp, st, stop);
+        case 3: return launch<3, 0>(c, a, b, mp, st, stop);
+        case 4: return launch<4, 0>(c, a, b, mp, st, stop);
+      }
+    } else {
+      switch (L) {
+        case 1: return launch<1, 1>(c, a, b, mp, st, stop);
+        case 2: return launch<2, 1>(c, a, b, mp, st, stop);
+        case 3: return launch<3, 1>(c, a, b, mp, st, stop);
+        case 4: return launch<4, 1>(c, a, b, mp, st, stop);
+      }
     }
     return kUnsupported;
   }

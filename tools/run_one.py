@@ -10,6 +10,9 @@ P = 65521
 mode = sys.argv[1]
 if mode == "cfg3":
     n = int(sys.argv[2])
+    for kv in os.environ.get("PLUQ_OPTS", "").split(","):
+        if kv:
+            kk, vv = kv.split("="); _native.context().set_option(kk, int(vv))
     a = torch.from_numpy(orc.gen_cfg3(seed=0, n=n)).cuda().to(torch.int32)
     for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 1):
         x = a.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
@@ -23,6 +26,7 @@ elif mode == "gemm":
     B = torch.randint(0, p, (k, n), generator=g, dtype=torch.int32).cuda()
     C = torch.randint(0, p, (m, n), generator=g, dtype=torch.int32).cuda()
     ctx = _native.context()
+    if os.environ.get("TC_CFG"): ctx.set_option("tc_cfg", int(os.environ["TC_CFG"]))
     for it in range(3):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         st = ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, p)
