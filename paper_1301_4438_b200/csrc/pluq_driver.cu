@@ -906,6 +906,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_min_k") c->tc_min_k = value;
   else if (k == "tc_k_pass") c->tc.k_pass_override = value;
   else if (k == "tc_cfg") c->tc.variant = (int)value;
+  else if (k == "tc_grid") c->tc.grid_override = (int)value;
+  else if (k == "tc_dbg") c->tc.dbg = (int)value;
   else if (k == "try_generic") c->try_generic = value;
   else if (k == "time_kernels") c->time_kernels = value;
   else if (k == "fixed_kernels") c->fixed_kernels = value;

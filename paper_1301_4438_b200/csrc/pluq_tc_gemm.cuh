@@ -82,6 +82,13 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row groups 1024 B apart).
@@ -121,9 +128,12 @@ template <> struct TcCfg<4, 1> { static constexpr int BN = 64, STAGES = 2, NBUF 
 
 constexpr int TC_BM = 128, TC_BK = 128;
 
+constexpr int TC_EPI_WARPS = 8, TC_CW = 16;                          // epilogue chunk: 16 columns
+constexpr size_t TC_EPI_SMEM = (size_t)TC_EPI_WARPS * 32 * (TC_CW + 1) * 4;  // per-warp transpose tile
+
 template <int L, int V>
 constexpr size_t tc_smem_bytes() {
-  return 1024 + (size_t)TcCfg<L, V>::STAGES * L * (TC_BM * TC_BK + TcCfg<L, V>::BN * TC_BK) + 256;
+  return 1024 + (size_t)TcCfg<L, V>::STAGES * L * (TC_BM * TC_BK + TcCfg<L, V>::BN * TC_BK) + 256 + TC_EPI_SMEM;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -135,7 +145,7 @@ constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, w
 template <int L, int V>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
-                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop) {
+                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg) {
   if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
   constexpr int NPOS = 2 * L - 1;
@@ -153,6 +163,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + STAGES;   // [NBUF]
   uint64_t* tempty = tfull + NBUF;    // [NBUF]
   uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + NBUF);
+  uint32_t* epi_smem = reinterpret_cast<uint32_t*>(sB + (size_t)STAGES * L * B_TILE + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = n_pad / BN, tiles = (m_pad / TC_BM) * tiles_n;
@@ -176,6 +187,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < kblocks; ++kb, ++g) {
         const uint32_t s = g % STAGES;
         mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        if (dbg == 1 && g >= (uint32_t)STAGES) {  // diagnostics: MMA rate without operand traffic
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_expect_tx(&full[s], STAGE_BYTES);
 #pragma unroll
         for (int l = 0; l < L; ++l) {
@@ -220,53 +235,64 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> recombine mod p -> C ----------------
-    // 8 warps: TMEM sub-partition q = warp % 4 (lanes 32q..32q+31), column half h.
-    // The limb positions are combined exactly in 64 bits (sum acc_s * 2^(8s) < 2^64 for
-    // L <= 3 since every acc_s < 2^31) and reduced ONCE; L = 4 reduces after position 4.
+    // 8 warps: TMEM sub-partition q = warp % 4 (lanes 32q..32q+31 = tile rows), column
+    // half h.  Per 16-column chunk a thread holds its row; the limb positions are
+    // combined exactly in 64 bits (sum acc_s * 2^(8s) < 2^64 for L <= 3 since every
+    // acc_s < 2^31; L = 4 reduces after position 4) and reduced ONCE, then the 32 x 16
+    // values are transposed through shared memory so that the read-modify-write of C is
+    // coalesced (lanes along a row, 16 independent loads in flight per thread).
     const int q = warp & 3, h = (warp - 4) >> 2;
     constexpr int HALF = BN / 2;
+    static_assert(HALF % TC_CW == 0, "epilogue chunking");
+    uint32_t* tr = epi_smem + (warp - 4) * 32 * (TC_CW + 1);
+    const int tc_col = lane & (TC_CW - 1), tc_row0 = lane >> 4;  // transposed phase: 2 rows x 16 columns
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const uint32_t buf = local % NBUF, use = local / NBUF;
       const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
-      uint32_t* crow = row < c.m ? c.row(row) : nullptr;
 #pragma unroll 1
-      for (int cc = h * HALF; cc < (h + 1) * HALF; cc += 8) {
-        uint32_t acc[NPOS][8];
+      for (int cc = h * HALF; cc < (h + 1) * HALF; cc += TC_CW) {
+        uint32_t acc[NPOS][TC_CW];
 #pragma unroll
-        for (int s = 0; s < NPOS; ++s) tmem_ld8(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+        for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
         tmem_ld_wait();
-        if (crow) {
-          uint32_t cur[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) cur[t] = (n0 + cc + t < c.n) ? crow[n0 + cc + t] : 0u;
+        for (int t = 0; t < TC_CW; ++t) {
+          uint32_t v;
+          if (NPOS <= 5) {
+            uint64_t x = 0;
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int col = n0 + cc + t;
-            if (col < c.n) {
-              uint32_t v;
-              if (NPOS <= 5) {
-                uint64_t x = 0;
+            for (int s = 0; s < NPOS; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+            v = reduce64(x, mp);
+          } else {
+            uint64_t hi = 0;
 #pragma unroll
-                for (int s = 0; s < NPOS; ++s) x += (uint64_t)acc[s][t] << (8 * s);
-                v = reduce64(x, mp);
-              } else {
-                uint64_t hi = 0;
+            for (int s = 4; s < NPOS; ++s) hi += (uint64_t)acc[s][t] << (8 * (s - 4));
+            uint64_t x = (uint64_t)reduce64(hi, mp) << 32;
 #pragma unroll
-                for (int s = 4; s < NPOS; ++s) hi += (uint64_t)acc[s][t] << (8 * (s - 4));
-                uint64_t x = (uint64_t)reduce64(hi, mp) << 32;
-#pragma unroll
-                for (int s = 0; s < 4; ++s) x += (uint64_t)acc[s][t] << (8 * s);
-                v = reduce64(x, mp);
-              }
-              crow[col] = submod(cur[t], v, mp);
-            }
+            for (int s = 0; s < 4; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+            v = reduce64(x, mp);
           }
+          tr[lane * (TC_CW + 1) + t] = v;
         }
+        __syncwarp();
+        const int col = n0 + cc + tc_col;
+        uint32_t w[16], cur[16];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const int rr = tc_row0 + 2 * kk, row = m0 + q * 32 + rr;
+          w[kk] = tr[rr * (TC_CW + 1) + tc_col];
+          cur[kk] = (row < c.m && col < c.n) ? c.row(row)[col] : 0u;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const int row = m0 + q * 32 + tc_row0 + 2 * kk;
+          if (row < c.m && col < c.n) c.row(row)[col] = submod(cur[kk], w[kk], mp);
+        }
+        __syncwarp();  // tr is reused by the next chunk
       }
       tc_fence_before();
       __syncwarp();
@@ -341,6 +367,8 @@ struct TcGemm {
   int64_t k_pass_override = 0;  // tests: force multi-pass K splitting
   bool attrs_set[2][5] = {};
   int variant = 1;              // TcCfg variant (option tc_cfg)
+  int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
+  int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring
 
   static int limbs(uint32_t p) {
     int bits = 0;
@@ -441,8 +469,9 @@ struct TcGemm {
         return kCuda;
       }
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
-      tc_modgemm_kernel<L, V><<<std::min(tiles, num_sms()), TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad,
-                                                                                   k_pad / TC_BK, mp, stop);
+      const int grid = std::min(tiles, grid_override > 0 ? grid_override : num_sms());
+      tc_modgemm_kernel<L, V><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop,
+                                                              dbg);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);

@@ -27,6 +27,8 @@ elif mode == "gemm":
     C = torch.randint(0, p, (m, n), generator=g, dtype=torch.int32).cuda()
     ctx = _native.context()
     if os.environ.get("TC_CFG"): ctx.set_option("tc_cfg", int(os.environ["TC_CFG"]))
+    if os.environ.get("TC_GRID"): ctx.set_option("tc_grid", int(os.environ["TC_GRID"]))
+    if os.environ.get("TC_DBG"): ctx.set_option("tc_dbg", int(os.environ["TC_DBG"]))
     for it in range(3):
         torch.cuda.synchronize(); t0 = time.perf_counter()
         st = ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, p)
