@@ -546,7 +546,11 @@ struct Driver {
     const uint16_t* itab = c->invtab(mp.p);
     const bool lazy = c->diag_lazy && BS <= 128;
     const size_t dsm = lazy ? diag_lazy_smem(itab != nullptr) : diag_fast_smem(BS, itab != nullptr);
-    if (lazy) CU(cudaFuncSetAttribute(diag_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    const int lazy_rw = c->diag_lazy == 2 ? 4 : 8;  // rows per warp of diag_lazy_kernel
+    if (lazy) {
+      CU(cudaFuncSetAttribute(diag_lazy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      CU(cudaFuncSetAttribute(diag_lazy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    }
     else CU(cudaFuncSetAttribute(diag_crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     bool stopped_early = false;
     int blk = 0;
@@ -555,8 +559,10 @@ struct Driver {
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
-        if (lazy)
-          diag_lazy_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+        if (lazy && lazy_rw == 8)
+          diag_lazy_kernel<8><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+        else if (lazy)
+          diag_lazy_kernel<4><<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
         else
           diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
                                                               c->d_stop + 1, k0);

@@ -1005,8 +1005,10 @@ __global__ void __launch_bounds__(1024) diag_crout_fast_kernel(View blk, ModP mp
 // takes one IMAD.WIDE per pivot; elements are reduced mod p once, when they become
 // part of pivot row t (U) or column t (L).  For primes where 128 products no longer fit
 // in 64 bits, all accumulators are reduced every kchunk - 1 steps.
-__global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, const uint16_t* invtab, int* stop,
-                                                        int* status, int k0) {
+template <int RW>  // rows per warp: 4 (32 warps) or 8 (16 warps, no register pressure)
+__global__ void __launch_bounds__(32 * (128 / RW)) diag_lazy_kernel(View blk, ModP mp, const uint16_t* invtab,
+                                                                    int* stop, int* status, int k0) {
+  constexpr int NT = 32 * (128 / RW);
   if (stopped(stop)) return;
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   constexpr int B = 128, LD = B + 1;
@@ -1014,21 +1016,21 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const bool use_tab = invtab != nullptr;
   uint16_t* tab = reinterpret_cast<uint16_t*>(smem_dyn);     // inverse table first (16-byte aligned)
-  unsigned long long* mbuf = reinterpret_cast<unsigned long long*>(smem_dyn + (use_tab ? 32768 : 0));  // [32][4]
-  uint32_t* lbuf = reinterpret_cast<uint32_t*>(mbuf + 32 * 4);  // [32][4]
-  uint32_t* pinv = lbuf + 32 * 4;                               // [2]
+  unsigned long long* mbuf = reinterpret_cast<unsigned long long*>(smem_dyn + (use_tab ? 32768 : 0));  // [NW][RW]
+  uint32_t* lbuf = reinterpret_cast<uint32_t*>(mbuf + 128);     // [NW][RW]
+  uint32_t* pinv = lbuf + 128;                                  // [2]
   uint32_t* prow = pinv + 2;                                    // [2][B] pivot rows
   uint32_t* out = prow + 2 * B;                                 // [B][LD] output image
   if (use_tab) {
     const int words = (int)(mp.p + 1) / 2;
     const uint4* src = reinterpret_cast<const uint4*>(invtab);
     uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (int q = tid; q < (words + 3) / 4; q += 1024) dst[q] = __ldg(src + q);
+    for (int q = tid; q < (words + 3) / 4; q += NT) dst[q] = __ldg(src + q);
   }
-  const int r0 = 4 * w;
-  unsigned long long acc[4][4];
+  const int r0 = RW * w;
+  unsigned long long acc[RW][4];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr)
+  for (int rr = 0; rr < RW; ++rr)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int i = r0 + rr, j = lane + 32 * q;
@@ -1046,8 +1048,17 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
   const uint64_t kc1 = mp.kchunk > 1 ? mp.kchunk - 1 : 1;
   const int kred = kc1 > (1u << 20) ? (1 << 20) : (int)kc1;
   int since = 0, stop_t = mn;
+#ifdef PLUQ_TRACE
+  long long T[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool trw = k0 == 0 && (tid >> 5) == (64 / RW);  // owner warp of row 64
+#define DMARK(x) do { if (trw && t == 63 && lane == 0) T[x] = clock64(); } while (0)
+#else
+#define DMARK(x) do { } while (0)
+#endif
   for (int t = 0; t < mn; ++t) {
+    DMARK(0);
     __syncthreads();  // pivot row t published
+    DMARK(1);
     const uint32_t iv = pinv[t & 1];
     if (iv == 0u) { stop_t = t; break; }  // block-uniform
     uint32_t nrv[4];
@@ -1056,31 +1067,33 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
       const uint32_t u = prow[(t & 1) * B + lane + 32 * q];
       nrv[q] = (lane + 32 * q > t && u) ? mp.p - u : 0u;  // columns <= t take no update
     }
-    if (r0 + 3 > t && r0 < m) {  // warp has rows below the pivot (warp-uniform)
+    if (r0 + RW - 1 > t && r0 < m) {  // warp has rows below the pivot (warp-uniform)
       const int tq = t >> 5;
       if (lane == (t & 31)) {
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
+        for (int rr = 0; rr < RW; ++rr) {
           unsigned long long x = acc[rr][0];
 #pragma unroll
           for (int q = 1; q < 4; ++q) x = q == tq ? acc[rr][q] : x;
-          mbuf[w * 4 + rr] = x;
+          mbuf[w * RW + rr] = x;
         }
       }
       __syncwarp();
-      if (lane < 4) {
+      DMARK(2);
+      if (lane < RW) {
         const int i = r0 + lane;
         uint32_t l = 0u;
         if (i > t && i < m) {
-          l = mulmod(reduce64(mbuf[w * 4 + lane], mp), iv, mp);
+          l = mulmod(reduce64(mbuf[w * RW + lane], mp), iv, mp);
           out[i * LD + t] = l;  // L entry, final
         }
-        lbuf[w * 4 + lane] = l;
+        lbuf[w * RW + lane] = l;
       }
       __syncwarp();
+      DMARK(3);
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const uint32_t l = lbuf[w * 4 + rr];
+      for (int rr = 0; rr < RW; ++rr) {
+        const uint32_t l = lbuf[w * RW + rr];
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[rr][q] += (unsigned long long)l * nrv[q];
       }
@@ -1088,19 +1101,20 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
     if (++since >= kred) {  // large p: keep the accumulators in range (block-uniform)
       since = 0;
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr)
+      for (int rr = 0; rr < RW; ++rr)
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[rr][q] = reduce64(acc[rr][q], mp);
     }
+    DMARK(4);
     const int t1 = t + 1;  // row t+1 is final: its owner reduces and publishes it
-    if (t1 < mn && (t1 >> 2) == w) {
-      const int rr1 = t1 & 3;
+    if (t1 < mn && t1 / RW == w) {
+      const int rr1 = t1 % RW;
       uint32_t x[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         unsigned long long y = acc[0][q];
 #pragma unroll
-        for (int rr = 1; rr < 4; ++rr) y = rr == rr1 ? acc[rr][q] : y;
+        for (int rr = 1; rr < RW; ++rr) y = rr == rr1 ? acc[rr][q] : y;
         x[q] = reduce64(y, mp);
       }
       const uint32_t d = __shfl_sync(0xffffffffu, lane_pick<4>(x, t1 >> 5), t1 & 31);
@@ -1112,9 +1126,15 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
       }
       if (lane == 0) pinv[t1 & 1] = pivinv(d);
     }
+    DMARK(5);
+#ifdef PLUQ_TRACE
+    if (trw && t == 63 && lane == 0)
+      printf("DIAG t=63 bar=%lld mul_stage=%lld mult=%lld imad=%lld fin=%lld total_to_bar=%lld\n", T[1] - T[0],
+             T[2] - T[1], T[3] - T[2], T[4] - T[3], T[5] - T[4], T[5] - T[1]);
+#endif
   }
   __syncthreads();
-  for (int idx = tid; idx < m * n; idx += 1024) {
+  for (int idx = tid; idx < m * n; idx += NT) {
     const int i = idx / n, j = idx - (idx / n) * n;
     blk.at(i, j) = out[i * LD + j];
   }
@@ -1127,7 +1147,7 @@ __global__ void __launch_bounds__(1024) diag_lazy_kernel(View blk, ModP mp, cons
 }
 
 inline size_t diag_lazy_smem(bool tab) {
-  return (size_t)(128 * 129 + 2 * 128 + 2) * 4 + 32 * 4 * 8 + 32 * 4 * 4 + 16 + (tab ? 65536 * 2 : 0);
+  return (size_t)(128 * 129 + 2 * 128 + 2) * 4 + 128 * 8 + 128 * 4 + 16 + (tab ? 65536 * 2 : 0);
 }
 
 inline size_t diag_fast_smem(int64_t bs, bool tab) {
