@@ -359,14 +359,21 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
     _native.raise_for(st, ctx, "tc gemm")
     t = ev0.elapsed_time(ev1) / 1e3 / reps
     limbs = 2
-    int8_peak = 2.0 * bf16  # dense int8 = 2x dense bf16 on B200; MEASURED_PEAKS has bf16 only
+    # the int8 (tcgen05 kind::i8) and FP64 peaks are microbenchmarked on this box
+    pk = max((ctx.measure_peaks() for _ in range(3)), key=lambda d: d["int8_tops"])
+    int8_peak = pk["int8_tops"]
+    achieved = 2.0 * m * n * k * limbs * limbs / t / 1e12
+    out["measured_peaks"] = {"int8_tcgen05_tops": int8_peak, "fp64_dmma_tflops": pk["fp64_tflops"],
+                             "how": "pluq_measure_peaks: back-to-back tcgen05.mma.kind::i8 128x256x32 per SM; "
+                                    "mma.sync m8n8k4 f64 on all SMs"}
     out["modgemm_4096"] = {
         "shape": [m, n, k], "ms": t * 1e3, "field_op_per_s": 2.0 * m * n * k / t / 1e9,
-        "int8_tops": 2.0 * m * n * k * limbs * limbs / t / 1e12,
-        "roofline": {"bound": "tensor", "achieved": 2.0 * m * n * k * limbs * limbs / t / 1e12, "peak": int8_peak,
-                     "unit": "TOP/s", "frac": 2.0 * m * n * k * limbs * limbs / t / 1e12 / int8_peak,
-                     "peak_kind": f"2 x {peak_kind} bf16 ({bf16} TF/s)",
-                     "note": "includes the limb-split conversion passes"},
+        "int8_tops": achieved,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOP/s",
+                     "frac": achieved / int8_peak, "peak_kind": "measured (tcgen05 kind::i8 microbenchmark)",
+                     "frac_vs_2x_bf16": achieved / (2.0 * bf16),
+                     "note": "int8 ops = 2mnk * L^2 (L = 2 limbs for p = 65521); includes the limb-split "
+                             "conversion passes"},
     }
     del A, B, C
     # --- cfg3: 8192^2 full-rank generic, device resident

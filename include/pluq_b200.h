@@ -113,6 +113,11 @@ int pluq_modgemm_sub_tc(pluq_ctx* ctx, uint32_t* dC, int64_t ldc, const uint32_t
  * `rank` (leading principal minors 1..rank nonzero), where P = Q = I.  Host-only. */
 int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, int64_t* counts);
 
+/* Microbenchmarked peaks of this device (SURVEY §8d roofline denominators):
+ * out[0] = tcgen05 kind::i8 dense TOP/s (128x256x32 MMAs, one CTA per SM),
+ * out[1] = FP64 DMMA (mma.sync m8n8k4) TFLOP/s.  Diagnostics; not on the factorization path. */
+int pluq_measure_peaks(pluq_ctx* ctx, double* out, int64_t nout);
+
 /* Device-side statistics of the last pluq_factor call (kernel launches, host syncs,
  * nodes, tensor-core GEMM launches and their summed device time in ms). */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);

@@ -28,6 +28,7 @@ SIGNATURES = {
     "pluq_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i64]),
     "pluq_last_error": (ctypes.c_char_p, [_p]),
     "pluq_last_stats": (ctypes.c_int, [_p, _pi64, _i64]),
+    "pluq_measure_peaks": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_double), _i64]),
     "pluq_generic_counts": (ctypes.c_int, [_i64, _i64, _i64, _i64, _pi64]),
     "pluq_factor": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_iterative": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
@@ -122,6 +123,12 @@ class Context:
                 "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves", "speculative_ok",
                 "speculative_fail", "t_generic_ns", "t_fallback_ns"]
         return dict(zip(keys, list(buf)))
+
+    def measure_peaks(self) -> dict:
+        """Microbenchmarked int8 tcgen05 and FP64 DMMA peaks of this device."""
+        buf = (ctypes.c_double * 2)()
+        raise_for(self.lib.pluq_measure_peaks(self.handle, buf, 2), self, "pluq_measure_peaks")
+        return {"int8_tops": buf[0], "fp64_tflops": buf[1]}
 
     def __del__(self):
         try:

@@ -931,6 +931,47 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
 
 const char* pluq_last_error(pluq_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+int pluq_measure_peaks(pluq_ctx* c, double* out, int64_t nout) {
+  if (!out || nout < 2) return kInvalid;
+  return guarded(c, [&] {
+    int dev = 0, sms = 148;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = 1024 + 2 * 128 * 128 + 128 * 128;
+    CU(cudaFuncSetAttribute(mma_peak_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    const int iters = 4096;
+    mma_peak_i8_kernel<<<sms, 128, smem, c->stream>>>(256);  // warm-up
+    c->check_launch();
+    CU(cudaEventRecord(e0, c->stream));
+    mma_peak_i8_kernel<<<sms, 128, smem, c->stream>>>(iters);
+    c->check_launch();
+    CU(cudaEventRecord(e1, c->stream));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    out[0] = 2.0 * 128 * 256 * 32 * (double)iters * sms / (ms * 1e-3) / 1e12;  // int8 TOP/s
+    double* sink = c->dalloc<double>(256);
+    const int fit = 2048;
+    mma_peak_f64_kernel<<<sms * 8, 256, 0, c->stream>>>(64, sink);  // warm-up
+    c->check_launch();
+    CU(cudaEventRecord(e0, c->stream));
+    mma_peak_f64_kernel<<<sms * 8, 256, 0, c->stream>>>(fit, sink);
+    c->check_launch();
+    CU(cudaEventRecord(e1, c->stream));
+    CU(cudaEventSynchronize(e1));
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    const double mmas = 4.0 * fit * (double)sms * 8 * 8;  // per warp: 4 per iteration; 8 warps per CTA
+    out[1] = 2.0 * 8 * 8 * 4 * mmas / (ms * 1e-3) / 1e12;  // fp64 TFLOP/s
+    c->dfree(sink);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->sync();
+  });
+}
+
 int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, int64_t* counts) {
   if (m < 0 || n < 0 || rank < 0 || rank > std::min(m, n) || threshold < 1 || !counts) return kInvalid;
   Counts c{0, 0, 0, 0};

@@ -246,6 +246,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     static_assert(HALF % TC_CW == 0, "epilogue chunking");
     uint32_t* tr = epi_smem + (warp - 4) * 32 * (TC_CW + 1);
     const int tc_col = lane & (TC_CW - 1), tc_row0 = lane >> 4;  // transposed phase: 2 rows x 16 columns
+    // limb positions of one 16-column chunk -> 16 reduced values of this thread's row
+    auto combine = [&](uint32_t lane_base, int cc, uint32_t (&v)[TC_CW]) {
+      uint32_t acc[NPOS][TC_CW];
+#pragma unroll
+      for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < TC_CW; ++t) {
+        if (NPOS <= 5) {
+          uint64_t x = 0;
+#pragma unroll
+          for (int s = 0; s < NPOS; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+          v[t] = reduce64(x, mp);
+        } else {
+          uint64_t hi = 0;
+#pragma unroll
+          for (int s = 4; s < NPOS; ++s) hi += (uint64_t)acc[s][t] << (8 * (s - 4));
+          uint64_t x = (uint64_t)reduce64(hi, mp) << 32;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) x += (uint64_t)acc[s][t] << (8 * s);
+          v[t] = reduce64(x, mp);
+        }
+      }
+    };
+    // transpose a chunk through shared memory and apply C <- C - v, coalesced
+    auto apply = [&](int m0, int n0, int cc, const uint32_t (&v)[TC_CW]) {
+#pragma unroll
+      for (int t = 0; t < TC_CW; ++t) tr[lane * (TC_CW + 1) + t] = v[t];
+      __syncwarp();
+      const int col = n0 + cc + tc_col;
+      uint32_t w[16], cur[16];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int rr = tc_row0 + 2 * kk, row = m0 + q * 32 + rr;
+        w[kk] = tr[rr * (TC_CW + 1) + tc_col];
+        cur[kk] = (row < c.m && col < c.n) ? c.row(row)[col] : 0u;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int row = m0 + q * 32 + tc_row0 + 2 * kk;
+        if (row < c.m && col < c.n) c.row(row)[col] = submod(cur[kk], w[kk], mp);
+      }
+      __syncwarp();  // tr is reused by the next chunk
+    };
+    constexpr int NCH = HALF / TC_CW;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const uint32_t buf = local % NBUF, use = local / NBUF;
@@ -253,50 +298,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int cc = h * HALF; cc < (h + 1) * HALF; cc += TC_CW) {
-        uint32_t acc[NPOS][TC_CW];
+      if constexpr (NBUF == 1 && NCH <= 4) {
+        // single accumulator set: drain TMEM into registers first and release it, so the
+        // next tile's MMAs overlap this tile's C read-modify-write
+        uint32_t v[NCH][TC_CW];
 #pragma unroll
-        for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int t = 0; t < TC_CW; ++t) {
-          uint32_t v;
-          if (NPOS <= 5) {
-            uint64_t x = 0;
-#pragma unroll
-            for (int s = 0; s < NPOS; ++s) x += (uint64_t)acc[s][t] << (8 * s);
-            v = reduce64(x, mp);
-          } else {
-            uint64_t hi = 0;
-#pragma unroll
-            for (int s = 4; s < NPOS; ++s) hi += (uint64_t)acc[s][t] << (8 * (s - 4));
-            uint64_t x = (uint64_t)reduce64(hi, mp) << 32;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) x += (uint64_t)acc[s][t] << (8 * s);
-            v = reduce64(x, mp);
-          }
-          tr[lane * (TC_CW + 1) + t] = v;
-        }
+        for (int ch = 0; ch < NCH; ++ch) combine(lane_base, h * HALF + ch * TC_CW, v[ch]);
+        tc_fence_before();
         __syncwarp();
-        const int col = n0 + cc + tc_col;
-        uint32_t w[16], cur[16];
+        if (lane == 0) mbar_arrive(&tempty[buf]);
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int rr = tc_row0 + 2 * kk, row = m0 + q * 32 + rr;
-          w[kk] = tr[rr * (TC_CW + 1) + tc_col];
-          cur[kk] = (row < c.m && col < c.n) ? c.row(row)[col] : 0u;
+        for (int ch = 0; ch < NCH; ++ch) apply(m0, n0, h * HALF + ch * TC_CW, v[ch]);
+      } else {
+#pragma unroll 1
+        for (int cc = h * HALF; cc < (h + 1) * HALF; cc += TC_CW) {
+          uint32_t v[TC_CW];
+          combine(lane_base, cc, v);
+          apply(m0, n0, cc, v);
         }
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int row = m0 + q * 32 + tc_row0 + 2 * kk;
-          if (row < c.m && col < c.n) c.row(row)[col] = submod(cur[kk], w[kk], mp);
-        }
-        __syncwarp();  // tr is reused by the next chunk
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   tc_fence_before();
@@ -354,6 +377,58 @@ __global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_p
       *reinterpret_cast<uint32_t*>(out + l * plane + (int64_t)(j0 + jj) * k_pad + k0 + kq) = packed;
     }
   }
+}
+
+// ------------------------- peak microbenchmarks -------------------------
+// int8 tensor-core peak: one elected thread per CTA issues `iters` back-to-back
+// tcgen05.mma.kind::i8 128x256x32 (SS operands, 32 KB of shared memory, contents
+// irrelevant) into one TMEM accumulator; one CTA per SM.  ops = 2*128*256*32 per MMA.
+__global__ void __launch_bounds__(128, 1) mma_peak_i8_kernel(int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_pk[];
+  __shared__ uint64_t done;
+  __shared__ uint32_t holder;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_pk) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(&holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t t = holder;
+  if (threadIdx.x == 32) {
+    constexpr uint32_t idesc = idesc_i8(256);
+    const uint64_t ad = desc_k_sw128(smem_u32(base));
+    const uint64_t bd = desc_k_sw128(smem_u32(base + 128 * 128));
+    for (int i = 0; i < iters; ++i) mma_i8(t, ad, bd, idesc, i > 0 ? 1u : 0u);
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(t, 256);
+  }
+}
+
+// FP64 DMMA peak (mma.sync m8n8k4): every warp runs `iters` dependent-free groups of 4
+// independent MMAs; flops = 2*8*8*4 per MMA.
+__global__ void __launch_bounds__(256) mma_peak_f64_kernel(int iters, double* sink) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c0[2] = {0, 0}, c1[2] = {0, 0}, c2[2] = {0, 0}, c3[2] = {0, 0};
+  for (int i = 0; i < iters; ++i) {
+#define PLUQ_DMMA(c)                                                                                      \
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"            \
+               : "+d"(c[0]), "+d"(c[1])                                                                  \
+               : "d"(a), "d"(b))
+    PLUQ_DMMA(c0); PLUQ_DMMA(c1); PLUQ_DMMA(c2); PLUQ_DMMA(c3);
+#undef PLUQ_DMMA
+  }
+  const double s = c0[0] + c0[1] + c1[0] + c1[1] + c2[0] + c2[1] + c3[0] + c3[1];
+  if (s == 12345.678) sink[threadIdx.x] = s;  // keep the work alive
 }
 
 // ------------------------------- host side ---------------------------------------------
