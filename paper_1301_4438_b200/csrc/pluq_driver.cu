@@ -101,6 +101,8 @@ struct pluq_ctx {
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
   int64_t diag_lazy = 1;           // speculative LU: lazy-reduction diagonal-block kernel
+  int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
+  int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 8;         // pipeline depth of the host-buffer batched path
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
@@ -194,6 +196,16 @@ struct pluq_ctx {
   void dfree(void* p) {
     if (p) CU(cudaFreeAsync(p, stream));
   }
+  template <typename T>
+  T* dalloc_on(size_t count, cudaStream_t s) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    CU(cudaMallocAsync(&p, count * sizeof(T), s));
+    return reinterpret_cast<T*>(p);
+  }
+  void dfree_on(void* p, cudaStream_t s) {
+    if (p) CU(cudaFreeAsync(p, s));
+  }
   void check_launch() {
     ++st_launch;
     cudaError_t e = cudaGetLastError();
@@ -209,12 +221,15 @@ struct Ops {
   pluq_ctx* c;
   ModP mp;
   const int* stop = nullptr;  // device stop flag of the speculative path (nullptr: none)
+  cudaStream_t st = nullptr;  // stream of this Ops (nullptr: the context's stream)
+  int max_ctas = 0;           // cap on the tensor-core GEMM's persistent grid (0: one CTA per SM)
+  cudaStream_t s() const { return st ? st : c->stream; }
 
   // ---- modular GEMM: C <- C - A B  (kernels.py:38-55) ------------------------------
   void gemm(const View& cv, const View& av, const View& bv) {
     if (cv.m == 0 || cv.n == 0 || av.n == 0) return;
     if (c->use_tc && cv.m >= c->tc_min_dim && cv.n >= c->tc_min_dim && av.n >= c->tc_min_k) {
-      int st = c->tc.run(cv, av, bv, mp, c->stream, stop);
+      int st = c->tc.run(cv, av, bv, mp, s(), stop, max_ctas);
       if (st == kOk) { ++c->st_tc; c->st_launch += 3; return; }
       if (st != kUnsupported) throw PluqError(st, "tensor-core GEMM failed: " + c->tc.last_error);
     }
@@ -227,9 +242,9 @@ struct Ops {
       return;
     }
     if (mp.kchunk < 2 * SG_BK)
-      simt_gemm_kernel<true><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp, stop);
+      simt_gemm_kernel<true><<<grid, 256, 0, s()>>>(cv, av, bv, mp, stop);
     else
-      simt_gemm_kernel<false><<<grid, 256, 0, c->stream>>>(cv, av, bv, mp, stop);
+      simt_gemm_kernel<false><<<grid, 256, 0, s()>>>(cv, av, bv, mp, stop);
     ++c->st_simt;
     c->check_launch();
   }
@@ -245,16 +260,16 @@ struct Ops {
     const int r = l.m;
     if (r == 0 || b.n == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
-    uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_lower_unit_kernel<<<nb, 256, 0, c->stream>>>(l, inv, mp, stop);
+    uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
+    trinv_lower_unit_kernel<<<nb, 256, 0, s()>>>(l, inv, mp, stop);
     c->check_launch();
     trsm_l_rec(l, b, inv);
-    c->dfree(inv);
+    c->dfree_on(inv, s());
   }
   void trsm_l_rec(const View& l, const View& b, const uint32_t* inv) {
     const int r = l.m;
     if (r <= TR_BASE) {
-      trsm_apply_left_kernel<<<(b.n + 31) / 32, 128, 0, c->stream>>>(inv, b, mp, stop);
+      trsm_apply_left_kernel<<<(b.n + 31) / 32, 128, 0, s()>>>(inv, b, mp, stop);
       c->check_launch();
       return;
     }
@@ -269,16 +284,16 @@ struct Ops {
     const int r = u.m;
     if (r == 0 || b.m == 0) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
-    uint32_t* inv = c->dalloc<uint32_t>((size_t)nb * TR_BASE * TR_BASE);
-    trinv_upper_kernel<<<nb, 256, 0, c->stream>>>(u, inv, mp, c->invtab(mp.p), stop);
+    uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
+    trinv_upper_kernel<<<nb, 256, 0, s()>>>(u, inv, mp, c->invtab(mp.p), stop);
     c->check_launch();
     trsm_u_rec(b, u, inv);
-    c->dfree(inv);
+    c->dfree_on(inv, s());
   }
   void trsm_u_rec(const View& b, const View& u, const uint32_t* inv) {
     const int r = u.m;
     if (r <= TR_BASE) {
-      trsm_apply_right_kernel<<<(b.m + 31) / 32, 128, 0, c->stream>>>(b, inv, mp, stop);
+      trsm_apply_right_kernel<<<(b.m + 31) / 32, 128, 0, s()>>>(b, inv, mp, stop);
       c->check_launch();
       return;
     }
@@ -554,6 +569,21 @@ struct Driver {
     else CU(cudaFuncSetAttribute(diag_crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     bool stopped_early = false;
     int blk = 0;
+    // Look-ahead: the outer update of panel P is split into the next panel's columns
+    // (critical path, this stream) and the rest, which runs on a side stream with a
+    // capped grid while panel P+1 is factored.  The side update is predicated on a
+    // snapshot of the stop flag taken at the end of panel P, so a zero pivot found in
+    // a later panel leaves it exactly as the sequential schedule would.
+    const bool la = c->lookahead != 0;
+    cudaStream_t side = c->side_streams()[5];
+    const int npanels = (mn + W - 1) / W;
+    int* snap = la ? c->dalloc<int>((size_t)npanels + 1) : nullptr;
+    cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+    if (la) {
+      CU(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+    }
+    bool side_pending = false;
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
       // inner right-looking LU of the panel columns [ps, pe)
@@ -581,8 +611,36 @@ struct Driver {
       if (stopped_early) break;
       // outer step: U rows [ps, pe) right of the panel, then the K = W trailing update
       const View l11 = x.sub(ps, ps, pe - ps, pe - ps);
-      sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
-      sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, n - pe));
+      if (side_pending) {  // rows [ps, pe) right of this panel came from the previous side update
+        CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+        side_pending = false;
+      }
+      const int ne = std::min(pe + W, n);
+      if (la && pe < mn && ne < n) {
+        sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne - pe));
+        sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, ne - pe));
+        const int pidx = ps / W;
+        CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+        CU(cudaEventRecord(ev_main, c->stream));
+        CU(cudaStreamWaitEvent(side, ev_main, 0));
+        Ops aops = ops;
+        aops.st = side;
+        aops.stop = snap + pidx;
+        aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
+        aops.trsm_l(l11, x.sub(ps, ne, pe - ps, n - ne));
+        aops.gemm(x.sub(pe, ne, m - pe, n - ne), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
+        CU(cudaEventRecord(ev_side, side));
+        side_pending = true;
+      } else {
+        sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+        sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, n - pe));
+      }
+    }
+    if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+    if (la) {
+      c->dfree(snap);
+      cudaEventDestroy(ev_main);
+      cudaEventDestroy(ev_side);
     }
     if (!stopped_early) {
       CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -919,6 +977,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "fixed_kernels") c->fixed_kernels = value;
   else if (k == "host_chunks") c->host_chunks = value;
   else if (k == "diag_lazy") c->diag_lazy = value;
+  else if (k == "lookahead") c->lookahead = value;
+  else if (k == "la_reserve") c->la_reserve = value;
   else if (k == "exact_kernel") c->exact_kernel = value;
   else if (k == "rpm_threads") c->rpm_threads = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;

@@ -498,7 +498,8 @@ struct TcGemm {
   }
 
   template <int L, int V>
-  int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop) {
+  int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop,
+             int max_ctas) {
     constexpr int BN = TcCfg<L, V>::BN;
     const int m = c.m, n = c.n, k = a.n;
     const int m_pad = (m + TC_BM - 1) / TC_BM * TC_BM;
@@ -544,7 +545,8 @@ struct TcGemm {
         return kCuda;
       }
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
-      const int grid = std::min(tiles, grid_override > 0 ? grid_override : num_sms());
+      const int grid =
+          std::min(tiles, max_ctas > 0 ? max_ctas : grid_override > 0 ? grid_override : num_sms());
       tc_modgemm_kernel<L, V><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop,
                                                               dbg);
       cudaError_t e = cudaGetLastError();
@@ -560,24 +562,25 @@ struct TcGemm {
     return kOk;
   }
 
-  int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop = nullptr) {
+  int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop = nullptr,
+          int max_ctas = 0) {
     if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
     if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
     if (!load()) return kUnsupported;
     const int L = limbs(mp.p);
     if (variant == 0) {
       switch (L) {
-        case 1: return launch<1, 0>(c, a, b, mp, st, stop);
-        case 2: return launch<2, 0>(c, a, b, mp, st, stop);
-        case 3: return launch<3, 0>(c, a, b, mp, st, stop);
-        case 4: return launch<4, 0>(c, a, b, mp, st, stop);
+        case 1: return launch<1, 0>(c, a, b, mp, st, stop, max_ctas);
+        case 2: return launch<2, 0>(c, a, b, mp, st, stop, max_ctas);
+        case 3: return launch<3, 0>(c, a, b, mp, st, stop, max_ctas);
+        case 4: return launch<4, 0>(c, a, b, mp, st, stop, max_ctas);
       }
     } else {
       switch (L) {
-        case 1: return launch<1, 1>(c, a, b, mp, st, stop);
-        case 2: return launch<2, 1>(c, a, b, mp, st, stop);
-        case 3: return launch<3, 1>(c, a, b, mp, st, stop);
-        case 4: return launch<4, 1>(c, a, b, mp, st, stop);
+        case 1: return launch<1, 1>(c, a, b, mp, st, stop, max_ctas);
+        case 2: return launch<2, 1>(c, a, b, mp, st, stop, max_ctas);
+        case 3: return launch<3, 1>(c, a, b, mp, st, stop, max_ctas);
+        case 4: return launch<4, 1>(c, a, b, mp, st, stop, max_ctas);
       }
     }
     return kUnsupported;

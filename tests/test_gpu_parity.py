@@ -486,3 +486,41 @@ def test_speculative_path_vs_oracle(pb, name, m, n, r, p):
         assert st["speculative_fail"] >= 1
     else:
         assert st["speculative_ok"] >= 1
+
+
+# 128-wide diagonal blocks (diag_lazy_kernel) with zero pivots inside / on the edge of a
+# full block and look-ahead between two panels of 256 columns
+SPEC128_CASES = [
+    ("full", 400, 400, None),
+    ("rank200", 400, 380, 200),     # zero pivot at t = 72 of the second 128-block
+    ("rank128", 384, 384, 128),     # zero pivot on a block boundary
+    ("rank50", 300, 300, 50),       # zero pivot inside the first block
+    ("profile", 300, 400, 150),     # non-generic: restore + exact recursion
+]
+
+
+@pytest.mark.parametrize("name,m,n,r", SPEC128_CASES)
+def test_speculative_128_blocks_vs_oracle(pb, name, m, n, r):
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    if name == "profile":
+        a0, _, _ = orc.gen_cfg4(seed=5, m=m, n=n, r=r, p=p)
+    elif r is None:
+        a0 = np.random.default_rng(m + n).integers(0, p, (m, n))
+    else:
+        a0 = orc.gen_xy_rank(m, n, r, p, 13)
+    P, Q, R, packed, cnt = _oracle(a0, p)
+    ctx = _native.context()
+    ctx.set_option("small_cap", 1)
+    ctx.set_option("spec_panel", 256)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0)
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        ctx.set_option("small_cap", 128 * 128)
+        ctx.set_option("spec_panel", 1024)
+    _check(f, a.data, P, Q, R, packed, cnt, c)
+    assert st["speculative_fail" if name == "profile" else "speculative_ok"] >= 1

@@ -101,3 +101,15 @@ elif mode == "e2etrace":
             dt2 = time.perf_counter() - t1
             print(f"{spec}: e2e {1e3*dt:.3f} ms  raw C call (reused outputs, already factored input) {1e3*dt2:.3f} ms", flush=True)
     ctx.set_option("trace_pipeline", 0)
+elif mode == "cfg5":
+    from paper_1301_4438_b200 import gen
+    for kv in os.environ.get("PLUQ_OPTS", "").split(","):
+        if kv:
+            kk, vv = kv.split("="); _native.context().set_option(kk, int(vv))
+    div = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    m = 65536 // div; r = 32768 // div
+    a0 = gen.gen_xy_rank_device(m, m, r, P, seed=0)
+    for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 1):
+        x = a0.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
+        f = pb.pluq(pb.DenseMatrix(pb.PrimeField(P), x)); torch.cuda.synchronize()
+        print(f"cfg5/{div}: {1e3*(time.perf_counter()-t0):.1f} ms rank {f.rank}", flush=True)
