@@ -103,7 +103,8 @@ struct pluq_ctx {
   int64_t diag_lazy = 1;           // speculative LU: lazy-reduction diagonal-block kernel
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
-  int64_t host_chunks = 8;         // pipeline depth of the host-buffer batched path
+  int64_t host_chunks = 16;        // pipeline depth of the host-buffer batched path
+  int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
@@ -976,6 +977,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "time_kernels") c->time_kernels = value;
   else if (k == "fixed_kernels") c->fixed_kernels = value;
   else if (k == "host_chunks") c->host_chunks = value;
+  else if (k == "chunk_shape") c->chunk_shape = value;
   else if (k == "diag_lazy") c->diag_lazy = value;
   else if (k == "lookahead") c->lookahead = value;
   else if (k == "la_reserve") c->la_reserve = value;
@@ -1189,7 +1191,24 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     // the f64 conversion (sfb: a handful of CTAs, latency-bound, so it overlaps the next
     // chunk's generic kernel), and D2H of chunk k-1 (sout).
     const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(c->host_chunks, batch));
-    const int64_t per = (batch + nchunks - 1) / nchunks;
+    // tent-shaped chunk sizes (weights min(k+1, C-k)): the D2H stream is the bottleneck
+    // once it runs, so the first chunk is small (D2H starts early) and so is the last
+    // (its compute and D2H follow the final H2D)
+    std::vector<int64_t> cb0(nchunks + 1, 0);
+    {
+      const int64_t C = nchunks;
+      int64_t wsum = 0;
+      auto wt = [&](int64_t kk) { return c->chunk_shape ? std::min(kk + 1, C - kk) : int64_t(1); };
+      for (int64_t kk = 0; kk < C; ++kk) wsum += wt(kk);
+      int64_t acc = 0, wacc = 0;
+      for (int64_t kk = 0; kk < C; ++kk) {
+        wacc += wt(kk);
+        const int64_t end = kk == C - 1 ? batch : std::max(acc, batch * wacc / wsum);
+        cb0[kk] = acc;
+        acc = end;
+      }
+      cb0[C] = batch;
+    }
     double* raw = c->dalloc<double>((size_t)batch * mn);
     uint32_t* dA = c->dalloc<uint32_t>((size_t)batch * mn);
     int32_t* dp = c->dalloc<int32_t>((size_t)(batch * (m + n + 1)));
@@ -1232,7 +1251,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     const size_t cs = crout_smem_bytes(m, n);
     CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
     // flags: per-block generic flag [batch] | per-chunk failure count [nchunks] | failure
-    // list [batch] (chunk k lists its failures, as global indices, from slot k*per on)
+    // list [batch] (chunk k lists its failures, as global indices, from slot cb0[k] on)
     int* flags = a.try_generic ? c->dalloc<int>(2 * (size_t)batch + nchunks) : nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
     if (flags) CU(cudaMemsetAsync(flags + batch, 0, sizeof(int) * nchunks, c->stream));
@@ -1240,8 +1259,8 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     CU(cudaEventRecord(ev0, sin));
     int64_t last = 0;
     for (int64_t k = 0; k < nchunks; ++k) {
-      const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
-      if (nb <= 0) break;
+      const int64_t b0 = cb0[k], nb = cb0[k + 1] - cb0[k];
+      if (nb <= 0) continue;
       last = k;
       CU(cudaMemcpyAsync(raw + b0 * mn, hA + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyHostToDevice, sin));
       CU(cudaEventRecord(ev_in[k], sin));
@@ -1291,7 +1310,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     CU(cudaEventRecord(ev_end, sout));
     for (int64_t k = 0; k <= last; ++k) {
       CU(cudaEventSynchronize(ev_res[k]));
-      const int64_t b0 = k * per, nb = std::min<int64_t>(per, batch - b0);
+      const int64_t b0 = cb0[k], nb = cb0[k + 1] - cb0[k];
       for (int64_t i = b0 * m; i < (b0 + nb) * m; ++i) psig[i] = host[i];
       for (int64_t i = b0 * n; i < (b0 + nb) * n; ++i) qsig[i] = host[batch * m + i];
       for (int64_t i = b0; i < b0 + nb; ++i) ranks[i] = host[batch * (m + n) + i];

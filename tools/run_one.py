@@ -113,3 +113,18 @@ elif mode == "cfg5":
         x = a0.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
         f = pb.pluq(pb.DenseMatrix(pb.PrimeField(P), x)); torch.cuda.synchronize()
         print(f"cfg5/{div}: {1e3*(time.perf_counter()-t0):.1f} ms rank {f.rank}", flush=True)
+elif mode == "e2emed":
+    # median of 10 untraced host-buffer batched calls per option setting
+    import statistics
+    src = orc.gen_cfg2(seed=0, batch=4096).astype(np.float64)
+    h = torch.from_numpy(src).pin_memory(); pin = h.numpy()
+    ctx = _native.context()
+    for rep in range(2):
+        for spec in sys.argv[2:]:
+            for kv in spec.split(","):
+                kk, v = kv.split("="); ctx.set_option(kk, int(v))
+            ts = []
+            for it in range(12):
+                pin[...] = src
+                t0 = time.perf_counter(); r = pb.pluq_batched(pin, P, 30); ts.append(time.perf_counter() - t0)
+            print(f"{spec}: e2e median {1e3*statistics.median(ts[2:]):.3f} ms min {1e3*min(ts[2:]):.3f}", flush=True)
