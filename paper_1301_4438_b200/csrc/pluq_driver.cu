@@ -445,8 +445,20 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
                          const int* fc, cudaStream_t st) {
   if (c->exact_kernel) {
     const size_t smem = rpm_smem_bytes(a.m, a.n);
-    CU(cudaFuncSetAttribute(rpm_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    rpm_pluq_kernel<<<grid, (unsigned)c->rpm_threads, smem, st>>>(a, fl, fc);
+    const unsigned nt = (unsigned)c->rpm_threads;
+    switch (rpm_shape(a.m, a.n, (int)nt)) {
+      case 1:
+        CU(cudaFuncSetAttribute(rpm_pluq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rpm_pluq_kernel<1><<<grid, nt, smem, st>>>(a, fl, fc);
+        break;
+      case 2:
+        CU(cudaFuncSetAttribute(rpm_pluq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rpm_pluq_kernel<2><<<grid, nt, smem, st>>>(a, fl, fc);
+        break;
+      default:
+        CU(cudaFuncSetAttribute(rpm_pluq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rpm_pluq_kernel<0><<<grid, nt, smem, st>>>(a, fl, fc);
+    }
   } else {
     const size_t smem = small_smem_bytes(a.m, a.n, a.threshold);
     CU(cudaFuncSetAttribute(small_pluq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -100,6 +100,9 @@ __device__ void small_pluq_block(const SmallArgs& args, int blk) {
 
 // Exact PLUQ of one block through its rank profile matrix (pluq_rpm.cuh): same outputs
 // as small_pluq_block, three short phases instead of the field-arithmetic recursion.
+// SHAPE (one code path per instantiation keeps each kernel small): 1 = registers, n <= 64
+// and <= 4 rows per warp; 2 = registers, n <= 128 and <= 8 rows per warp; 0 = shared memory.
+template <int SHAPE>
 __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   __shared__ Counts s_cnt;
@@ -123,19 +126,18 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   uint32_t* diag = dpre + mn;
   uint32_t* rowbuf = diag + mn;
   int* stk = reinterpret_cast<int*>(rowbuf + 256);
-  // register-resident phases when the block fits (n <= 64 with <= 4 rows per warp),
-  // shared-memory phases otherwise (one instantiation keeps the kernel's code small)
-  const int shape = (n <= 64 && m <= 4 * nw) ? 1 : 0;
+  constexpr int shape = SHAPE;
   for (int t = tid; t < m; t += nt) rows[t] = t;
   for (int t = tid; t < n; t += nt) cols[t] = t;
-  if (shape == 0) {
+  if constexpr (shape == 0) {
     for (int i = w; i < m; i += nw)
       for (int j = lane; j < n; j += 32) W[i * ld + j] = ga[(int64_t)i * args.lda + j];
   }
   __syncthreads();
   RPM_MARK(1);
   int r;
-  if (shape == 1) r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  if constexpr (shape == 1) r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  else if constexpr (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
   RPM_MARK(2);
   if (tid < 32) {
@@ -150,9 +152,12 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   __syncthreads();
   RPM_MARK(4);
   const bool inv = args.invtab != nullptr;
-  if (shape == 1) {
+  if constexpr (shape == 1) {
     if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+  } else if constexpr (shape == 2) {
+    if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+    else lu_reg<4, 8, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else {
     for (int t = w; t < m; t += nw) {  // A'[t][u] = A[P^-1(t)][Q(u)]
       const uint32_t* src = ga + (int64_t)pinv[t] * args.lda;
@@ -185,16 +190,23 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
 }
 
 // One CTA per block, or a persistent grid over the failure list of the generic kernel.
-__global__ void __launch_bounds__(512) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+template <int SHAPE>
+__global__ void __launch_bounds__(512, 1) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
   if (fail_list) {
     const int cnt = *fail_count;
     for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-      rpm_pluq_block(args, fail_list[q]);
+      rpm_pluq_block<SHAPE>(args, fail_list[q]);
       __syncthreads();
     }
     return;
   }
-  rpm_pluq_block(args, blockIdx.x);
+  rpm_pluq_block<SHAPE>(args, blockIdx.x);
+}
+
+// register shape of rpm_pluq_kernel for an m x n block with `threads` per CTA
+inline int rpm_shape(int m, int n, int threads) {
+  const int nw = threads / 32;
+  return (n <= 64 && m <= 4 * nw) ? 1 : (n <= 128 && m <= 8 * nw) ? 2 : 0;
 }
 
 inline size_t rpm_smem_bytes(int64_t m, int64_t n) { return (size_t)rpm_smem_words(m, n) * 4; }

@@ -128,3 +128,14 @@ elif mode == "e2emed":
                 pin[...] = src
                 t0 = time.perf_counter(); r = pb.pluq_batched(pin, P, 30); ts.append(time.perf_counter() - t0)
             print(f"{spec}: e2e median {1e3*statistics.median(ts[2:]):.3f} ms min {1e3*min(ts[2:]):.3f}", flush=True)
+elif mode == "cfg4":
+    from paper_1301_4438_b200 import gen
+    for kv in os.environ.get("PLUQ_OPTS", "").split(","):
+        if kv:
+            kk, vv = kv.split("="); _native.context().set_option(kk, int(vv))
+    div = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    a0, _, _ = gen.gen_cfg4_device(16384 // div, 32768 // div, 8192 // div, 8388593, seed=0)
+    for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 1):
+        x = a0.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
+        f = pb.pluq(pb.DenseMatrix(pb.PrimeField(8388593), x)); torch.cuda.synchronize()
+        print(f"cfg4/{div}: {1e3*(time.perf_counter()-t0):.1f} ms rank {f.rank} {pb.last_stats()}", flush=True)
