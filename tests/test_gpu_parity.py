@@ -495,6 +495,8 @@ SPEC128_CASES = [
     ("rank200", 400, 380, 200),     # zero pivot at t = 72 of the second 128-block
     ("rank128", 384, 384, 128),     # zero pivot on a block boundary
     ("rank50", 300, 300, 50),       # zero pivot inside the first block
+    ("rank300", 600, 640, 300),     # zero pivot in the SECOND panel: the look-ahead side update
+                                    # of panel 0 (snapshot taken before the stop) must complete
     ("profile", 300, 400, 150),     # non-generic: restore + exact recursion
 ]
 
@@ -524,3 +526,18 @@ def test_speculative_128_blocks_vs_oracle(pb, name, m, n, r):
         ctx.set_option("spec_panel", 1024)
     _check(f, a.data, P, Q, R, packed, cnt, c)
     assert st["speculative_fail" if name == "profile" else "speculative_ok"] >= 1
+
+
+@pytest.mark.parametrize("bsz", [1, 5, 17, 100])
+def test_batched_host_odd_sizes(pb, bsz):
+    """Host-buffer batches whose tent-shaped chunking leaves empty / uneven chunks."""
+    p = 65521
+    rng = np.random.default_rng(bsz)
+    batch = rng.integers(0, p, (bsz, 64, 64)).astype(np.float64)
+    batch[::3] = np.stack([orc.gen_xy_rank(64, 64, 20, p, s).astype(np.float64) for s in range(0, bsz, 3)])
+    orig = batch.copy()
+    res = pb.pluq_batched(batch, p, 30)
+    for b in range(bsz):
+        P, Q, r, packed, _ = _oracle(orig[b].astype(np.int64), p)
+        assert res.ranks[b] == r and np.array_equal(res.p_sigma[b], P) and np.array_equal(res.q_sigma[b], Q)
+        assert np.array_equal(batch[b], packed)
