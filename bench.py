@@ -358,6 +358,10 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
     torch.cuda.synchronize(dev)
     _native.raise_for(st, ctx, "tc gemm")
     t = ev0.elapsed_time(ev1) / 1e3 / reps
+    ctx.set_option("tc_time", 1)  # one extra call: the MMA kernel alone, without the limb split
+    ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, P)
+    t_mma = ctx.stats()["t_tc_mma_ns"] / 1e9
+    ctx.set_option("tc_time", 0)
     limbs = 2
     # the int8 (tcgen05 kind::i8) and FP64 peaks are microbenchmarked on this box
     pk = max((ctx.measure_peaks() for _ in range(3)), key=lambda d: d["int8_tops"])
@@ -372,6 +376,8 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOP/s",
                      "frac": achieved / int8_peak, "peak_kind": "measured (tcgen05 kind::i8 microbenchmark)",
                      "frac_vs_2x_bf16": achieved / (2.0 * bf16),
+                     "mma_kernel_ms": t_mma * 1e3,
+                     "mma_kernel_frac": (2.0 * m * n * k * limbs * limbs / t_mma / 1e12 / int8_peak) if t_mma > 0 else None,
                      "note": "int8 ops = 2mnk * L^2 (L = 2 limbs for p = 65521); includes the limb-split "
                              "conversion passes"},
     }

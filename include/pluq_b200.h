@@ -118,8 +118,10 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
  * out[1] = FP64 DMMA (mma.sync m8n8k4) TFLOP/s.  Diagnostics; not on the factorization path. */
 int pluq_measure_peaks(pluq_ctx* ctx, double* out, int64_t nout);
 
-/* Device-side statistics of the last pluq_factor call (kernel launches, host syncs,
- * nodes, tensor-core GEMM launches and their summed device time in ms). */
+/* Statistics of the last call: launches, host syncs, nodes, small-node kernels, base-case
+ * kernels, tensor-core / SIMT GEMMs, zero-block skips, generic leaves, speculative ok/fail,
+ * generic- and fallback-kernel ns of a batch (option time_kernels), and the MMA-kernel ns of
+ * the last tensor-core GEMM (option tc_time). */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);
 
 #ifdef __cplusplus

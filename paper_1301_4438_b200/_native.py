@@ -117,11 +117,11 @@ class Context:
         raise_for(self.lib.pluq_set_option(self.handle, key.encode(), int(value)), self, f"option {key}")
 
     def stats(self) -> dict:
-        buf = (ctypes.c_int64 * 13)()
-        self.lib.pluq_last_stats(self.handle, buf, 13)
+        buf = (ctypes.c_int64 * 14)()
+        self.lib.pluq_last_stats(self.handle, buf, 14)
         keys = ["launches", "host_syncs", "nodes", "small_node_kernels", "basecase_kernels",
                 "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves", "speculative_ok",
-                "speculative_fail", "t_generic_ns", "t_fallback_ns"]
+                "speculative_fail", "t_generic_ns", "t_fallback_ns", "t_tc_mma_ns"]
         return dict(zip(keys, list(buf)))
 
     def measure_peaks(self) -> dict:

@@ -985,6 +985,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_cfg") c->tc.variant = (int)value;
   else if (k == "tc_grid") c->tc.grid_override = (int)value;
   else if (k == "tc_dbg") c->tc.dbg = (int)value;
+  else if (k == "tc_vec") c->tc.vec_limbs = (int)value;
+  else if (k == "tc_time") c->tc.time_mma = (int)value;
   else if (k == "try_generic") c->try_generic = value;
   else if (k == "time_kernels") c->time_kernels = value;
   else if (k == "fixed_kernels") c->fixed_kernels = value;
@@ -1056,10 +1058,11 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[13] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+  int64_t v[14] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
                    c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail,
-                   (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f)};
-  for (int64_t i = 0; i < nout && i < 13; ++i) out[i] = v[i];
+                   (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f),
+                   (int64_t)(c->tc.mma_ms * 1e6f)};
+  for (int64_t i = 0; i < nout && i < 14; ++i) out[i] = v[i];
   return kOk;
 }
 

@@ -379,6 +379,44 @@ __global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_p
   }
 }
 
+// Vectorised limb split of a row-major view: 16 consecutive k per thread, one 16-byte
+// store per limb plane (k_pad is a multiple of 128, so every store is aligned).
+__global__ void limb_rows16_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  const int64_t plane = (int64_t)rows_pad * k_pad;
+  const int kq = k_pad / 16;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rows_pad * kq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / kq), k16 = (int)(t - (int64_t)i * kq) * 16;
+    uint32_t w[16];
+    if (i < v.m) {
+      const uint32_t* r = v.row(i) + k16;
+      if (k16 + 16 <= v.n && (reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint4 q = reinterpret_cast<const uint4*>(r)[e];
+          w[4 * e] = q.x; w[4 * e + 1] = q.y; w[4 * e + 2] = q.z; w[4 * e + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) w[e] = (k16 + e < v.n) ? r[e] : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) w[e] = 0u;
+    }
+    for (int l = 0; l < L; ++l) {
+      const int sh = 8 * l;
+      uint32_t pk[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        pk[e] = ((w[4 * e] >> sh) & 255u) | (((w[4 * e + 1] >> sh) & 255u) << 8) |
+                (((w[4 * e + 2] >> sh) & 255u) << 16) | (((w[4 * e + 3] >> sh) & 255u) << 24);
+      *reinterpret_cast<uint4*>(out + l * plane + (int64_t)i * k_pad + k16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+  }
+}
+
 // ------------------------- peak microbenchmarks -------------------------
 // int8 tensor-core peak: one elected thread per CTA issues `iters` back-to-back
 // tcgen05.mma.kind::i8 128x256x32 (SS operands, 32 KB of shared memory, contents
@@ -444,6 +482,9 @@ struct TcGemm {
   int variant = 1;              // TcCfg variant (option tc_cfg)
   int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
   int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring
+  int vec_limbs = 1;            // vectorised limb-split kernels (option tc_vec)
+  int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
+  float mma_ms = 0.f;           // summed MMA-kernel time of the last call when timed
 
   static int limbs(uint32_t p) {
     int bits = 0;
@@ -529,14 +570,18 @@ struct TcGemm {
       const int k_pad = (kc + TC_BK - 1) / TC_BK * TC_BK;
       View as = a.sub(0, (int)k0, m, kc);
       View bs = b.sub((int)k0, 0, kc, n);
-      {
+      if (vec_limbs) {
+        const int64_t work = (int64_t)m_pad * (k_pad / 16);
+        const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
+        limb_rows16_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad, stop);
+      } else {
         int64_t work = (int64_t)m_pad * (k_pad / 4);
         int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 32);
         limb_rows_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad, stop);
       }
       {
-        dim3 grid(n_pad / 32, k_pad / 32);
-        limb_cols_kernel<<<grid, 256, 0, st>>>(bs, db, L, n_pad, k_pad, stop);
+        dim3 cgrid(n_pad / 32, k_pad / 32);
+        limb_cols_kernel<<<cgrid, 256, 0, st>>>(bs, db, L, n_pad, k_pad, stop);
       }
       CUtensorMap ta, tb;
       if (!make_map(&ta, da, k_pad, (int64_t)L * m_pad, TC_BM) || !make_map(&tb, db, k_pad, (int64_t)L * n_pad, BN)) {
@@ -547,8 +592,23 @@ struct TcGemm {
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
       const int grid =
           std::min(tiles, max_ctas > 0 ? max_ctas : grid_override > 0 ? grid_override : num_sms());
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (time_mma) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+      }
       tc_modgemm_kernel<L, V><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop,
                                                               dbg);
+      if (time_mma) {
+        float ms = 0.f;
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        mma_ms += ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) {
         last_error = std::string("tc_modgemm launch: ") + cudaGetErrorString(e);
@@ -564,6 +624,7 @@ struct TcGemm {
 
   int run(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop = nullptr,
           int max_ctas = 0) {
+    mma_ms = 0.f;
     if (c.m == 0 || c.n == 0 || a.n == 0) return kOk;
     if (c.m > (1 << 24) || c.n > (1 << 24)) return kUnsupported;
     if (!load()) return kUnsupported;
