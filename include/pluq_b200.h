@@ -113,6 +113,10 @@ int pluq_modgemm_sub_tc(pluq_ctx* ctx, uint32_t* dC, int64_t ldc, const uint32_t
  * `rank` (leading principal minors 1..rank nonzero), where P = Q = I.  Host-only. */
 int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, int64_t* counts);
 
+/* *out = 1 if the device view (uint32, pitch ld) has a nonzero entry, else 0.  Used by the
+ * multi-GPU driver for the "Schur complement vanishes" test (recursive.py:188-189 zero blocks). */
+int pluq_nonzero(pluq_ctx* ctx, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t* out);
+
 /* Microbenchmarked peaks of this device (SURVEY §8d roofline denominators):
  * out[0] = tcgen05 kind::i8 dense TOP/s (128x256x32 MMAs, one CTA per SM),
  * out[1] = FP64 DMMA (mma.sync m8n8k4) TFLOP/s.  Diagnostics; not on the factorization path. */

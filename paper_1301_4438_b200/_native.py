@@ -29,6 +29,7 @@ SIGNATURES = {
     "pluq_last_error": (ctypes.c_char_p, [_p]),
     "pluq_last_stats": (ctypes.c_int, [_p, _pi64, _i64]),
     "pluq_measure_peaks": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_double), _i64]),
+    "pluq_nonzero": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _pi64]),
     "pluq_generic_counts": (ctypes.c_int, [_i64, _i64, _i64, _i64, _pi64]),
     "pluq_factor": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_iterative": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),

@@ -1007,6 +1007,14 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
 
 const char* pluq_last_error(pluq_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+int pluq_nonzero(pluq_ctx* c, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t* out) {
+  if (!out || m < 0 || n < 0 || (m > 0 && n > 0 && (!dA || ld < n))) return kInvalid;
+  return guarded(c, [&] {
+    Ops ops{c, ModP::make(2)};
+    *out = (m > 0 && n > 0) ? (ops.nonzero(View{const_cast<uint32_t*>(dA), ld, (int)m, (int)n}) ? 1 : 0) : 0;
+  });
+}
+
 int pluq_measure_peaks(pluq_ctx* c, double* out, int64_t nout) {
   if (!out || nout < 2) return kInvalid;
   return guarded(c, [&] {

@@ -1,0 +1,155 @@
+"""Single large matrix across ranks (paper_1301_4438_b200/distributed.py).
+
+CPU: world_size-2 gloo process group; the panel kernels are a numpy stand-in backend
+defined HERE (the product backend is the C ABI on each rank's GPU).  The assembled result
+must equal the oracle's pluq(A) bit for bit: P = Q = I, rank, packed, and the generic
+closed-form OpCounts; non-generic inputs must be detected so that rank 0 falls back to
+the exact single-GPU recursion.
+GPU: the CUDA backend in one process (every panel owned by rank 0) against the oracle.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import pluq_oracle as orc
+
+
+class NumpyPanelBackend:
+    """Test-only stand-in for CudaPanelBackend on CPU int64 torch tensors."""
+
+    def __init__(self, p, threshold):
+        self.p, self.threshold = p, threshold
+
+    def factor_panel(self, x):
+        a = x.numpy()
+        f = a.astype(orc.field_dtype(self.p))
+        P, Q, r, _ = orc.pluq(f, self.p, self.threshold)
+        a[...] = f.astype(np.int64)
+        return r, bool(np.array_equal(P, np.arange(a.shape[0])) and np.array_equal(Q, np.arange(a.shape[1])))
+
+    def trsm_llu(self, l, b):
+        bb = b.numpy().astype(orc.field_dtype(self.p))
+        orc.trsm_left_unit_lower(l.numpy().astype(orc.field_dtype(self.p)), bb, self.p, orc.Counts())
+        b.numpy()[...] = bb.astype(np.int64)
+
+    def gemm_sub(self, c, a, b):
+        cc = c.numpy()
+        cc[...] = np.mod(cc - orc.matmul_mod(a.numpy(), b.numpy(), self.p).astype(np.int64), self.p)
+
+    def is_zero(self, x):
+        return not x.numpy().any()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = [  # (name, m, n, rank or None, p, width)
+    ("full", 40, 40, None, 65521, 8),
+    ("wide", 24, 50, None, 65521, 8),
+    ("tall", 50, 24, None, 65521, 8),
+    ("rank20_mid_panel", 40, 44, 20, 65521, 8),   # zero pivot inside panel 2 (owner rank 0)
+    ("rank12_edge", 40, 40, 16, 65521, 8),        # zero pivot on a panel edge
+    ("small_p", 36, 36, None, 101, 8),
+    ("non_generic", 32, 40, 12, 101, 8),          # prescribed profiles -> not generic
+]
+
+
+def _matrix(name, m, n, r, p):
+    if name == "non_generic":
+        a, _, _ = orc.gen_cfg4(seed=2, m=m, n=n, r=r, p=p)
+        return a
+    if r is None:
+        return np.random.default_rng(m * n + p).integers(0, p, (m, n))
+    return orc.gen_xy_rank(m, n, r, p, 3)
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_4438_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for name, m, n, r, p, width in CASES:
+            a0 = _matrix(name, m, n, r, p)
+            full = torch.from_numpy(a0.astype(np.int64)) if rank == 0 else None
+            flags = D._Flags(torch.device("cpu"), torch.int64)
+            local = D.scatter_panels(full, n, width, lambda w: flags.new_panel(m, w))
+            owned = sorted(local)
+            rk = D.distributed_generic_lu(local, m, n, width, NumpyPanelBackend(p, 30), flags)
+            if rk is not None:
+                D.gather_panels(local, full if rank == 0 else None, n, width)
+            out.append((name, rk, owned, full.numpy().copy() if rank == 0 and rk is not None else None))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_distributed_panels_vs_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for i, (name, m, n, r, p, width) in enumerate(CASES):
+        a0 = _matrix(name, m, n, r, p)
+        x = a0.astype(orc.field_dtype(p))
+        P, Q, rr, _ = orc.pluq(x, p, 30)
+        generic = np.array_equal(P, np.arange(m)) and np.array_equal(Q, np.arange(n))
+        npan = (n + width - 1) // width
+        assert res[0][i][2] == [k for k in range(npan) if k % 2 == 0]  # block-cyclic ownership
+        assert res[1][i][2] == [k for k in range(npan) if k % 2 == 1]
+        rk0, rk1 = res[0][i][1], res[1][i][1]
+        assert rk0 == rk1, name  # every rank reaches the same decision
+        if not generic:
+            assert rk0 is None, name
+            continue
+        assert rk0 == rr, name
+        assert np.array_equal(res[0][i][3], x.astype(np.int64)), name
+
+
+# ---------------------------------------------------------------------------------------
+# GPU: the CUDA backend (C ABI) in a single process, several panels on one rank
+# ---------------------------------------------------------------------------------------
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,m,n,r,p,width", [
+    ("full", 300, 300, None, 65521, 64), ("wide", 200, 420, None, 65521, 96),
+    ("rank150", 320, 300, 150, 65521, 64), ("p23", 256, 256, None, 8388593, 64),
+    ("non_generic", 200, 260, 90, 65521, 64),
+])
+def test_cuda_panels_vs_oracle(cuda_ok, name, m, n, r, p, width):
+    import torch
+
+    import paper_1301_4438_b200 as pb
+    from paper_1301_4438_b200.distributed import pluq_distributed
+
+    a0 = _matrix(name, m, n, r, p)
+    x = a0.astype(orc.field_dtype(p))
+    c0 = orc.Counts()
+    P, Q, rr, _ = orc.pluq(x, p, 30, c0)
+    a = pb.DenseMatrix(pb.PrimeField(p), torch.from_numpy(a0).cuda().to(torch.int32))
+    c = pb.OpCounts()
+    f = pluq_distributed(a, m, n, p, 30, width=width, counts=c)
+    assert f.rank == rr and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data.cpu().numpy().astype(np.int64), x.astype(np.int64))
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == \
+           (c0.field_mul, c0.field_add, c0.field_inv, c0.modular_reductions)
+    assert f.packed is a
