@@ -396,8 +396,15 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
         torch.cuda.synchronize(dev)
         times.append(time.perf_counter() - t0)
     w3 = work(n3, n3, f.rank)
+    # whole-PLUQ roofline: a field MAC (2 field ops) is L^2 int8 MACs (2 L^2 int8
+    # ops) on the tensor pipe, so the field-op/s ceiling is int8_peak / L^2 (L = 2 for p = 65521,
+    # 3 for p = 8388593)
+    def tensor_frac(value_gfops, limbs_):
+        return value_gfops * 1e9 / (int8_peak * 1e12 / (limbs_ * limbs_))
+
     out["cfg3_8192"] = {"rank": f.rank, "s_best": min(times), "s_median": statistics.median(times),
-                        "value": w3 / min(times) / 1e9, "unit": UNIT, "stats": pb.last_stats()}
+                        "value": w3 / min(times) / 1e9, "unit": UNIT, "stats": pb.last_stats(),
+                        "frac_of_tensor_roofline": tensor_frac(w3 / min(times) / 1e9, 2)}
     # --- cfg1: 512^2 rank 384
     a1 = orc.gen_cfg1(seed=0)
     t1 = torch.from_numpy(a1).to(dev).to(torch.int32)
@@ -436,9 +443,10 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
         if rows is not None:
             checks["row_profile"] = pb.row_rank_profile(f) == tuple(int(v) for v in rows)
             checks["col_profile"] = pb.col_rank_profile(f) == tuple(int(v) for v in cols)
+        val = work(m_, n_, f.rank) / min(times) / 1e9
         out[name] = {"shape": [m_, n_], "p": p_, "rank": f.rank, "s_best": min(times),
-                     "value": work(m_, n_, f.rank) / min(times) / 1e9, "unit": UNIT, "checks": checks,
-                     "stats": pb.last_stats()}
+                     "value": val, "unit": UNIT, "checks": checks, "stats": pb.last_stats(),
+                     "frac_of_tensor_roofline": tensor_frac(val, 2 if p_ < 65536 else 3)}
         del a0, f, xa
         torch.cuda.empty_cache()
     return out
