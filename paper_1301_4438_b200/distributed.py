@@ -93,26 +93,55 @@ def _world():
     return 0, 1
 
 
-def scatter_panels(a_full, n: int, width: int, make_empty):
-    """Rank 0 holds a_full (m x n); returns {k: panel tensor} for the panels this rank owns."""
+class LocalSlab:
+    """The panels a rank owns, side by side in ONE m x (sum of widths) tensor, so that its
+    later panels are always a contiguous column range (one TRSM + one GEMM per step)."""
+
+    def __init__(self, tensor, owned, offsets, widths):
+        self.t, self.owned, self.off, self.w = tensor, owned, offsets, widths
+
+    def panel(self, k):
+        return self.t[:, self.off[k]:self.off[k] + self.w[k]]
+
+    def after(self, k):
+        """Columns of the owned panels j > k (a contiguous view, possibly empty)."""
+        later = [j for j in self.owned if j > k]
+        if not later:
+            return None
+        return self.t[:, self.off[later[0]]:]
+
+
+def _layout(n: int, width: int, rank: int, world: int):
+    owned, offsets, widths, col = [], {}, {}, 0
+    for k, (c0, c1) in enumerate(panel_bounds(n, width)):
+        if panel_owner(k, world) == rank:
+            owned.append(k)
+            offsets[k], widths[k] = col, c1 - c0
+            col += c1 - c0
+    return owned, offsets, widths, col
+
+
+def scatter_panels(a_full, m: int, n: int, width: int, make_empty) -> LocalSlab:
+    """Rank 0 holds a_full (m x n); every rank receives the panels it owns."""
     import torch.distributed as dist
 
     rank, world = _world()
-    local = {}
+    owned, offsets, widths, cols = _layout(n, width, rank, world)
+    slab = LocalSlab(make_empty(m, cols), owned, offsets, widths)
     for k, (c0, c1) in enumerate(panel_bounds(n, width)):
         owner = panel_owner(k, world)
         if owner == 0 and rank == 0:
-            local[k] = a_full[:, c0:c1].contiguous()
+            slab.panel(k).copy_(a_full[:, c0:c1])
         elif rank == 0:
             dist.send(a_full[:, c0:c1].contiguous(), dst=owner)
         elif rank == owner:
-            t = make_empty(c1 - c0)
-            dist.recv(t, src=0)
-            local[k] = t
-    return local
+            buf = make_empty(m, c1 - c0)
+            dist.recv(buf, src=0)
+            slab.panel(k).copy_(buf)
+    return slab
 
 
-def gather_panels(local, a_full, n: int, width: int):
+def gather_panels(slab: LocalSlab, a_full, m: int, n: int, width: int, make_empty):
     """Inverse of scatter_panels: rank 0 writes every panel back into a_full."""
     import torch.distributed as dist
 
@@ -120,16 +149,16 @@ def gather_panels(local, a_full, n: int, width: int):
     for k, (c0, c1) in enumerate(panel_bounds(n, width)):
         owner = panel_owner(k, world)
         if owner == 0 and rank == 0:
-            a_full[:, c0:c1] = local[k]
+            a_full[:, c0:c1] = slab.panel(k)
         elif rank == 0:
-            t = a_full.new_empty((a_full.shape[0], c1 - c0))
-            dist.recv(t, src=owner)
-            a_full[:, c0:c1] = t
+            buf = make_empty(m, c1 - c0)
+            dist.recv(buf, src=owner)
+            a_full[:, c0:c1] = buf
         elif rank == owner:
-            dist.send(local[k], dst=0)
+            dist.send(slab.panel(k).contiguous(), dst=0)
 
 
-def distributed_generic_lu(local, m: int, n: int, width: int, backend, make_flag):
+def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags):
     """Factor the distributed panels in place.  Returns the rank r when the matrix has a
     generic rank profile (then P = Q = I), or None when it does not (panels are then
     partially updated; the caller restarts from the original on one GPU)."""
@@ -137,45 +166,37 @@ def distributed_generic_lu(local, m: int, n: int, width: int, backend, make_flag
 
     rank, world = _world()
     mn = min(m, n)
-    bounds = panel_bounds(n, width)
-    for k, (c0, c1) in enumerate(bounds):
+    for k, (c0, c1) in enumerate(panel_bounds(n, width)):
         if c0 >= mn:
             break
         owner = panel_owner(k, world)
         wk = c1 - c0
-        flag = make_flag()
+        flag = flags()
+        pan = flags.new_panel(m - c0, wk)  # contiguous broadcast buffer
         if rank == owner:
-            sub = local[k][c0:, :]  # rows c0.. of a row-major m x wk panel: contiguous
-            rk, generic = backend.factor_panel(sub)
+            pview = slab.panel(k)[c0:, :]
+            rk, generic = backend.factor_panel(pview)
+            pan.copy_(pview)
             flag[0], flag[1] = rk, int(generic)
         if world > 1:
             dist.broadcast(flag, src=owner)
         rk, generic = int(flag[0]), bool(int(flag[1]))
         if not generic:
             return None
-        if rank == owner:
-            pan = local[k][c0:, :]
-        else:
-            pan = local[k][c0:, :] if k in local else None
-            if pan is None:
-                pan = make_flag.new_panel(m - c0, wk)
         if world > 1:
             dist.broadcast(pan, src=owner)
         g = c0 + rk
-        l11 = pan[:rk, :rk]
-        l21 = pan[rk:, :rk]
-        for j, t in local.items():
-            if j <= k or rk == 0:
-                continue
-            top = t[c0:g, :]
-            backend.trsm_llu(l11, top)                 # U12: pivot rows of panel j
+        rest = slab.after(k)
+        if rest is not None and rk > 0:
+            top = rest[c0:g, :]
+            backend.trsm_llu(pan[:rk, :rk], top)                  # U12: pivot rows of the later panels
             if g < m:
-                backend.gemm_sub(t[g:, :], l21, top)   # A22 -= L21 U12
+                backend.gemm_sub(rest[g:, :], pan[rk:, :rk], top)  # A22 -= L21 U12
         if rk < wk:
             # zero pivot at g: generic only if the whole Schur complement A[g:, g:] vanishes
             # (panel k's own part was checked by the exact panel factorization)
-            nz = make_flag()
-            nz[0] = int(any(not backend.is_zero(t[g:, :]) for j, t in local.items() if j > k and g < m))
+            nz = flags()
+            nz[0] = int(rest is not None and g < m and not backend.is_zero(rest[g:, :]))
             if world > 1:
                 dist.all_reduce(nz, op=dist.ReduceOp.MAX)
             return g if int(nz[0]) == 0 else None
@@ -195,6 +216,9 @@ class _Flags:
 
     def new_panel(self, rows, cols):
         return self.torch.empty((rows, cols), dtype=self.dtype, device=self.device)
+
+    def empty(self, rows, cols):
+        return self.new_panel(rows, cols)
 
 
 def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: int = 30,
@@ -221,10 +245,10 @@ def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: i
         full = x.clone()  # the original stays untouched until the final gather
     else:
         full = None
-    local = scatter_panels(full, n, width, lambda w: flags.new_panel(m, w))
-    r = distributed_generic_lu(local, m, n, width, backend, flags)
+    slab = scatter_panels(full, m, n, width, flags.empty)
+    r = distributed_generic_lu(slab, m, n, width, backend, flags)
     if r is not None:
-        gather_panels(local, full if rank == 0 else None, n, width)
+        gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
     if rank != 0:
         return r
     if r is None:  # not generic: the exact recursion on one GPU, from the untouched original

@@ -85,11 +85,11 @@ def _worker(rank, world, port, q):
             a0 = _matrix(name, m, n, r, p)
             full = torch.from_numpy(a0.astype(np.int64)) if rank == 0 else None
             flags = D._Flags(torch.device("cpu"), torch.int64)
-            local = D.scatter_panels(full, n, width, lambda w: flags.new_panel(m, w))
-            owned = sorted(local)
-            rk = D.distributed_generic_lu(local, m, n, width, NumpyPanelBackend(p, 30), flags)
+            slab = D.scatter_panels(full, m, n, width, flags.empty)
+            owned = list(slab.owned)
+            rk = D.distributed_generic_lu(slab, m, n, width, NumpyPanelBackend(p, 30), flags)
             if rk is not None:
-                D.gather_panels(local, full if rank == 0 else None, n, width)
+                D.gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
             out.append((name, rk, owned, full.numpy().copy() if rank == 0 and rk is not None else None))
         q.put((rank, out))
     finally:
