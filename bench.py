@@ -36,6 +36,9 @@ METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
 # dram__bytes_read.sum + dram__bytes_write.sum of the generic kernel per launch from the committed
 # ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
 TRAFFIC = 78_460_928  # 67.27 MB read + 11.19 MB write (profiles/r1/prof_fixed_raw.txt)
+# the generic kernel is issue/latency bound, not HBM bound: ncu --set full of the same kernel
+# (profiles/r1/prof_batch_v11_raw.txt): issue slots busy 60.9 %, IPC 2.43 of 4 per SM
+ISSUE_BUSY, IPC = 0.609, 2.43
 UNIT = "Gfield-op/s"
 
 
@@ -315,6 +318,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "crout_fixed_kernel<64,64,128>", "achieved": alg_bytes / t_gen / 1e9,
                      "peak": hbm, "unit": "GB/s", "frac": alg_bytes / t_gen / 1e9 / hbm, "traffic": TRAFFIC,
                      "traffic_unit": "bytes per launch (ncu --set full, dram read+write; output writes partly still in L2)",
+                     "issue_slots_busy": ISSUE_BUSY, "ipc_of_4": IPC,
                      "alg_bytes": alg_bytes,
                      "peak_kind": peak_kind, "kernel_ms": t_gen * 1e3,
                      "fallback_kernel_ms": kst["t_fallback_ns"] / 1e6,
