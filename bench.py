@@ -224,9 +224,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_1301_4438_b200 as pb
-    from oracle import pluq_oracle as orc  # input generator only (seeded synthetic data)
 
-    host = orc.gen_cfg2(seed=rank, batch=BATCH)
+    # seeded synthetic cfg2 batch (PCG64, uniform in [0, p)); the oracle is not used here
+    host = np.random.default_rng(rank).integers(0, P, (BATCH, M, N), dtype=np.int64)
     pristine = torch.from_numpy(host).to(dev).to(torch.int32)
     work_buf = torch.empty_like(pristine)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -331,13 +331,13 @@ def main():
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline_leg()
     if not args.no_secondary and world == 1:
-        line["secondary"] = secondary(pb, orc, dev, hbm, bf16, peak_kind)
+        line["secondary"] = secondary(pb, dev, hbm, bf16, peak_kind)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def secondary(pb, orc, dev, hbm, bf16, peak_kind):
+def secondary(pb, dev, hbm, bf16, peak_kind):
     """The modular GEMM's tensor roofline, cfg3 (8192^2), cfg1, and cfg4/cfg5 at full size."""
     import torch
     from paper_1301_4438_b200 import _native
@@ -388,7 +388,7 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
     del A, B, C
     # --- cfg3: 8192^2 full-rank generic, device resident
     n3 = 8192
-    a3 = orc.gen_cfg3(seed=0, n=n3)
+    a3 = np.random.default_rng(0).integers(0, P, (n3, n3), dtype=np.int64)
     t3 = torch.from_numpy(a3).to(dev).to(torch.int32)
     x = torch.empty_like(t3)
     times = []
@@ -410,8 +410,9 @@ def secondary(pb, orc, dev, hbm, bf16, peak_kind):
                         "value": w3 / min(times) / 1e9, "unit": UNIT, "stats": pb.last_stats(),
                         "frac_of_tensor_roofline": tensor_frac(w3 / min(times) / 1e9, 2)}
     # --- cfg1: 512^2 rank 384
-    a1 = orc.gen_cfg1(seed=0)
-    t1 = torch.from_numpy(a1).to(dev).to(torch.int32)
+    from paper_1301_4438_b200 import gen as dgen
+
+    t1 = dgen.gen_xy_rank_device(512, 512, 384, P, seed=0).to(dev)
     x1 = torch.empty_like(t1)
     times = []
     for it in range(5):
