@@ -100,13 +100,14 @@ struct pluq_ctx {
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
-  int64_t diag_lazy = 1;           // speculative LU: lazy-reduction diagonal-block kernel
+  int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 16;        // pipeline depth of the host-buffer batched path
   int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
+  int64_t rpm_lazy = 1;            // rank-profile kernel: lazy-reduction register phases
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
@@ -444,20 +445,23 @@ static size_t block_smem_bytes(int64_t m, int64_t n, int64_t thr) {
 static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigned threads, const int* fl,
                          const int* fc, cudaStream_t st) {
   if (c->exact_kernel) {
-    const size_t smem = rpm_smem_bytes(a.m, a.n);
     const unsigned nt = (unsigned)c->rpm_threads;
-    switch (rpm_shape(a.m, a.n, (int)nt)) {
+    const int shape = rpm_shape(a.m, a.n, (int)nt);
+    SmallArgs al = a;
+    al.lazy = (int)c->rpm_lazy;
+    const size_t smem = rpm_smem_bytes(a.m, a.n, shape == 1 && al.lazy && a.invtab != nullptr);
+    switch (shape) {
       case 1:
         CU(cudaFuncSetAttribute(rpm_pluq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rpm_pluq_kernel<1><<<grid, nt, smem, st>>>(a, fl, fc);
+        rpm_pluq_kernel<1><<<grid, nt, smem, st>>>(al, fl, fc);
         break;
       case 2:
         CU(cudaFuncSetAttribute(rpm_pluq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rpm_pluq_kernel<2><<<grid, nt, smem, st>>>(a, fl, fc);
+        rpm_pluq_kernel<2><<<grid, nt, smem, st>>>(al, fl, fc);
         break;
       default:
         CU(cudaFuncSetAttribute(rpm_pluq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rpm_pluq_kernel<0><<<grid, nt, smem, st>>>(a, fl, fc);
+        rpm_pluq_kernel<0><<<grid, nt, smem, st>>>(al, fl, fc);
     }
   } else {
     const size_t smem = small_smem_bytes(a.m, a.n, a.threshold);
@@ -572,8 +576,15 @@ struct Driver {
     Ops sops = ops;
     sops.stop = c->d_stop;
     const uint16_t* itab = c->invtab(mp.p);
-    const bool lazy = c->diag_lazy && BS <= 128;
-    const size_t dsm = lazy ? diag_lazy_smem(itab != nullptr) : diag_fast_smem(BS, itab != nullptr);
+    const bool reg = c->diag_lazy == 3 && BS <= 128 && (itab != nullptr || mp.kchunk >= 130);
+    const bool lazy = !reg && c->diag_lazy && BS <= 128;
+    const size_t dsm = reg    ? diag_reg_smem(itab != nullptr)
+                       : lazy ? diag_lazy_smem(itab != nullptr)
+                              : diag_fast_smem(BS, itab != nullptr);
+    if (reg) {
+      CU(cudaFuncSetAttribute(diag_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      CU(cudaFuncSetAttribute(diag_reg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    }
     const int lazy_rw = c->diag_lazy == 2 ? 4 : 8;  // rows per warp of diag_lazy_kernel
     if (lazy) {
       CU(cudaFuncSetAttribute(diag_lazy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -602,7 +613,11 @@ struct Driver {
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
-        if (lazy && lazy_rw == 8)
+        if (reg && itab)
+          diag_reg_kernel<true><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+        else if (reg)
+          diag_reg_kernel<false><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+        else if (lazy && lazy_rw == 8)
           diag_lazy_kernel<8><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
         else if (lazy)
           diag_lazy_kernel<4><<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
@@ -997,6 +1012,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "la_reserve") c->la_reserve = value;
   else if (k == "exact_kernel") c->exact_kernel = value;
   else if (k == "rpm_threads") c->rpm_threads = value;
+  else if (k == "rpm_lazy") c->rpm_lazy = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;

@@ -2,6 +2,7 @@
 #pragma once
 #include "pluq_small.cuh"
 #include "pluq_rpm.cuh"
+#include "pluq_diag.cuh"
 
 namespace pluq {
 
@@ -32,6 +33,7 @@ struct SmallArgs {
   int* fail_list;               // compacted indices of blocks needing the exact recursion
   int* fail_count;
   int fail_base;                // index offset of this launch's first block in the list
+  int lazy = 1;                 // rank-profile kernel: lazy-reduction register phases (shape 1)
 };
 
 __device__ void small_pluq_block(const SmallArgs& args, int blk);
@@ -136,7 +138,17 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   __syncthreads();
   RPM_MARK(1);
   int r;
-  if constexpr (shape == 1) r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  // shape 1: lazy-reduction phases (table staged in shared memory behind the block's words)
+  const bool lazy = shape == 1 && args.lazy && (args.invtab != nullptr || args.mp.kchunk >= 66);
+  uint16_t* stab = reinterpret_cast<uint16_t*>(smem_dyn + ((rpm_smem_words(m, n) + 3) & ~3ll));
+  if (lazy && args.invtab) rl_stage_table(stab, args.invtab, args.mp.p);
+  if constexpr (shape == 1) {
+    if (lazy && args.invtab) r = rpm_rows_lazy<true>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                                     reinterpret_cast<int*>(diag));
+    else if (lazy) r = rpm_rows_lazy<false>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                            reinterpret_cast<int*>(diag));
+    else r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  }
   else if constexpr (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
   RPM_MARK(2);
@@ -153,7 +165,9 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   RPM_MARK(4);
   const bool inv = args.invtab != nullptr;
   if constexpr (shape == 1) {
-    if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+    if (lazy && inv) lu_lazy<true>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (lazy) lu_lazy<false>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else if constexpr (shape == 2) {
     if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
@@ -209,7 +223,9 @@ inline int rpm_shape(int m, int n, int threads) {
   return (n <= 64 && m <= 4 * nw) ? 1 : (n <= 128 && m <= 8 * nw) ? 2 : 0;
 }
 
-inline size_t rpm_smem_bytes(int64_t m, int64_t n) { return (size_t)rpm_smem_words(m, n) * 4; }
+inline size_t rpm_smem_bytes(int64_t m, int64_t n, bool table = false) {
+  return (size_t)((rpm_smem_words(m, n) + 3) & ~3ll) * 4 + (table ? 65536 * 2 : 0);
+}
 
 // Dynamic shared memory of small_pluq_kernel: block (odd pitch) + P/Q + recursion stack.
 // Lean generic-profile kernel (no recursion compiled in, so few registers and many

@@ -530,6 +530,199 @@ __device__ void lu_reg(uint32_t* ga, int64_t lda, int m, int n, int r, const int
   }
 }
 
+// ---- lazy-reduction variants of a) and c) for blocks up to 64 x 64 (shape 1, 512
+// threads).  Warp w holds rows k = w + 16 t (t < 4), lane holds columns c = lane + 32 q
+// (q < 2); every element is a 64-bit accumulator taking ONE IMAD.WIDE per elimination
+// step (acc += c_k * w_c) and reduced only when read: the pivot row by its owner warp
+// (two values per lane), the pivot column by the lanes 0..3 of each warp after a shuffle
+// gather.  A step costs one CTA barrier and ~10 integer instructions per element instead
+// of two modular products.  kSmall: p < 2^16, accumulators < 2^38 (two 32-bit Barrett
+// steps), inverse table staged in shared memory; else 64 (p-1)^2 + p < 2^64 and Euclid.
+template <bool kSmall>
+__device__ __forceinline__ uint32_t rl_red(unsigned long long x, const ModP& mp, uint32_t e32) {
+  if (kSmall) return reduce32(reduce32((uint32_t)x, mp) + (uint32_t)(x >> 32) * e32, mp);
+  return reduce64(x, mp);
+}
+template <bool kSmall>
+__device__ __forceinline__ uint32_t rl_mul(uint32_t a, uint32_t b, const ModP& mp) {
+  if (kSmall) return reduce32(a * b, mp);
+  return reduce64((unsigned long long)a * b, mp);
+}
+template <bool kSmall>
+__device__ __forceinline__ uint32_t rl_inv(uint32_t d, const ModP& mp, const uint16_t* stab) {
+  if (d == 0u) return 0u;
+  return kSmall ? (uint32_t)stab[d] : invmod(d, mp);
+}
+__device__ __forceinline__ unsigned long long rl_sel(const unsigned long long (&a)[4][2], int t, int q) {
+  unsigned long long x0 = a[0][0], x1 = a[0][1];
+#pragma unroll
+  for (int u = 1; u < 4; ++u) { x0 = t == u ? a[u][0] : x0; x1 = t == u ? a[u][1] : x1; }
+  return q ? x1 : x0;
+}
+
+// Column `col` of this warp's four rows, reduced (rows k <= lim give 0).
+template <bool kSmall>
+__device__ __forceinline__ void rl_column(const unsigned long long (&a)[4][2], int col, int lim, int m,
+                                          const ModP& mp, uint32_t e32, uint32_t (&cv)[4]) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cq = col >> 5, cl = col & 31;
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const unsigned long long x = cq ? a[t][1] : a[t][0];
+    const unsigned long long y = __shfl_sync(FULL, x, cl);
+    mine = lane == t ? y : mine;
+  }
+  const uint32_t red = rl_red<kSmall>(mine, mp, e32);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int k = w + 16 * t;
+    const uint32_t v = __shfl_sync(FULL, red, t);
+    cv[t] = (k > lim && k < m) ? v : 0u;
+  }
+}
+
+// Stage the inverse table (p < 2^16) into shared memory with cp.async.
+__device__ __forceinline__ void rl_stage_table(uint16_t* stab, const uint16_t* tab, uint32_t p) {
+  const int words16 = (int)((p + 7) / 8);  // 16-byte chunks covering entries [0, p)
+  for (int q = threadIdx.x; q < words16; q += blockDim.x) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(stab + 8 * q);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(tab + 8 * q));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+__device__ __forceinline__ void rl_wait_table() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// a) R_A by row-order elimination (same outputs as rpm_rows_reg<2, 4>).
+template <bool kSmall>
+__device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, const ModP mp, int* rp, int* cp,
+                             const uint16_t* stab, uint32_t* wbuf /* [2][64] */, int* jbuf /* [2] */) {
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
+  unsigned long long a[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int k = w + 16 * t;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      a[t][q] = (k < m && c < n) ? ga[(int64_t)k * lda + c] : 0u;
+    }
+  }
+  for (int t = tid; t < m; t += blockDim.x) rp[t] = -1;
+  for (int t = tid; t < n; t += blockDim.x) cp[t] = -1;
+  if (kSmall) rl_wait_table();
+  __syncthreads();  // table staged, rp/cp initialised
+  // the owner warp of row i finds its first nonzero column and publishes -row / pivot
+  auto publish = [&](int i) {
+    if (w != (i & 15)) return;
+    const int ti = i >> 4;
+    const uint32_t u0 = rl_red<kSmall>(rl_sel(a, ti, 0), mp, e32);
+    const uint32_t u1 = rl_red<kSmall>(rl_sel(a, ti, 1), mp, e32);
+    const unsigned b0 = __ballot_sync(FULL, u0 != 0u && lane < n);
+    const unsigned b1 = __ballot_sync(FULL, u1 != 0u && lane + 32 < n);
+    const int j = b0 ? __ffs(b0) - 1 : b1 ? 32 + __ffs(b1) - 1 : -1;
+    uint32_t* wb = wbuf + (i & 1) * 64;
+    if (j >= 0) {
+      const uint32_t d = __shfl_sync(FULL, j < 32 ? u0 : u1, j & 31);
+      const uint32_t iv = rl_inv<kSmall>(d, mp, stab);
+      wb[lane] = u0 ? rl_mul<kSmall>(mp.p - u0, iv, mp) : 0u;
+      wb[lane + 32] = u1 ? rl_mul<kSmall>(mp.p - u1, iv, mp) : 0u;
+      if (lane == 0) { rp[i] = j; cp[j] = i; }
+    }
+    if (lane == 0) jbuf[i & 1] = j;
+  };
+  if (m > 0) publish(0);
+  int r = 0;
+  for (int i = 0; i < m && r < n; ++i) {
+    __syncthreads();  // row i published
+    const int j = jbuf[i & 1];
+    if (j >= 0) {
+      ++r;
+      uint32_t cv[4];
+      rl_column<kSmall>(a, j, i, m, mp, e32, cv);
+      const uint32_t* wb = wbuf + (i & 1) * 64;
+      const uint32_t w0 = wb[lane], w1 = wb[lane + 32];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[t][0] += (unsigned long long)cv[t] * w0;
+        a[t][1] += (unsigned long long)cv[t] * w1;
+      }
+    }
+    if (i + 1 < m && r < n) publish(i + 1);
+  }
+  __syncthreads();
+  return r;
+}
+
+// c) unpivoted LU of A'[k][c] = A[pinv[k]][Q[c]] (r nonzero leading pivots), packed
+// factors written back to ga.  inv_s: r words of shared scratch.
+template <bool kSmall>
+__device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const int* pinv, const int* Q,
+                        const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][64] */, uint32_t* inv_s) {
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
+  unsigned long long a[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int k = w + 16 * t;
+    const uint32_t* src = k < m ? ga + (int64_t)pinv[k] * lda : ga;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      a[t][q] = (k < m && c < n) ? src[Q[c]] : 0u;
+    }
+  }
+  __syncthreads();  // every original row is in registers before any packed row is written
+  auto publish = [&](int s) {
+    if (w != (s & 15)) return;
+    const int ts = s >> 4;
+    const uint32_t u0 = rl_red<kSmall>(rl_sel(a, ts, 0), mp, e32);
+    const uint32_t u1 = rl_red<kSmall>(rl_sel(a, ts, 1), mp, e32);
+    const uint32_t d = __shfl_sync(FULL, s < 32 ? u0 : u1, s & 31);
+    if (d == 0u) __trap();  // impossible for A' (leading minors 1..r nonzero)
+    const uint32_t iv = rl_inv<kSmall>(d, mp, stab);
+    uint32_t* wb = wbuf + (s & 1) * 64;
+    wb[lane] = (lane > s && u0) ? rl_mul<kSmall>(mp.p - u0, iv, mp) : 0u;
+    wb[lane + 32] = (lane + 32 > s && u1) ? rl_mul<kSmall>(mp.p - u1, iv, mp) : 0u;
+    if (lane == 0) inv_s[s] = iv;
+  };
+  if (r > 0) publish(0);
+  for (int s = 0; s < r; ++s) {
+    __syncthreads();  // pivot row s published
+    uint32_t cv[4];
+    rl_column<kSmall>(a, s, s, m, mp, e32, cv);
+    const uint32_t* wb = wbuf + (s & 1) * 64;
+    const uint32_t w0 = wb[lane], w1 = wb[lane + 32];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      a[t][0] += (unsigned long long)cv[t] * w0;
+      a[t][1] += (unsigned long long)cv[t] * w1;
+    }
+    if (s + 1 < r) publish(s + 1);
+  }
+  __syncthreads();  // inverses of every pivot published
+  // U entries are frozen after their row's pivot step, L entries (c < k) hold the Schur
+  // value of their column's step (w_c = 0 afterwards), the trailing block is zero.
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int k = w + 16 * t;
+    if (k >= m) continue;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      if (c >= n) continue;
+      uint32_t v = rl_red<kSmall>(a[t][q], mp, e32);
+      if (c < k && c < r) v = rl_mul<kSmall>(v, inv_s[c], mp);
+      else if (k >= r && c >= r) v = 0u;
+      ga[(int64_t)k * lda + c] = v;
+    }
+  }
+}
+
 // Shared-memory words of rpm_pluq_block for an m x n block.
 __host__ __device__ inline int64_t rpm_smem_words(int64_t m, int64_t n) {
   const int64_t mn = m < n ? m : n;
