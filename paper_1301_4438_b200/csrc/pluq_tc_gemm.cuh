@@ -102,9 +102,24 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   return d;
 }
 
-// kind::i8 instruction descriptor: s32 accumulate, u8 x u8, both K-major, M=128.
-__host__ __device__ constexpr uint32_t idesc_i8(int n) {
-  return (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// MN-major, SWIZZLE_128B descriptor for a tile whose MN extent is one 128-byte swizzle
+// atom (rows = K, 128 bytes of N each): 8-row K groups 1024 B apart (SBO); LBO (the
+// stride between MN atoms) is unused with a single atom.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((128 * 128) >> 4) << 16;  // leading byte offset (next MN atom; unused)
+  d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset: next group of 8 K rows
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::i8 instruction descriptor: s32 accumulate, u8 x u8, A K-major, B K-major
+// (mnb = false) or MN-major (mnb = true, bit 16), M=128.
+__host__ __device__ constexpr uint32_t idesc_i8(int n, bool mnb = false) {
+  return (2u << 4) | (0u << 7) | (0u << 10) | ((mnb ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
 }
 
 // Persistent tiling: each CTA (one per SM) walks output tiles; TMEM holds TWO
@@ -142,12 +157,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warps 4..11 epilogue
 
-template <int L, int V>
+// MNB: B limb planes are row-major k x n (MN-major operand, written by the same
+// vectorised split as A, no transpose pass); requires BN == 128 (one swizzle atom).
+template <int L, int V, bool MNB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
                       int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg) {
+  const int kplane = kblocks * TC_BK;  // rows of one MN-major B limb plane
   if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
+  static_assert(!MNB || BN == 128, "MN-major B needs one 128-byte swizzle atom per tile");
   constexpr int NPOS = 2 * L - 1;
   constexpr int ACC_COLS = NPOS * BN;               // one accumulator set
   constexpr uint32_t TCOLS = 512;
@@ -195,13 +214,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int l = 0; l < L; ++l) {
           tma_load_2d(sA + ((size_t)s * L + l) * A_TILE, &ta, &full[s], kb * TC_BK, l * m_pad + m0);
-          tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], kb * TC_BK, l * n_pad + n0);
+          if (MNB)
+            tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], n0, l * kplane + kb * TC_BK);
+          else
+            tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], kb * TC_BK, l * n_pad + n0);
         }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
-    constexpr uint32_t idesc = idesc_i8(BN);
+    constexpr uint32_t idesc = idesc_i8(BN, MNB);
     uint32_t g = 0, local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const uint32_t buf = local % NBUF, use = local / NBUF;
@@ -224,7 +246,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const int first_i = pos < L ? 0 : pos - (L - 1);
               const uint32_t acc = (kb > 0 || kk > 0 || i != first_i) ? 1u : 0u;
               const uint64_t ad = desc_k_sw128(a0 + i * A_TILE + kk * 32);
-              const uint64_t bd = desc_k_sw128(b0 + j * B_TILE + kk * 32);
+              const uint64_t bd = MNB ? desc_mn_sw128(b0 + j * B_TILE + kk * 32 * 128)
+                                      : desc_k_sw128(b0 + j * B_TILE + kk * 32);
               mma_i8(dacc + (uint32_t)(pos * BN), ad, bd, idesc, acc);
             }
           }
@@ -478,12 +501,13 @@ struct TcGemm {
   PFN_encodeTiled encode = nullptr;
   std::string last_error;
   int64_t k_pass_override = 0;  // tests: force multi-pass K splitting
-  bool attrs_set[2][5] = {};
+  bool attrs_set[2][2][5] = {};
   int variant = 1;              // TcCfg variant (option tc_cfg)
   int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
   int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring
   int vec_limbs = 1;            // vectorised limb-split kernels (option tc_vec)
   int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
+  int mn_b = 1;                 // option tc_mnb: MN-major B operand when the tile allows it (no transpose)
   float mma_ms = 0.f;           // summed MMA-kernel time of the last call when timed
 
   static int limbs(uint32_t p) {
@@ -523,10 +547,11 @@ struct TcGemm {
     return true;
   }
 
-  bool make_map(CUtensorMap* map, void* base, int64_t inner_bytes, int64_t rows, int box_rows) {
+  bool make_map(CUtensorMap* map, void* base, int64_t inner_bytes, int64_t rows, int box_rows,
+                int box_inner = TC_BK) {
     cuuint64_t dims[2] = {(cuuint64_t)inner_bytes, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)inner_bytes};
-    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -538,7 +563,7 @@ struct TcGemm {
     return true;
   }
 
-  template <int L, int V>
+  template <int L, int V, bool MNB>
   int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop,
              int max_ctas) {
     constexpr int BN = TcCfg<L, V>::BN;
@@ -557,13 +582,13 @@ struct TcGemm {
       return kNoMemory;
     }
     constexpr size_t smem = tc_smem_bytes<L, V>();
-    if (!attrs_set[V][L]) {
-      if (cudaFuncSetAttribute(tc_modgemm_kernel<L, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess) {
+    if (!attrs_set[MNB][V][L]) {
+      if (cudaFuncSetAttribute(tc_modgemm_kernel<L, V, MNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess) {
         last_error = "cannot set shared memory size";
         return kCuda;
       }
-      attrs_set[V][L] = true;
+      attrs_set[MNB][V][L] = true;
     }
     for (int64_t k0 = 0; k0 < k; k0 += kp) {
       const int kc = (int)std::min<int64_t>(kp, k - k0);
@@ -579,12 +604,18 @@ struct TcGemm {
         int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 32);
         limb_rows_kernel<<<grid, 256, 0, st>>>(as, da, L, m_pad, k_pad, stop);
       }
-      {
+      if (MNB) {  // B planes row-major (k_pad x n_pad): the same split as A, no transpose
+        const int64_t work = (int64_t)k_pad * (n_pad / 16);
+        const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
+        limb_rows16_kernel<<<grid, 256, 0, st>>>(bs, db, L, k_pad, n_pad, stop);
+      } else {
         dim3 cgrid(n_pad / 32, k_pad / 32);
         limb_cols_kernel<<<cgrid, 256, 0, st>>>(bs, db, L, n_pad, k_pad, stop);
       }
       CUtensorMap ta, tb;
-      if (!make_map(&ta, da, k_pad, (int64_t)L * m_pad, TC_BM) || !make_map(&tb, db, k_pad, (int64_t)L * n_pad, BN)) {
+      const bool okb = MNB ? make_map(&tb, db, n_pad, (int64_t)L * k_pad, TC_BK, BN)
+                           : make_map(&tb, db, k_pad, (int64_t)L * n_pad, BN);
+      if (!make_map(&ta, da, k_pad, (int64_t)L * m_pad, TC_BM) || !okb) {
         cudaFreeAsync(da, st);
         cudaFreeAsync(db, st);
         return kCuda;
@@ -598,8 +629,8 @@ struct TcGemm {
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      tc_modgemm_kernel<L, V><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop,
-                                                              dbg);
+      tc_modgemm_kernel<L, V, MNB><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp,
+                                                                   stop, dbg);
       if (time_mma) {
         float ms = 0.f;
         cudaEventRecord(e1, st);
@@ -631,17 +662,19 @@ struct TcGemm {
     const int L = limbs(mp.p);
     if (variant == 0) {
       switch (L) {
-        case 1: return launch<1, 0>(c, a, b, mp, st, stop, max_ctas);
-        case 2: return launch<2, 0>(c, a, b, mp, st, stop, max_ctas);
-        case 3: return launch<3, 0>(c, a, b, mp, st, stop, max_ctas);
-        case 4: return launch<4, 0>(c, a, b, mp, st, stop, max_ctas);
+        case 1: return launch<1, 0, false>(c, a, b, mp, st, stop, max_ctas);
+        case 2: return launch<2, 0, false>(c, a, b, mp, st, stop, max_ctas);
+        case 3: return launch<3, 0, false>(c, a, b, mp, st, stop, max_ctas);
+        case 4: return launch<4, 0, false>(c, a, b, mp, st, stop, max_ctas);
       }
     } else {
       switch (L) {
-        case 1: return launch<1, 1>(c, a, b, mp, st, stop, max_ctas);
-        case 2: return launch<2, 1>(c, a, b, mp, st, stop, max_ctas);
-        case 3: return launch<3, 1>(c, a, b, mp, st, stop, max_ctas);
-        case 4: return launch<4, 1>(c, a, b, mp, st, stop, max_ctas);
+        case 1: return launch<1, 1, false>(c, a, b, mp, st, stop, max_ctas);
+        case 2:
+          return mn_b ? launch<2, 1, true>(c, a, b, mp, st, stop, max_ctas)
+                      : launch<2, 1, false>(c, a, b, mp, st, stop, max_ctas);
+        case 3: return launch<3, 1, false>(c, a, b, mp, st, stop, max_ctas);
+        case 4: return launch<4, 1, false>(c, a, b, mp, st, stop, max_ctas);
       }
     }
     return kUnsupported;
