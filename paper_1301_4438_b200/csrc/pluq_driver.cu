@@ -1309,13 +1309,16 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cntk + 255) / 256));
       from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw + b0 * mn, dA + b0 * mn, cntk);
       c->check_launch();
+      // chunk k's results are one contiguous record [P (nb x m) | Q (nb x n) | rank (nb)]
+      // so that a single D2H copy returns them
+      int32_t* rec = dp + b0 * (m + n + 1);
       a.a = dA + b0 * mn;
-      a.p_out = dp + b0 * m; a.q_out = dp + batch * m + b0 * n; a.r_out = dp + batch * (m + n) + b0;
+      a.p_out = rec; a.q_out = rec + nb * m; a.r_out = rec + nb * (m + n);
       a.cnt_out = cnt + 4 * b0;
       cudaStream_t tail = c->stream;
       if (flags) {
         a.generic_flag = flags + b0;
-        a.fail_base = (int)b0;
+        a.fail_base = 0;  // chunk-local indices
         a.fail_count = flags + batch + k;
         a.fail_list = flags + batch + nchunks + b0;
         if (!(c->fixed_kernels && launch_crout_fixed(a, nb, c->stream)))
@@ -1324,10 +1327,8 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
         CU(cudaEventRecord(ev_gen[k], c->stream));
         cudaStream_t sfb = sfbs[k % kFb];
         CU(cudaStreamWaitEvent(sfb, ev_gen[k], 0));
-        // failures are listed with global indices: run them with the chunk base at 0
         SmallArgs g = a;
-        g.a = dA; g.p_out = dp; g.q_out = dp + batch * m; g.r_out = dp + batch * (m + n);
-        g.cnt_out = cnt; g.generic_flag = nullptr;
+        g.generic_flag = nullptr;
         launch_exact(c, g, (unsigned)std::min<int64_t>(nb, 148 * 2), (unsigned)c->batch_threads, a.fail_list,
                      a.fail_count, sfb);
         tail = sfb;
@@ -1340,20 +1341,17 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       CU(cudaStreamWaitEvent(sout, ev_done[k], 0));
       CU(cudaMemcpyAsync(hA + b0 * mn, raw + b0 * mn, (size_t)nb * mn * 8, cudaMemcpyDeviceToHost, sout));
       CU(cudaEventRecord(ev_out[k], sout));
-      CU(cudaMemcpyAsync(host + b0 * m, dp + b0 * m, (size_t)nb * m * 4, cudaMemcpyDeviceToHost, sout));
-      CU(cudaMemcpyAsync(host + batch * m + b0 * n, dp + batch * m + b0 * n, (size_t)nb * n * 4,
-                         cudaMemcpyDeviceToHost, sout));
-      CU(cudaMemcpyAsync(host + batch * (m + n) + b0, dp + batch * (m + n) + b0, (size_t)nb * 4,
-                         cudaMemcpyDeviceToHost, sout));
+      CU(cudaMemcpyAsync(host + b0 * (m + n + 1), rec, (size_t)nb * (m + n + 1) * 4, cudaMemcpyDeviceToHost, sout));
       CU(cudaEventRecord(ev_res[k], sout));
     }
     CU(cudaEventRecord(ev_end, sout));
     for (int64_t k = 0; k <= last; ++k) {
       CU(cudaEventSynchronize(ev_res[k]));
       const int64_t b0 = cb0[k], nb = cb0[k + 1] - cb0[k];
-      for (int64_t i = b0 * m; i < (b0 + nb) * m; ++i) psig[i] = host[i];
-      for (int64_t i = b0 * n; i < (b0 + nb) * n; ++i) qsig[i] = host[batch * m + i];
-      for (int64_t i = b0; i < b0 + nb; ++i) ranks[i] = host[batch * (m + n) + i];
+      const int32_t* hr = host + b0 * (m + n + 1);
+      for (int64_t i = 0; i < nb * m; ++i) psig[b0 * m + i] = hr[i];
+      for (int64_t i = 0; i < nb * n; ++i) qsig[b0 * n + i] = hr[nb * m + i];
+      for (int64_t i = 0; i < nb; ++i) ranks[b0 + i] = hr[nb * (m + n) + i];
     }
     CU(cudaStreamSynchronize(sout));
     CU(cudaStreamSynchronize(c->stream));
@@ -1374,8 +1372,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     if (flags) c->dfree(flags);
     c->dfree(dp);
     c->dfree(dA);
-    c->dfree(raw);
-    c->sync();
+    c->dfree(raw);  // stream-ordered: every stream that used these buffers has been synchronised
     if (tr)
       fprintf(stderr, "pipeline: frees %.3f ms\n",
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());
