@@ -108,6 +108,7 @@ struct pluq_ctx {
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
   int64_t rpm_lazy = 1;            // rank-profile kernel: lazy-reduction register phases
+  int64_t par_trsm = 1;            // speculative LU: the panel's L21 and U12 solves on two streams
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
@@ -608,6 +609,10 @@ struct Driver {
       CU(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     }
     bool side_pending = false;
+    cudaStream_t side2 = c->side_streams()[4];
+    cudaEvent_t ev_d = nullptr, ev_t = nullptr;
+    CU(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
       // inner right-looking LU of the panel columns [ps, pe)
@@ -626,8 +631,20 @@ struct Driver {
                                                               c->d_stop + 1, k0);
         c->check_launch();
         const View b11 = x.sub(k0, k0, bs, bs);
-        sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                       // L21
-        sops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                      // U12 (panel)
+        if (c->par_trsm && pe - k0 - bs > 0) {
+          // L21 and U12 are independent: U12 runs on a side stream next to L21
+          CU(cudaEventRecord(ev_d, c->stream));
+          CU(cudaStreamWaitEvent(side2, ev_d, 0));
+          Ops tops = sops;
+          tops.st = side2;
+          tops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                    // U12 (panel)
+          CU(cudaEventRecord(ev_t, side2));
+          sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                     // L21
+          CU(cudaStreamWaitEvent(c->stream, ev_t, 0));
+        } else {
+          sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                     // L21
+          sops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                    // U12 (panel)
+        }
         sops.gemm(x.sub(k0 + bs, k0 + bs, m - k0 - bs, pe - k0 - bs), x.sub(k0 + bs, k0, m - k0 - bs, bs),
                   x.sub(k0, k0 + bs, bs, pe - k0 - bs));
         if (blk == 0 || (blk + 1) % c->spec_check == 0) {  // abort early on non-generic input
@@ -665,6 +682,8 @@ struct Driver {
       }
     }
     if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+    cudaEventDestroy(ev_d);
+    cudaEventDestroy(ev_t);
     if (la) {
       c->dfree(snap);
       cudaEventDestroy(ev_main);
@@ -1014,6 +1033,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "exact_kernel") c->exact_kernel = value;
   else if (k == "rpm_threads") c->rpm_threads = value;
   else if (k == "rpm_lazy") c->rpm_lazy = value;
+  else if (k == "par_trsm") c->par_trsm = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;
