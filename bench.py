@@ -35,10 +35,10 @@ THRESHOLD = 30
 METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
 # dram__bytes_read.sum + dram__bytes_write.sum of the generic kernel per launch from the committed
 # ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
-TRAFFIC = 78_460_928  # 67.27 MB read + 11.19 MB write (profiles/r1/prof_fixed_raw.txt)
+TRAFFIC = 78_012_160  # 67.27 MB read + 10.74 MB write (profiles/r1/prof_crout_v18_raw.txt)
 # the generic kernel is issue/latency bound, not HBM bound: ncu --set full of the same kernel
-# (profiles/r1/prof_batch_v11_raw.txt): issue slots busy 60.9 %, IPC 2.43 of 4 per SM
-ISSUE_BUSY, IPC = 0.609, 2.43
+# (profiles/r1/prof_crout_v18_raw.txt): issue slots busy 60.6 %, IPC 2.42 of 4 per SM
+ISSUE_BUSY, IPC = 0.606, 2.42
 UNIT = "Gfield-op/s"
 
 
