@@ -109,6 +109,7 @@ struct pluq_ctx {
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
   int64_t rpm_lazy = 1;            // rank-profile kernel: lazy-reduction register phases
   int64_t par_trsm = 1;            // speculative LU: the panel's L21 and U12 solves on two streams
+  int64_t sym_par = 1;             // rank-profile kernel: parallel symbolic replay (16 warps)
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
@@ -450,7 +451,15 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
     const int shape = rpm_shape(a.m, a.n, (int)nt);
     SmallArgs al = a;
     al.lazy = (int)c->rpm_lazy;
-    const size_t smem = rpm_smem_bytes(a.m, a.n, shape == 1 && al.lazy && a.invtab != nullptr);
+    size_t smem = rpm_smem_bytes(a.m, a.n, shape == 1 && al.lazy && a.invtab != nullptr);
+    // parallel symbolic replay: its scratch follows the table when it still fits
+    const size_t par_bytes = (size_t)sym_par_words(a.m, a.n) * 4;
+    al.sym_par = 0;
+    if (c->sym_par && nt >= 512 && smem + par_bytes <= 227 * 1024) {
+      al.sym_par = 1;
+      al.sym_par_off = (int)(smem - rpm_smem_bytes(a.m, a.n, false));
+      smem += par_bytes;
+    }
     switch (shape) {
       case 1:
         CU(cudaFuncSetAttribute(rpm_pluq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1034,6 +1043,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "rpm_threads") c->rpm_threads = value;
   else if (k == "rpm_lazy") c->rpm_lazy = value;
   else if (k == "par_trsm") c->par_trsm = value;
+  else if (k == "sym_par") c->sym_par = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;

@@ -34,6 +34,8 @@ struct SmallArgs {
   int* fail_count;
   int fail_base;                // index offset of this launch's first block in the list
   int lazy = 1;                 // rank-profile kernel: lazy-reduction register phases (shape 1)
+  int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
+  int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
 };
 
 __device__ void small_pluq_block(const SmallArgs& args, int blk);
@@ -152,7 +154,12 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   else if constexpr (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
   RPM_MARK(2);
-  if (tid < 32) {
+  if (args.sym_par && nw >= 16) {  // parallel replay (scratch behind the table region)
+    int* sp = reinterpret_cast<int*>(smem_dyn + ((rpm_smem_words(m, n) + 3) & ~3ll) + (args.sym_par_off >> 2));
+    Counts cc;
+    const int rs = sym_par(rows, cols, m, n, P, Q, args.threshold, rp, cp, sp, stk, &cc);
+    if (tid == 0) { s_cnt = cc; s_r = rs; }
+  } else if (tid < 32) {
     SymCtx s{rp, cp, rpos, cpos, args.threshold, {0, 0, 0, 0}};
     const int rs = sym_rec(rows, cols, m, n, P, Q, stk, s);
     if (lane == 0) { s_cnt = s.cnt; s_r = rs; }

@@ -307,6 +307,210 @@ __host__ __device__ inline int64_t sym_stack_words(int64_t m, int64_t n) {
   return 12 * (m + n) + 64;
 }
 
+// b') Parallel symbolic replay (16 warps).  The rank profile matrix of every node of
+// Algorithm 1 is R_A restricted to the node's rows x columns, so the split of a node
+// needs no child result: A1 = top-left quadrant; F = the top rows that are not A1
+// pivots (original order, as P1 leaves them) x the right columns; G = the bottom rows x
+// the left columns that are not A1 pivots; H = the bottom rows that are not G pivots x
+// the right columns that are not F pivots; and each child's rank is the number of ones
+// of R_A inside it.  The root and its four children are split top-down (one warp per
+// node), the up to 16 grandchildren (or terminal children) are replayed concurrently
+// by the sequential sym_rec (one warp each), then P, Q, rank and the charges are
+// composed bottom-up exactly as sym_rec does (recursive.py:248-254).
+struct SymNode {
+  const int* rows;
+  const int* cols;
+  int m, n;
+  int* P;
+  int* Q;
+  int r, kind;   // kind: 0 = unused, 1 = split, 2 = replayed sequentially
+  int cr[4];     // ranks of the four children (split nodes)
+  Counts cnt;
+};
+
+__host__ __device__ inline int64_t sym_par_words(int64_t m, int64_t n) {
+  return 16 * (m + n)                                   // per-warp rpos/cpos
+         + (m + n + 8) + 2 * (m + n) + 8                // level-1 lists, P/Q
+         + 4 * ((m + n) / 2 + 8) + 4 * (m + n + 8)      // level-2 lists, P/Q
+         + 4 * sym_stack_words(m / 2 + 1, n / 2 + 1)    // terminal level-1 nodes
+         + 16 * sym_stack_words(m / 4 + 2, n / 4 + 2)   // level-2 nodes
+         + 64;
+}
+
+__device__ __forceinline__ bool sym_terminal(int m, int n, int thr) {
+  return m == 0 || n == 0 || m == 1 || n == 1 || min(m, n) <= thr;
+}
+
+// Split node X (one converged warp): children written to ch[0..3]; lists and P/Q
+// storage are bump-allocated from *lp / *pq.
+__device__ __noinline__ void sym_split(const SymNode& X, SymNode* ch, int*& lp, int*& pq, const int* rp, const int* cp,
+                          int* rpos, int* cpos, int thr) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int m = X.m, n = X.n, kr = m / 2, kc = n / 2;
+  for (int a = lane; a < m; a += 32) rpos[X.rows[a]] = a;
+  for (int b = lane; b < n; b += 32) cpos[X.cols[b]] = b;
+  __syncwarp();
+  // local column of row a's one inside X (or -1), local row of column b's one
+  auto rowone = [&](int a) -> int {
+    const int x = rp[X.rows[a]];
+    if (x < 0) return -1;
+    const int q = cpos[x];
+    return ((unsigned)q < (unsigned)n && X.cols[q] == x) ? q : -1;
+  };
+  auto colone = [&](int b) -> int {
+    const int y = cp[X.cols[b]];
+    if (y < 0) return -1;
+    const int q = rpos[y];
+    return ((unsigned)q < (unsigned)m && X.rows[q] == y) ? q : -1;
+  };
+  // stable warp compaction of the indices [lo, hi) whose predicate holds
+  auto compact = [&](int lo, int hi, const int* src, int* dst, auto pred) -> int {
+    int cnt = 0;
+    for (int base = lo; base < hi; base += 32) {
+      const int i = base + lane;
+      const bool keep = i < hi && pred(i);
+      const unsigned bal = __ballot_sync(FULL, keep);
+      if (keep) dst[cnt + __popc(bal & ((1u << lane) - 1u))] = src[i];
+      cnt += __popc(bal);
+    }
+    return cnt;
+  };
+  int* Frows = lp; lp += kr;
+  const int nF = compact(0, kr, X.rows, Frows, [&](int a) { const int q = rowone(a); return !(q >= 0 && q < kc); });
+  int* Gcols = lp; lp += kc;
+  const int nG = compact(0, kc, X.cols, Gcols, [&](int b) { const int q = colone(b); return !(q >= 0 && q < kr); });
+  const int r1 = kr - nF;
+  // F pivots: right columns whose one lies in the top rows; G pivots: bottom rows whose
+  // one lies in the left columns (neither can be an A1 pivot)
+  int* Hrows = lp; lp += m - kr;
+  const int nH = compact(kr, m, X.rows, Hrows, [&](int a) { const int q = rowone(a); return !(q >= 0 && q < kc); });
+  int* Hcols = lp; lp += n - kc;
+  const int nHc = compact(kc, n, X.cols, Hcols, [&](int b) { const int q = colone(b); return !(q >= 0 && q < kr); });
+  const int r3 = (m - kr) - nH, r2 = (n - kc) - nHc;
+  __syncwarp();
+  if (lane == 0) {
+    ch[0] = SymNode{X.rows, X.cols, kr, kc, nullptr, nullptr, 0, 0, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    ch[1] = SymNode{Frows, X.cols + kc, nF, n - kc, nullptr, nullptr, 0, 0, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    ch[2] = SymNode{X.rows + kr, Gcols, m - kr, nG, nullptr, nullptr, 0, 0, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    ch[3] = SymNode{Hrows, Hcols, nH, nHc, nullptr, nullptr, 0, 0, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    for (int c = 0; c < 4; ++c) {
+      ch[c].P = pq; pq += ch[c].m;
+      ch[c].Q = pq; pq += ch[c].n;
+      ch[c].kind = sym_terminal(ch[c].m, ch[c].n, thr) ? 2 : 1;
+    }
+    (void)r1; (void)r2; (void)r3;
+  }
+  __syncwarp();
+}
+
+// P, Q, rank and charges of split node X from its four children (sym_rec's tail).
+__device__ void sym_compose(SymNode& X, const SymNode* ch) {
+  const int lane = threadIdx.x & 31;
+  const int m = X.m, n = X.n, kr = m / 2, kc = n / 2;
+  const int r1 = ch[0].r, r2 = ch[1].r, r3 = ch[2].r, r4 = ch[3].r;
+  const int* P1 = ch[0].P; const int* Q1 = ch[0].Q;
+  const int* P2 = ch[1].P; const int* Q2 = ch[1].Q;
+  const int* P3 = ch[2].P; const int* Q3 = ch[2].Q;
+  const int* P4 = ch[3].P; const int* Q4 = ch[3].Q;
+  for (int t = lane; t < m; t += 32) {
+    int y;
+    if (t < kr) { const int z = P1[t]; y = z < r1 ? z : r1 + P2[z - r1]; }
+    else { const int z = P3[t - kr]; y = kr + (z < r3 ? z : r3 + P4[z - r3]); }
+    X.P[t] = s_sigma(y, r1, r2, r3, r4, kr);
+  }
+  for (int t = lane; t < n; t += 32) {
+    const int z = t_sigma(t, r1, r2, r3, r4, kc);
+    int y;
+    if (z < kc) { const int w = z < r1 ? z : r1 + Q3[z - r1]; y = Q1[w]; }
+    else { const int zz = z - kc; const int w = zz < r2 ? zz : r2 + Q4[zz - r2]; y = kc + Q2[w]; }
+    X.Q[t] = y;
+  }
+  if (lane == 0) {
+    Counts c{0, 0, 0, 0};
+    for (int q = 0; q < 4; ++q) {
+      c.mul += ch[q].cnt.mul; c.add += ch[q].cnt.add; c.inv += ch[q].cnt.inv; c.red += ch[q].cnt.red;
+    }
+    charge_trsm_l(c, r1, n - kc);
+    charge_trsm_u(c, m - kr, r1);
+    charge_mm(c, kr - r1, n - kc, r1);
+    charge_mm(c, m - kr, kc - r1, r1);
+    charge_mm(c, m - kr, n - kc, r1);
+    const int m4 = m - kr - r3, n4 = n - kc - r2;
+    charge_trsm_u(c, r3, r2);
+    charge_trsm_l(c, r3, r2);
+    charge_trsm_u(c, m4, r2);
+    charge_trsm_l(c, r3, n4);
+    charge_mm(c, r3, n4, r2);
+    charge_mm(c, m4, n4, r2);
+    charge_mm(c, m4, n4, r3);
+    X.cnt = c;
+    X.r = r1 + r2 + r3 + r4;
+  }
+  __syncwarp();
+}
+
+// All threads of the CTA (>= 16 warps).  Returns the rank; P, Q, cnt_out as sym_rec.
+__device__ __noinline__ int sym_par(const int* rows, const int* cols, int m, int n, int* P, int* Q, int thr, const int* rp,
+                       const int* cp, int* scratch, int* stk_seq, Counts* cnt_out) {
+  __shared__ SymNode nd[21];  // root, 4 children, 16 grandchildren
+  __shared__ int s_rank;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int* rposw = scratch + w * (m + n);
+  int* cposw = rposw + m;
+  int* sp = scratch + 16 * (m + n);
+  int* l1_lists = sp; sp += m + n + 8;
+  int* l1_pq = sp; sp += 2 * (m + n) + 8;
+  int* l2_lists = sp; sp += 4 * ((m + n) / 2 + 8);
+  int* l2_pq = sp; sp += 4 * (m + n + 8);
+  const int big = (int)sym_stack_words(m / 2 + 1, n / 2 + 1), small = (int)sym_stack_words(m / 4 + 2, n / 4 + 2);
+  int* big_stk = sp; sp += 4 * big;
+  int* small_stk = sp;
+  if (sym_terminal(m, n, thr)) {  // whole block replayed by one warp
+    if (w == 0) {
+      SymCtx s{rp, cp, rposw, cposw, thr, {0, 0, 0, 0}};
+      const int r = sym_rec(rows, cols, m, n, P, Q, stk_seq, s);
+      if (lane == 0) { *cnt_out = s.cnt; s_rank = r; }
+    }
+    __syncthreads();
+    return s_rank;
+  }
+  if (w == 0) {
+    if (lane == 0) nd[0] = SymNode{rows, cols, m, n, P, Q, 0, 1, {0, 0, 0, 0}, {0, 0, 0, 0}};
+    __syncwarp();
+    int* lp = l1_lists; int* pq = l1_pq;
+    sym_split(nd[0], nd + 1, lp, pq, rp, cp, rposw, cposw, thr);
+  }
+  __syncthreads();
+  if (w < 4 && nd[1 + w].kind == 1) {
+    int* lp = l2_lists + w * ((m + n) / 2 + 8);
+    int* pq = l2_pq + w * (m + n + 8);
+    sym_split(nd[1 + w], nd + 5 + 4 * w, lp, pq, rp, cp, rposw, cposw, thr);
+  }
+  __syncthreads();
+  // replay: level-2 node 5 + w (its parent split), or the terminal level-1 node w / 4
+  {
+    SymNode* X = nullptr;
+    int* stk = nullptr;
+    if (nd[1 + w / 4].kind == 1) { X = nd + 5 + w; stk = small_stk + w * small; }
+    else if ((w & 3) == 0) { X = nd + 1 + w / 4; stk = big_stk + (w / 4) * big; }
+    if (X) {
+      SymCtx s{rp, cp, rposw, cposw, thr, {0, 0, 0, 0}};
+      const int r = sym_rec(X->rows, X->cols, X->m, X->n, X->P, X->Q, stk, s);
+      if (lane == 0) { X->r = r; X->cnt = s.cnt; }
+    }
+  }
+  __syncthreads();
+  if (w < 4 && nd[1 + w].kind == 1) sym_compose(nd[1 + w], nd + 5 + 4 * w);
+  __syncthreads();
+  if (w == 0) {
+    sym_compose(nd[0], nd + 1);
+    if (lane == 0) { *cnt_out = nd[0].cnt; s_rank = nd[0].r; }
+  }
+  __syncthreads();
+  return s_rank;
+}
+
 // c) Fraction-free right-looking LU of the generic block W (r pivots on the diagonal),
 // then L[k][s] = W[k][s] / W[s][s] and U[s][c] = W[s][c] / prod_{t<s} W[t][t].
 // dinv, dpre: r words of scratch each.
