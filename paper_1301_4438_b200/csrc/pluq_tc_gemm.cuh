@@ -162,7 +162,7 @@ constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, w
 template <int L, int V, bool MNB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
-                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg) {
+                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg, int group) {
   const int kplane = kblocks * TC_BK;  // rows of one MN-major B limb plane
   if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
@@ -185,7 +185,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t* epi_smem = reinterpret_cast<uint32_t*>(sB + (size_t)STAGES * L * B_TILE + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_n = n_pad / BN, tiles = (m_pad / TC_BM) * tiles_n;
+  const int tiles_n = n_pad / BN, tiles_m = m_pad / TC_BM, tiles = tiles_m * tiles_n;
+  // grouped rasterisation: consecutive tiles walk `group` tile rows before moving to the
+  // next tile column, so a wave of persistent CTAs touches a compact set of A row panels
+  // and B column panels (they stay in L2 instead of streaming B once per wave)
+  auto tile_coords = [&](int tile, int& m0, int& n0) {
+    const int g = group > 0 ? group : tiles_m;
+    const int span = g * tiles_n, gid = tile / span, fm = gid * g, gsz = min(tiles_m - fm, g);
+    const int rem = tile - gid * span;
+    m0 = (fm + rem % gsz) * TC_BM;
+    n0 = (rem / gsz) * BN;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -202,7 +212,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- TMA producer ----------------
     uint32_t g = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
+      int m0, n0;
+      tile_coords(tile, m0, n0);
       for (int kb = 0; kb < kblocks; ++kb, ++g) {
         const uint32_t s = g % STAGES;
         mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
@@ -317,7 +328,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const uint32_t buf = local % NBUF, use = local / NBUF;
-      const int m0 = (tile / tiles_n) * TC_BM, n0 = (tile % tiles_n) * BN;
+      int m0, n0;
+      tile_coords(tile, m0, n0);
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
@@ -508,6 +520,7 @@ struct TcGemm {
   int vec_limbs = 1;            // vectorised limb-split kernels (option tc_vec)
   int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
   int mn_b = 1;                 // option tc_mnb: MN-major B operand when the tile allows it (no transpose)
+  int raster_group = 8;         // option tc_group: tile rows per rasterisation group (0: row-major tiles)
   float mma_ms = 0.f;           // summed MMA-kernel time of the last call when timed
 
   static int limbs(uint32_t p) {
@@ -630,7 +643,7 @@ struct TcGemm {
         cudaEventRecord(e0, st);
       }
       tc_modgemm_kernel<L, V, MNB><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp,
-                                                                   stop, dbg);
+                                                                   stop, dbg, raster_group);
       if (time_mma) {
         float ms = 0.f;
         cudaEventRecord(e1, st);
