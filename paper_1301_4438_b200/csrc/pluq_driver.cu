@@ -1028,6 +1028,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "tc_cfg") c->tc.variant = (int)value;
   else if (k == "tc_mnb") c->tc.mn_b = (int)value;
   else if (k == "tc_group") c->tc.raster_group = (int)value;
+  else if (k == "tc_cpf") c->tc.c_prefetch = (int)value;
   else if (k == "tc_grid") c->tc.grid_override = (int)value;
   else if (k == "tc_dbg") c->tc.dbg = (int)value;
   else if (k == "tc_vec") c->tc.vec_limbs = (int)value;

@@ -162,7 +162,8 @@ constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, w
 template <int L, int V, bool MNB>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
-                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg, int group) {
+                      int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg, int group,
+                      int c_prefetch) {
   const int kplane = kblocks * TC_BK;  // rows of one MN-major B limb plane
   if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
   constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
@@ -330,6 +331,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t buf = local % NBUF, use = local / NBUF;
       int m0, n0;
       tile_coords(tile, m0, n0);
+      if (c_prefetch) {
+        // pull this thread's C row segment (HALF columns) into L2 while the tile's MMAs
+        // run, so the read-modify-write after the TMEM drain hits L2 instead of HBM
+        const int row = m0 + q * 32 + lane, col = n0 + h * HALF;
+        if (row < c.m && col < c.n) {
+          const char* p = reinterpret_cast<const char*>(c.row(row) + col);
+          const int bytes = min(HALF, c.n - col) * 4;
+          for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+        }
+      }
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
@@ -521,6 +532,7 @@ struct TcGemm {
   int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
   int mn_b = 1;                 // option tc_mnb: MN-major B operand when the tile allows it (no transpose)
   int raster_group = 8;         // option tc_group: tile rows per rasterisation group (0: row-major tiles)
+  int c_prefetch = 1;           // option tc_cpf: L2 prefetch of the C tile while its MMAs run
   float mma_ms = 0.f;           // summed MMA-kernel time of the last call when timed
 
   static int limbs(uint32_t p) {
@@ -643,7 +655,7 @@ struct TcGemm {
         cudaEventRecord(e0, st);
       }
       tc_modgemm_kernel<L, V, MNB><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp,
-                                                                   stop, dbg, raster_group);
+                                                                   stop, dbg, raster_group, c_prefetch);
       if (time_mma) {
         float ms = 0.f;
         cudaEventRecord(e1, st);

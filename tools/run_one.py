@@ -30,6 +30,7 @@ elif mode == "gemm":
     if os.environ.get("TC_GRID"): ctx.set_option("tc_grid", int(os.environ["TC_GRID"]))
     if os.environ.get("TC_DBG"): ctx.set_option("tc_dbg", int(os.environ["TC_DBG"]))
     if os.environ.get("TC_GROUP"): ctx.set_option("tc_group", int(os.environ["TC_GROUP"]))
+    if os.environ.get("TC_CPF"): ctx.set_option("tc_cpf", int(os.environ["TC_CPF"]))
     if os.environ.get("TC_VEC"): ctx.set_option("tc_vec", int(os.environ["TC_VEC"]))
     for it in range(3):
         torch.cuda.synchronize(); t0 = time.perf_counter()
