@@ -441,6 +441,9 @@ struct NodeRes {
 
 // Exact factorization of the blocks listed in fl/fc (every block of the grid when fl is
 // null): the rank-profile kernel (pluq_rpm.cuh) or the field-arithmetic recursion.
+// Dynamic shared memory a single-CTA block kernel may request: the 227 KB per-CTA limit
+// minus headroom for the kernels' static shared arrays (the symbolic replay's nodes).
+constexpr size_t kMaxDynSmem = 227 * 1024 - 4096;
 static size_t block_smem_bytes(int64_t m, int64_t n, int64_t thr) {
   return std::max(small_smem_bytes(m, n, thr), rpm_smem_bytes(m, n));
 }
@@ -455,7 +458,7 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
     // parallel symbolic replay: its scratch follows the table when it still fits
     const size_t par_bytes = (size_t)sym_par_words(a.m, a.n) * 4;
     al.sym_par = 0;
-    if (c->sym_par && nt >= 512 && smem + par_bytes <= 227 * 1024) {
+    if (c->sym_par && nt >= 512 && smem + par_bytes <= kMaxDynSmem) {
       al.sym_par = 1;
       al.sym_par_off = (int)(smem - rpm_smem_bytes(a.m, a.n, false));
       smem += par_bytes;
@@ -491,7 +494,7 @@ struct Driver {
   Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ModP::make(p)), threshold(thr), ops{ctx, ModP::make(p)} {}
 
   bool fits_small(int64_t m, int64_t n) const {
-    return m * n <= c->small_cap && block_smem_bytes(m, n, threshold) <= 227 * 1024;
+    return m * n <= c->small_cap && block_smem_bytes(m, n, threshold) <= kMaxDynSmem;
   }
 
   int depth = 0;            // depth of the node being processed
@@ -1139,7 +1142,7 @@ int pluq_factor_iterative(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int6
 }
 
 int64_t pluq_batched_max_elems(pluq_ctx*, int64_t m, int64_t n) {
-  return block_smem_bytes(m, n, 30) <= 227 * 1024 ? m * n : 0;
+  return block_smem_bytes(m, n, 30) <= kMaxDynSmem ? m * n : 0;
 }
 
 int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch, int64_t m, int64_t n,
@@ -1147,7 +1150,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
                         uint64_t* d_counts) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (block_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
+  if (block_smem_bytes(m, n, threshold) > kMaxDynSmem) return kUnsupported;
   if (batch == 0) return kOk;
   c->reset_stats();
   return guarded(c, [&] {
@@ -1246,7 +1249,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
                                  int64_t threshold, int64_t* psig, int64_t* qsig, int64_t* ranks) {
   if (threshold < 1 || batch < 0) return kInvalid;
   if (int v = validate(m, n, p)) return v;
-  if (block_smem_bytes(m, n, threshold) > 227 * 1024) return kUnsupported;
+  if (block_smem_bytes(m, n, threshold) > kMaxDynSmem) return kUnsupported;
   const auto hentry = std::chrono::steady_clock::now();
   return guarded(c, [&] {
     const int64_t mn = m * n;
