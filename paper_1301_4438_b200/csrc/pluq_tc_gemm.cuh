@@ -105,10 +105,10 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
 // MN-major, SWIZZLE_128B descriptor for a tile whose MN extent is one 128-byte swizzle
 // atom (rows = K, 128 bytes of N each): 8-row K groups 1024 B apart (SBO); LBO (the
 // stride between MN atoms) is unused with a single atom.
-__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo = 128 * 128) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((128 * 128) >> 4) << 16;  // leading byte offset (next MN atom; unused)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;  // leading byte offset: next 128-byte MN atom
   d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset: next group of 8 K rows
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
@@ -169,7 +169,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int BN = TcCfg<L, V>::BN, STAGES = TcCfg<L, V>::STAGES, NBUF = TcCfg<L, V>::NBUF;
   static_assert(!MNB || BN == 128, "MN-major B needs one 128-byte swizzle atom per tile");
   constexpr int NPOS = 2 * L - 1;
-  constexpr int ACC_COLS = NPOS * BN;               // one accumulator set
+  // MNB (L = 2): the two B limb tiles sit side by side along N in shared memory, so each
+  // A limb multiplies [B_lo | B_hi] in ONE N = 256 MMA: X = A_lo [B_lo|B_hi], Y = A_hi
+  // [B_lo|B_hi], and the limb positions are X0, X1 + Y0, Y1 (2 MMAs per K step, not 4).
+  constexpr bool CAT = MNB && L == 2;
+  constexpr int ACC_COLS = CAT ? 4 * BN : NPOS * BN;  // one accumulator set
   constexpr uint32_t TCOLS = 512;
   static_assert(NBUF * ACC_COLS <= 512, "the accumulator sets must fit in TMEM");
   constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
@@ -236,6 +240,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
     constexpr uint32_t idesc = idesc_i8(BN, MNB);
+    constexpr uint32_t idesc_cat = idesc_i8(2 * BN, true);
     uint32_t g = 0, local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       const uint32_t buf = local % NBUF, use = local / NBUF;
@@ -248,6 +253,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + (size_t)s * L * A_TILE);
         const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
+        if constexpr (CAT) {
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 32; ++kk) {
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            const uint64_t bd = desc_mn_sw128(b0 + kk * 32 * 128, B_TILE);
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              mma_i8(dacc + (uint32_t)(i * 2 * BN), desc_k_sw128(a0 + i * A_TILE + kk * 32), bd, idesc_cat, acc);
+          }
+          mma_commit(&empty[s]);
+          continue;
+        }
 #pragma unroll
         for (int kk = 0; kk < TC_BK / 32; ++kk) {
 #pragma unroll
@@ -284,9 +301,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // limb positions of one 16-column chunk -> 16 reduced values of this thread's row
     auto combine = [&](uint32_t lane_base, int cc, uint32_t (&v)[TC_CW]) {
       uint32_t acc[NPOS][TC_CW];
+      if constexpr (CAT) {  // X0 | X1 | Y0 | Y1  ->  positions X0, X1 + Y0, Y1
+        uint32_t y0[TC_CW];
+        tmem_ld16(lane_base + (uint32_t)cc, acc[0]);
+        tmem_ld16(lane_base + (uint32_t)(BN + cc), acc[1]);
+        tmem_ld16(lane_base + (uint32_t)(2 * BN + cc), y0);
+        tmem_ld16(lane_base + (uint32_t)(3 * BN + cc), acc[2]);
+        tmem_ld_wait();
 #pragma unroll
-      for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
-      tmem_ld_wait();
+        for (int t = 0; t < TC_CW; ++t) acc[1][t] += y0[t];
+      } else {
+#pragma unroll
+        for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+        tmem_ld_wait();
+      }
 #pragma unroll
       for (int t = 0; t < TC_CW; ++t) {
         if (NPOS <= 5) {
