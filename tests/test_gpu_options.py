@@ -1,0 +1,146 @@
+"""Every tuning option of the CUDA path gives the reference's bits (A/B of the kernel variants).
+
+The defaults are exercised by test_gpu_parity.py; here each alternative kernel selected by
+an option is run against the oracle on inputs that reach it: non-generic 64x64 batch
+blocks (rank-profile kernel: lazy phases, parallel symbolic replay), cfg4-shaped leaves
+(shape-2 rank-profile kernel), 128-wide speculative blocks (diagonal kernels, parallel
+panel solves) and the tensor-core GEMM (MN-major vs transposed B operand).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import pluq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb(cuda_ok):
+    import paper_1301_4438_b200 as mod
+    from paper_1301_4438_b200 import _native
+
+    _native.load_library()
+    return mod
+
+
+def _oracle(a0, p, thr=30):
+    x = np.asarray(a0, dtype=np.int64).astype(orc.field_dtype(p))
+    c = orc.Counts()
+    P, Q, r, c = orc.pluq(x, p, thr, c)
+    return P, Q, r, x.astype(np.int64), c.as_tuple()
+
+
+DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 3, "tc_mnb": 1, "par_trsm": 1, "small_cap": 128 * 128}
+
+
+class _opts:
+    def __init__(self, **kw):
+        from paper_1301_4438_b200 import _native
+
+        self.ctx, self.kw = _native.context(), kw
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.ctx.set_option(k, v)
+
+    def __exit__(self, *exc):
+        for k in self.kw:
+            self.ctx.set_option(k, DEFAULTS[k])
+
+
+def _nongeneric_batch(p, n_blocks, seed):
+    """64x64 blocks whose rank profile is not generic (zero leading minors, low rank)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in range(n_blocks):
+        kind = b % 3
+        if kind == 0:
+            a = rng.integers(0, p, (64, 64))
+            a[int(rng.integers(0, 64))] = 0  # a zero row
+            a[:, int(rng.integers(0, 8))] = 0  # a zero leading column
+        elif kind == 1:
+            a = orc.gen_xy_rank(64, 64, int(rng.integers(1, 60)), p, seed + b)
+        else:
+            a, _, _ = orc.gen_cfg4(seed=seed + b, m=64, n=64, r=int(rng.integers(4, 40)), p=p)
+        out.append(np.asarray(a, dtype=np.int64))
+    return np.stack(out)
+
+
+@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(sym_par=0, rpm_lazy=0), {}])
+@pytest.mark.parametrize("p", [65521, 8388593, 101])
+def test_rank_profile_kernel_variants(pb, opts, p):
+    import torch
+
+    batch = _nongeneric_batch(p, 24, seed=31 + p % 97)
+    with _opts(**opts):
+        t = torch.from_numpy(batch).cuda().to(torch.int32)
+        res = pb.pluq_batched(t, p, 30, with_counts=True)
+        torch.cuda.synchronize()
+    counts = res.counts.cpu().numpy()
+    for b in range(batch.shape[0]):
+        P, Q, r, packed, cnt = _oracle(batch[b], p)
+        assert int(res.ranks[b]) == r
+        assert np.array_equal(res.p_sigma[b].cpu().numpy(), P)
+        assert np.array_equal(res.q_sigma[b].cpu().numpy(), Q)
+        assert np.array_equal(t[b].cpu().numpy(), packed)
+        assert tuple(int(v) for v in counts[b]) == cnt
+
+
+@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), {}])
+@pytest.mark.parametrize("thr", [30, 4])
+def test_cfg4_shaped_leaves(pb, opts, thr):
+    """Prescribed rank profiles: the host recursion ends in shape-2 rank-profile leaves."""
+    p = 8388593
+    a0, _, _ = orc.gen_cfg4(seed=5, m=200, n=320, r=90, p=p)
+    P, Q, r, packed, cnt = _oracle(a0, p, thr)
+    with _opts(**opts):
+        a = pb.DenseMatrix(pb.PrimeField(p), np.asarray(a0, dtype=np.int64))
+        c = pb.OpCounts()
+        f = pb.pluq(a, threshold=thr, counts=c)
+    assert f.rank == r
+    assert np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(np.asarray(a.data, dtype=np.int64), packed)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cnt
+
+
+@pytest.mark.parametrize("opts", [dict(diag_lazy=1), dict(par_trsm=0), dict(diag_lazy=1, par_trsm=0), {}])
+@pytest.mark.parametrize("case", [("full", 400, 400, None), ("rank200", 400, 380, 200), ("rank128", 384, 384, 128)])
+def test_speculative_variants(pb, opts, case):
+    name, m, n, r = case
+    p = 65521
+    rng = np.random.default_rng(m + n)
+    a0 = rng.integers(0, p, (m, n)) if r is None else orc.gen_xy_rank(m, n, r, p, 11)
+    P, Q, rk, packed, _ = _oracle(a0, p)
+    with _opts(small_cap=1, **opts):
+        a = pb.DenseMatrix(pb.PrimeField(p), np.asarray(a0, dtype=np.int64))
+        f = pb.pluq(a)
+        st = pb.last_stats()
+    assert st["speculative_ok"] >= 1
+    assert f.rank == rk
+    assert np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(np.asarray(a.data, dtype=np.int64), packed)
+
+
+@pytest.mark.parametrize("mnb", [0, 1])
+@pytest.mark.parametrize("shape", [(256, 384, 200), (130, 260, 1100), (512, 128, 64)])
+def test_tc_gemm_b_layouts(pb, mnb, shape):
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    m, n, k = shape
+    p = 65521
+    rng = np.random.default_rng(m * 7 + k)
+    A = rng.integers(0, p, (m, k))
+    B = rng.integers(0, p, (k, n))
+    C = rng.integers(0, p, (m, n))
+    tc = torch.from_numpy(C).cuda().to(torch.int32)
+    ta = torch.from_numpy(A).cuda().to(torch.int32)
+    tb = torch.from_numpy(B).cuda().to(torch.int32)
+    with _opts(tc_mnb=mnb):
+        ctx = _native.context()
+        st = ctx.lib.pluq_modgemm_sub_tc(ctx.handle, tc.data_ptr(), n, ta.data_ptr(), k, tb.data_ptr(), n, m, n, k, p)
+        _native.raise_for(st, ctx, "tc gemm")
+        torch.cuda.synchronize()
+    want = (C.astype(object) - A.astype(object).dot(B.astype(object))) % p
+    assert np.array_equal(tc.cpu().numpy().astype(np.int64), want.astype(np.int64))
