@@ -110,6 +110,8 @@ struct pluq_ctx {
   int64_t rpm_lazy = 1;            // rank-profile kernel: lazy-reduction register phases
   int64_t par_trsm = 1;            // speculative LU: the panel's L21 and U12 solves on two streams
   int64_t sym_par = 1;             // rank-profile kernel: parallel symbolic replay (16 warps)
+  int64_t tc_trsm = 1;             // 128-wide TRSM as one in-place tensor-core GEMM with I - T^-1
+  int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
@@ -260,9 +262,32 @@ struct Ops {
   }
 
   // ---- B <- L^-1 B (kernels.py:59-83) -------------------------------------------------
+  // 128 x 128 triangular factor: B' = I - T^-1 from the two 64-block inverses, then one
+  // in-place tensor-core GEMM (C aliases an operand; both are split into limb planes first).
+  bool trsm128_tc(const View& t, const View& b, bool upper) {
+    if (!c->tc_trsm || !c->use_tc || t.m != 128 || (upper ? b.m : b.n) < c->tc_trsm_min) return false;
+    uint32_t* inv = c->dalloc_on<uint32_t>(2 * TR_BASE * TR_BASE, s());
+    uint32_t* bp = c->dalloc_on<uint32_t>(128 * 128, s());
+    if (upper) trinv_upper_kernel<<<2, 256, 0, s()>>>(t, inv, mp, c->invtab(mp.p), stop);
+    else trinv_lower_unit_kernel<<<2, 256, 0, s()>>>(t, inv, mp, stop);
+    c->check_launch();
+    if (upper) trinv128_combine_kernel<true><<<4, 256, 0, s()>>>(t, inv, bp, mp, stop);
+    else trinv128_combine_kernel<false><<<4, 256, 0, s()>>>(t, inv, bp, mp, stop);
+    c->check_launch();
+    const View bpv{bp, 128, 128, 128};
+    const int st = upper ? c->tc.run(b, b, bpv, mp, s(), stop, max_ctas) : c->tc.run(b, bpv, b, mp, s(), stop, max_ctas);
+    if (st != kOk) throw PluqError(st, "tensor-core TRSM failed: " + c->tc.last_error);
+    ++c->st_tc;
+    c->st_launch += 3;
+    c->dfree_on(bp, s());
+    c->dfree_on(inv, s());
+    return true;
+  }
+
   void trsm_l(const View& l, const View& b) {
     const int r = l.m;
     if (r == 0 || b.n == 0) return;
+    if (trsm128_tc(l, b, false)) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
     trinv_lower_unit_kernel<<<nb, 256, 0, s()>>>(l, inv, mp, stop);
@@ -287,6 +312,7 @@ struct Ops {
   void trsm_u(const View& b, const View& u) {
     const int r = u.m;
     if (r == 0 || b.m == 0) return;
+    if (trsm128_tc(u, b, true)) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
     trinv_upper_kernel<<<nb, 256, 0, s()>>>(u, inv, mp, c->invtab(mp.p), stop);
@@ -1049,6 +1075,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "rpm_lazy") c->rpm_lazy = value;
   else if (k == "par_trsm") c->par_trsm = value;
   else if (k == "sym_par") c->sym_par = value;
+  else if (k == "tc_trsm") c->tc_trsm = value;
+  else if (k == "tc_trsm_min") c->tc_trsm_min = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
   else if (k == "spec_check") c->spec_check = value;

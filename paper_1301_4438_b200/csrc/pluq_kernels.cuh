@@ -758,6 +758,100 @@ __global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t*
   for (int idx = threadIdx.x; idx < TR_BASE * TR_BASE; idx += blockDim.x) o[idx] = X[idx >> 6][idx & 63];
 }
 
+// 128x128 triangular block: B' = I - T^-1 from the inverses of its two 64x64 diagonal
+// blocks (trinv_*_kernel output, 2 x 64 x 64), so that the whole TRSM becomes ONE
+// in-place modular GEMM: B U^-1 = B - B (I - U^-1) and L^-1 B = B - (I - L^-1) B (the
+// tensor-core GEMM splits its A and B operands into limb planes before the MMA kernel,
+// so C may alias either operand).  Off-diagonal block of the inverse:
+//   upper  [X1 X12; 0 X2]:  X12 = -X1 (U12 X2)
+//   lower  [Y1 0; Y21 Y2]:  Y21 = -Y2 (L21 Y1)
+// Grid: 4 CTAs, each writes 32 columns of B'; the two CTAs over the off-diagonal block
+// compute their 32 columns of it (2 x 64 x 32 x 64 MACs).
+template <bool kUpper>
+__global__ void __launch_bounds__(256) trinv128_combine_kernel(View t, const uint32_t* inv64, uint32_t* bp,
+                                                               ModP mp, const int* stop) {
+  if (stopped(stop)) return;
+  __shared__ uint32_t MA[64][65], M3[64][33], T[64][33];  // MA holds B in pass 0, A in pass 1
+  const int tid = threadIdx.x, c0 = 32 * blockIdx.x;  // output columns [c0, c0 + 32)
+  const uint32_t* X1 = inv64;                // upper: X1 (top-left); lower: Y1
+  const uint32_t* X2 = inv64 + 64 * 64;      // upper: X2 (bottom-right); lower: Y2
+  const bool offdiag = kUpper ? c0 >= 64 : c0 < 64;
+  if (!offdiag) {
+    // diagonal-block columns: I - X (the other block row is 0 - 0 = 0)
+    const uint32_t* X = kUpper ? X1 : X2;
+    const int cb = kUpper ? c0 : c0 - 64;    // column inside the diagonal block
+    const int r0 = kUpper ? 0 : 64;          // block row holding the diagonal block
+    for (int idx = tid; idx < 128 * 32; idx += 256) {
+      const int i = idx >> 5, j = idx & 31;
+      uint32_t v = 0u;
+      if (i >= r0 && i < r0 + 64) {
+        const uint32_t x = X[(i - r0) * 64 + cb + j];
+        const uint32_t d = (i - r0 == cb + j) ? 1u : 0u;
+        v = d >= x ? d - x : d + (mp.p - x);
+      }
+      bp[i * 128 + c0 + j] = v;
+    }
+    return;
+  }
+  // off-diagonal columns: Z[:, cols] = -A (B C[:, cols]) with
+  //   upper: A = X1, B = U12 = t[0:64, 64:128], C = X2, cols = c0 - 64 ..
+  //   lower: A = Y2, B = L21 = t[64:128, 0:64], C = Y1, cols = c0 ..
+  const int cc = kUpper ? c0 - 64 : c0;
+  const uint32_t* Am = kUpper ? X1 : X2;
+  const uint32_t* Cm = kUpper ? X2 : X1;
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int i = idx >> 6, j = idx & 63;
+    MA[i][j] = kUpper ? t.at(i, 64 + j) : t.at(64 + i, j);
+  }
+  for (int idx = tid; idx < 64 * 32; idx += 256) {
+    const int i = idx >> 5, j = idx & 31;
+    M3[i][j] = Cm[i * 64 + cc + j];
+  }
+  __syncthreads();
+  const bool lazy = mp.kchunk >= 64;
+  const int i0 = tid >> 3, j0 = (tid & 7) * 4;  // 2 rows x 4 columns per thread: rows i0, i0 + 32
+  for (int pass = 0; pass < 2; ++pass) {
+    unsigned long long acc[2][4] = {};
+    for (int k = 0; k < 64; ++k) {
+      const uint32_t a0 = MA[i0][k];
+      const uint32_t a1 = MA[i0 + 32][k];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t b = pass == 0 ? M3[k][j0 + q] : T[k][j0 + q];
+        acc[0][q] += (unsigned long long)a0 * b;
+        acc[1][q] += (unsigned long long)a1 * b;
+        if (!lazy) { acc[0][q] = reduce64(acc[0][q], mp); acc[1][q] = reduce64(acc[1][q], mp); }
+      }
+    }
+    if (pass == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { T[i0][j0 + q] = reduce64(acc[0][q], mp); T[i0 + 32][j0 + q] = reduce64(acc[1][q], mp); }
+      __syncthreads();  // every read of MA (= B) is done
+      for (int idx = tid; idx < 64 * 64; idx += 256) MA[idx >> 6][idx & 63] = Am[idx];
+      __syncthreads();
+    } else {
+      // B' = I - Inv = -Z = A (B C) on the off-diagonal block (its identity part is 0)
+      const int rb = kUpper ? 0 : 64;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bp[(rb + i0) * 128 + c0 + j0 + q] = reduce64(acc[0][q], mp);
+        bp[(rb + i0 + 32) * 128 + c0 + j0 + q] = reduce64(acc[1][q], mp);
+      }
+    }
+  }
+  // the diagonal block in these columns: I - X2 (upper, rows 64..127) or I - Y1 (lower, rows 0..63)
+  {
+    const int rb = kUpper ? 64 : 0;          // block row of the diagonal block in these columns
+    const uint32_t* X = kUpper ? X2 : X1;
+    for (int idx = tid; idx < 64 * 32; idx += 256) {
+      const int i = idx >> 5, j = idx & 31;
+      const uint32_t x = X[i * 64 + cc + j];
+      const uint32_t d = (i == cc + j) ? 1u : 0u;
+      bp[(rb + i) * 128 + c0 + j] = d >= x ? d - x : d + (mp.p - x);
+    }
+  }
+}
+
 // B <- B * Uinv for a w-column block (w <= 64): one CTA owns 32 rows of B (in place);
 // 128 threads, each a 4x4 register tile (8 shared loads per 16 products).
 __global__ void __launch_bounds__(128) trsm_apply_right_kernel(View b, const uint32_t* uinv, ModP mp,
