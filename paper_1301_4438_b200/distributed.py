@@ -5,8 +5,9 @@ Schur-complement update is partitioned across GPUs and the pivot panels are broa
 (NCCL over NVLink on the GPU box, gloo in the CPU tests); the recursion and the base case
 stay on one GPU.
 
-Layout: column panels of width W, panel k (columns [kW, kW+W)) owned by rank k % N for
-all m rows (a 1 x N process grid of the 2D block partition).  Step k:
+Layout (default): column panels of width W, panel k (columns [kW, kW+W)) owned by rank
+k % N for all m rows (a 1 x N process grid); grid=(pr, pc) selects the 2D block-cyclic
+layout below (`distributed_generic_lu_2d`).  Step k of the 1 x N layout:
   1. the owner factors the panel below row kW on its GPU with the exact single-GPU path
      (`pluq_factor`, speculative generic LU inside);
   2. the panel is broadcast; every rank turns the pivot rows of its later panels into U
@@ -203,6 +204,213 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
     return mn
 
 
+# ---------------------------------------------------------------------------------------
+# 2D block-cyclic process grid (pr x pc): W x W blocks, row block b on grid row b % pr,
+# column panel k on grid column k % pc.  Per panel step the panel column is gathered on
+# its diagonal owner and factored there (the recursion and base case stay on one GPU),
+# the factored panel is broadcast, the grid row holding the pivot rows solves U12 for its
+# columns and broadcasts it down each grid column, and every rank updates its own rows x
+# columns with one GEMM (A22 -= L21 U12): the Schur-complement update is 2D-partitioned.
+# ---------------------------------------------------------------------------------------
+
+
+class Grid2D:
+    def __init__(self, pr: int, pc: int, rank: int):
+        self.pr, self.pc = pr, pc
+        self.gr, self.gc = divmod(rank, pc)
+        self.col_groups = None
+
+    def rank_of(self, gr: int, gc: int) -> int:
+        return gr * self.pc + gc
+
+    def make_groups(self):
+        """One process group per grid column (every rank creates every group, in order)."""
+        import torch.distributed as dist
+
+        self.col_groups = [dist.new_group([self.rank_of(r, c) for r in range(self.pr)]) for c in range(self.pc)]
+
+
+def _row_blocks(m: int, width: int, gr: int, pr: int):
+    """(global start, global end, local start) of the row blocks grid row gr owns."""
+    out, loc = [], 0
+    for b, r0 in enumerate(range(0, m, width)):
+        if b % pr == gr:
+            r1 = min(r0 + width, m)
+            out.append((r0, r1, loc))
+            loc += r1 - r0
+    return out, loc
+
+
+class LocalBlocks:
+    """A rank's blocks of the 2D layout in one dense tensor: its row blocks (in order) x
+    its column panels (in order), so that "my rows >= g" and "my panels > k" are always a
+    contiguous row suffix and column suffix."""
+
+    def __init__(self, tensor, rows, cols: LocalSlab):
+        self.t, self.rows, self.cols = tensor, rows, cols
+
+    def first_row_at_or_after(self, g: int) -> int:
+        for r0, r1, l0 in self.rows:
+            if r1 > g:
+                return l0 + max(0, g - r0)
+        return self.t.shape[0]
+
+    def global_rows(self, from_local: int):
+        idx = []
+        for r0, r1, l0 in self.rows:
+            for i in range(r0, r1):
+                if l0 + (i - r0) >= from_local:
+                    idx.append(i)
+        return idx
+
+    def panel(self, k):
+        return self.t[:, self.cols.off[k]:self.cols.off[k] + self.cols.w[k]]
+
+    def after(self, k):
+        later = [j for j in self.cols.owned if j > k]
+        return None if not later else self.t[:, self.cols.off[later[0]]:]
+
+
+def _layout_2d(m, n, width, grid: Grid2D, gr=None, gc=None):
+    gr = grid.gr if gr is None else gr
+    gc = grid.gc if gc is None else gc
+    rows, nrows = _row_blocks(m, width, gr, grid.pr)
+    owned, offsets, widths, ncols = _layout(n, width, gc, grid.pc)
+    return rows, nrows, LocalSlab(None, owned, offsets, widths), ncols
+
+
+def _index_lists(m, n, width, grid, gr, gc):
+    rows, _, cols, _ = _layout_2d(m, n, width, grid, gr, gc)
+    ridx = [i for r0, r1, _ in rows for i in range(r0, r1)]
+    cidx = [j for k in cols.owned for j in range(panel_bounds(n, width)[k][0], panel_bounds(n, width)[k][1])]
+    return ridx, cidx
+
+
+def scatter_2d(a_full, m, n, width, grid: Grid2D, make_empty) -> LocalBlocks:
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world()
+    rows, nrows, cols, ncols = _layout_2d(m, n, width, grid)
+    loc = LocalBlocks(make_empty(nrows, ncols), rows, cols)
+    for dst in range(world):
+        gr, gc = divmod(dst, grid.pc)
+        ridx, cidx = _index_lists(m, n, width, grid, gr, gc)
+        if not ridx or not cidx:
+            continue
+        if rank == 0:
+            ri = torch.tensor(ridx, device=a_full.device)
+            ci = torch.tensor(cidx, device=a_full.device)
+            blk = a_full.index_select(0, ri).index_select(1, ci).contiguous()
+            if dst == 0:
+                loc.t.copy_(blk)
+            else:
+                dist.send(blk, dst=dst)
+        elif rank == dst:
+            dist.recv(loc.t, src=0)
+    return loc
+
+
+def gather_2d(loc: LocalBlocks, a_full, m, n, width, grid: Grid2D, make_empty):
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world()
+    for src in range(world):
+        gr, gc = divmod(src, grid.pc)
+        ridx, cidx = _index_lists(m, n, width, grid, gr, gc)
+        if not ridx or not cidx:
+            continue
+        if rank == 0:
+            if src == 0:
+                blk = loc.t
+            else:
+                blk = make_empty(len(ridx), len(cidx))
+                dist.recv(blk, src=src)
+            ri = torch.tensor(ridx, device=a_full.device)
+            ci = torch.tensor(cidx, device=a_full.device)
+            a_full[ri.unsqueeze(1), ci.unsqueeze(0)] = blk
+        elif rank == src:
+            dist.send(loc.t.contiguous(), dst=0)
+
+
+def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid: Grid2D, backend, flags):
+    """distributed_generic_lu on a pr x pc grid (same contract: the rank r, or None)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world()
+    mn = min(m, n)
+    for k, (c0, c1) in enumerate(panel_bounds(n, width)):
+        if c0 >= mn:
+            break
+        wk = c1 - c0
+        gck, grk = k % grid.pc, k % grid.pr
+        root = grid.rank_of(grk, gck)
+        # 1. gather panel column k (rows >= c0) on its diagonal owner, in global row order
+        pan = flags.new_panel(m - c0, wk)
+        if grid.gc == gck:
+            lr = loc.first_row_at_or_after(c0)
+            mine = loc.panel(k)[lr:, :]
+            grows = loc.global_rows(lr)
+        for gr in range(grid.pr):
+            src = grid.rank_of(gr, gck)
+            rows_gr, _ = _row_blocks(m, width, gr, grid.pr)
+            gidx = [i for r0, r1, _ in rows_gr for i in range(max(r0, c0), r1)]
+            if not gidx:
+                continue
+            if rank == root:
+                if src == root:
+                    blk = mine
+                else:
+                    blk = flags.new_panel(len(gidx), wk)
+                    dist.recv(blk, src=src)
+                pan[torch.tensor(gidx, device=pan.device) - c0] = blk
+            elif rank == src:
+                dist.send(mine.contiguous(), dst=root)
+        # 2. factor on the root, broadcast the verdict and the factored panel
+        flag = flags()
+        if rank == root:
+            rk, generic = backend.factor_panel(pan)
+            flag[0], flag[1] = rk, int(generic)
+        if world > 1:
+            dist.broadcast(flag, src=root)
+        rk, generic = int(flag[0]), bool(int(flag[1]))
+        if not generic:
+            return None
+        if world > 1:
+            dist.broadcast(pan, src=root)
+        g = c0 + rk
+        # 3. the panel's grid column takes its rows of the factored panel back
+        if grid.gc == gck and len(grows):
+            loc.panel(k)[lr:, :] = pan[torch.tensor(grows, device=pan.device) - c0]
+        # 4. U12 on the grid row of the pivot rows, broadcast down each grid column
+        rest = loc.after(k)
+        top = None
+        if rest is not None and rk > 0:
+            if grid.gr == grk:
+                t0 = loc.first_row_at_or_after(c0)
+                top = rest[t0:t0 + rk, :]
+                backend.trsm_llu(pan[:rk, :rk], top)
+            if grid.pr > 1:
+                buf = top.contiguous() if grid.gr == grk else flags.new_panel(rk, rest.shape[1])
+                dist.broadcast(buf, src=grid.rank_of(grk, grid.gc), group=grid.col_groups[grid.gc])
+                top = buf
+            # 5. A22 -= L21 U12 on my rows >= g x my later panels
+            lg = loc.first_row_at_or_after(g)
+            if lg < loc.t.shape[0]:
+                l21 = pan[torch.tensor(loc.global_rows(lg), device=pan.device) - c0][:, :rk].contiguous()
+                backend.gemm_sub(rest[lg:, :], l21, top)
+        if rk < wk:
+            nz = flags()
+            lg = loc.first_row_at_or_after(g)
+            nz[0] = int(rest is not None and lg < loc.t.shape[0] and not backend.is_zero(rest[lg:, :]))
+            if world > 1:
+                dist.all_reduce(nz, op=dist.ReduceOp.MAX)
+            return g if int(nz[0]) == 0 else None
+    return mn
+
+
 class _Flags:
     """Small int64 flag tensors and panel receive buffers on the backend's device."""
 
@@ -223,10 +431,12 @@ class _Flags:
 
 def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: int = 30,
                      width: int = DEFAULT_PANEL, counts: OpCounts | None = None, backend=None,
-                     device=None):
+                     device=None, grid: tuple[int, int] | None = None):
     """pluq() of one large matrix held by rank 0 (CUDA int32 DenseMatrix), with the
     trailing updates spread over every rank of the default process group.  All ranks call
-    it; rank 0 gets the PluqFactors (in place, `f.packed is a`), the others get the rank."""
+    it; rank 0 gets the PluqFactors (in place, `f.packed is a`), the others get the rank.
+    grid=(pr, pc) with pr * pc == world selects the 2D block-cyclic layout (W x W blocks);
+    the default is the 1 x N column-panel layout."""
     import torch
 
     rank, world = _world()
@@ -245,10 +455,22 @@ def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: i
         full = x.clone()  # the original stays untouched until the final gather
     else:
         full = None
-    slab = scatter_panels(full, m, n, width, flags.empty)
-    r = distributed_generic_lu(slab, m, n, width, backend, flags)
-    if r is not None:
-        gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
+    if grid is not None:
+        pr, pc = grid
+        if pr * pc != world:
+            raise ValueError("grid must cover the process group")
+        g2 = Grid2D(pr, pc, rank)
+        if world > 1:
+            g2.make_groups()
+        loc = scatter_2d(full, m, n, width, g2, flags.empty)
+        r = distributed_generic_lu_2d(loc, m, n, width, g2, backend, flags)
+        if r is not None:
+            gather_2d(loc, full if rank == 0 else None, m, n, width, g2, flags.empty)
+    else:
+        slab = scatter_panels(full, m, n, width, flags.empty)
+        r = distributed_generic_lu(slab, m, n, width, backend, flags)
+        if r is not None:
+            gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
     if rank != 0:
         return r
     if r is None:  # not generic: the exact recursion on one GPU, from the untouched original

@@ -125,6 +125,80 @@ def test_two_rank_distributed_panels_vs_oracle():
 
 
 # ---------------------------------------------------------------------------------------
+# 2D block-cyclic grid (pr x pc) over 4 gloo ranks
+# ---------------------------------------------------------------------------------------
+
+CASES_2D = [  # (name, m, n, rank or None, p, width)
+    ("full", 40, 40, None, 65521, 8),
+    ("wide", 24, 50, None, 65521, 8),
+    ("tall", 52, 24, None, 65521, 8),
+    ("ragged", 45, 43, None, 65521, 8),           # partial last row block and panel
+    ("rank20_mid_panel", 40, 44, 20, 65521, 8),
+    ("rank16_edge", 40, 40, 16, 65521, 8),
+    ("small_p", 36, 36, None, 101, 8),
+    ("non_generic", 32, 40, 12, 101, 8),
+]
+
+
+def _worker_2d(rank, world, port, grids, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_4438_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for grid in grids:
+            g2 = D.Grid2D(grid[0], grid[1], rank)
+            g2.make_groups()
+            for name, m, n, r, p, width in CASES_2D:
+                a0 = _matrix(name, m, n, r, p)
+                full = torch.from_numpy(a0.astype(np.int64)) if rank == 0 else None
+                flags = D._Flags(torch.device("cpu"), torch.int64)
+                loc = D.scatter_2d(full, m, n, width, g2, flags.empty)
+                rk = D.distributed_generic_lu_2d(loc, m, n, width, g2, NumpyPanelBackend(p, 30), flags)
+                if rk is not None:
+                    D.gather_2d(loc, full if rank == 0 else None, m, n, width, g2, flags.empty)
+                out.append((grid, name, rk, full.numpy().copy() if rank == 0 and rk is not None else None))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_four_rank_2d_grid_vs_oracle():
+    grids = [(2, 2), (4, 1), (1, 4)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, 4, port, grids, q)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    i = 0
+    for grid in grids:
+        for name, m, n, r, p, width in CASES_2D:
+            a0 = _matrix(name, m, n, r, p)
+            x = a0.astype(orc.field_dtype(p))
+            P, Q, rr, _ = orc.pluq(x, p, 30)
+            generic = np.array_equal(P, np.arange(m)) and np.array_equal(Q, np.arange(n))
+            ranks = {res[k][i][2] for k in range(4)}
+            assert len(ranks) == 1, (grid, name)  # every rank reaches the same decision
+            rk0 = res[0][i][2]
+            if not generic:
+                assert rk0 is None, (grid, name)
+            else:
+                assert rk0 == rr, (grid, name)
+                assert np.array_equal(res[0][i][3], x.astype(np.int64)), (grid, name)
+            i += 1
+
+
+# ---------------------------------------------------------------------------------------
 # GPU: the CUDA backend (C ABI) in a single process, several panels on one rank
 # ---------------------------------------------------------------------------------------
 
@@ -135,7 +209,8 @@ def test_two_rank_distributed_panels_vs_oracle():
     ("rank150", 320, 300, 150, 65521, 64), ("p23", 256, 256, None, 8388593, 64),
     ("non_generic", 200, 260, 90, 65521, 64),
 ])
-def test_cuda_panels_vs_oracle(cuda_ok, name, m, n, r, p, width):
+@pytest.mark.parametrize("grid", [None, (1, 1)])
+def test_cuda_panels_vs_oracle(cuda_ok, name, m, n, r, p, width, grid):
     import torch
 
     import paper_1301_4438_b200 as pb
@@ -147,7 +222,7 @@ def test_cuda_panels_vs_oracle(cuda_ok, name, m, n, r, p, width):
     P, Q, rr, _ = orc.pluq(x, p, 30, c0)
     a = pb.DenseMatrix(pb.PrimeField(p), torch.from_numpy(a0).cuda().to(torch.int32))
     c = pb.OpCounts()
-    f = pluq_distributed(a, m, n, p, 30, width=width, counts=c)
+    f = pluq_distributed(a, m, n, p, 30, width=width, counts=c, grid=grid)
     assert f.rank == rr and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
     assert np.array_equal(a.data.cpu().numpy().astype(np.int64), x.astype(np.int64))
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == \
