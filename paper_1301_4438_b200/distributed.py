@@ -256,12 +256,10 @@ class LocalBlocks:
         return self.t.shape[0]
 
     def global_rows(self, from_local: int):
-        idx = []
-        for r0, r1, l0 in self.rows:
-            for i in range(r0, r1):
-                if l0 + (i - r0) >= from_local:
-                    idx.append(i)
-        return idx
+        """Global indices of the local rows [from_local, end) as an int64 numpy array."""
+        parts = [np.arange(max(r0, r0 + from_local - l0), r1, dtype=np.int64)
+                 for r0, r1, l0 in self.rows if l0 + (r1 - r0) > from_local]
+        return np.concatenate(parts) if parts else np.zeros(0, np.int64)
 
     def panel(self, k):
         return self.t[:, self.cols.off[k]:self.cols.off[k] + self.cols.w[k]]
@@ -356,8 +354,9 @@ def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid
         for gr in range(grid.pr):
             src = grid.rank_of(gr, gck)
             rows_gr, _ = _row_blocks(m, width, gr, grid.pr)
-            gidx = [i for r0, r1, _ in rows_gr for i in range(max(r0, c0), r1)]
-            if not gidx:
+            parts = [np.arange(max(r0, c0), r1, dtype=np.int64) for r0, r1, _ in rows_gr if r1 > c0]
+            gidx = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+            if not len(gidx):
                 continue
             if rank == root:
                 if src == root:
@@ -365,7 +364,10 @@ def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid
                 else:
                     blk = flags.new_panel(len(gidx), wk)
                     dist.recv(blk, src=src)
-                pan[torch.tensor(gidx, device=pan.device) - c0] = blk
+                if len(gidx) == gidx[-1] - gidx[0] + 1:  # contiguous rows: a slice copy
+                    pan[int(gidx[0]) - c0:int(gidx[-1]) + 1 - c0] = blk
+                else:
+                    pan[torch.from_numpy(gidx - c0).to(pan.device)] = blk
             elif rank == src:
                 dist.send(mine.contiguous(), dst=root)
         # 2. factor on the root, broadcast the verdict and the factored panel
@@ -383,7 +385,10 @@ def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid
         g = c0 + rk
         # 3. the panel's grid column takes its rows of the factored panel back
         if grid.gc == gck and len(grows):
-            loc.panel(k)[lr:, :] = pan[torch.tensor(grows, device=pan.device) - c0]
+            if len(grows) == grows[-1] - grows[0] + 1:
+                loc.panel(k)[lr:, :] = pan[int(grows[0]) - c0:int(grows[-1]) + 1 - c0]
+            else:
+                loc.panel(k)[lr:, :] = pan[torch.from_numpy(grows - c0).to(pan.device)]
         # 4. U12 on the grid row of the pivot rows, broadcast down each grid column
         rest = loc.after(k)
         top = None
@@ -399,7 +404,11 @@ def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid
             # 5. A22 -= L21 U12 on my rows >= g x my later panels
             lg = loc.first_row_at_or_after(g)
             if lg < loc.t.shape[0]:
-                l21 = pan[torch.tensor(loc.global_rows(lg), device=pan.device) - c0][:, :rk].contiguous()
+                gl = loc.global_rows(lg)
+                if len(gl) == gl[-1] - gl[0] + 1:
+                    l21 = pan[int(gl[0]) - c0:int(gl[-1]) + 1 - c0, :rk]
+                else:
+                    l21 = pan[torch.from_numpy(gl - c0).to(pan.device)][:, :rk].contiguous()
                 backend.gemm_sub(rest[lg:, :], l21, top)
         if rk < wk:
             nz = flags()

@@ -1,8 +1,9 @@
 """One large matrix across N GPUs (paper_1301_4438_b200.distributed), timed as the max over
 ranks of device-synchronised wall time.  Launch:
   python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
-      --master-port 29531 tools/dist_single.py cfg3|cfg5 [div] [panel]
-(cfg5 = 65536^2 rank 32768 / div; cfg3 = 8192^2 / div).  Rank 0 checks rank, structure and
+      --master-port 29531 tools/dist_single.py cfg3|cfg5 [div] [panel] [pr]
+(cfg5 = 65536^2 rank 32768 / div; cfg3 = 8192^2 / div; pr > 0 selects the 2D pr x (N/pr)
+grid, the default is the 1 x N column-panel layout).  Rank 0 checks rank, structure and
 Freivalds.  Single process without torchrun: world size 1."""
 import os
 import sys
@@ -20,6 +21,7 @@ from paper_1301_4438_b200.sharding import reduce_timing
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 div = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 width = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
+prow = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
 local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -40,7 +42,7 @@ for it in range(2):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    f = pb.pluq_distributed(a, m, n, p, 30, width=width)
+    f = pb.pluq_distributed(a, m, n, p, 30, width=width, grid=(prow, world // prow) if prow else None)
     torch.cuda.synchronize()
     t, _ = reduce_timing(time.perf_counter() - t0, 0.0, torch.device("cuda", local))
     if rank == 0:
