@@ -480,7 +480,7 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
     const int shape = rpm_shape(a.m, a.n, (int)nt);
     SmallArgs al = a;
     al.lazy = (int)c->rpm_lazy;
-    size_t smem = rpm_smem_bytes(a.m, a.n, shape == 1 && al.lazy && a.invtab != nullptr);
+    size_t smem = rpm_smem_bytes(a.m, a.n, (shape == 1 || shape == 2) && al.lazy && nt == 512 && a.invtab != nullptr);
     // parallel symbolic replay: its scratch follows the table when it still fits
     const size_t par_bytes = (size_t)sym_par_words(a.m, a.n) * 4;
     al.sym_par = 0;

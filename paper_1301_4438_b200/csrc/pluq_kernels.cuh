@@ -140,18 +140,25 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   __syncthreads();
   RPM_MARK(1);
   int r;
-  // shape 1: lazy-reduction phases (table staged in shared memory behind the block's words)
-  const bool lazy = shape == 1 && args.lazy && (args.invtab != nullptr || args.mp.kchunk >= 66);
+  // shapes 1 and 2: lazy-reduction phases (table staged in shared memory behind the block's
+  // words when p < 2^16; else 64-bit accumulators must hold 32 NR products: kchunk check)
+  const bool lazy = (shape == 1 || shape == 2) && args.lazy && nt == 512 &&  // rows w + 16 t: 16 warps
+                    (args.invtab != nullptr || args.mp.kchunk >= (shape == 1 ? 66u : 130u));
   uint16_t* stab = reinterpret_cast<uint16_t*>(smem_dyn + ((rpm_smem_words(m, n) + 3) & ~3ll));
   if (lazy && args.invtab) rl_stage_table(stab, args.invtab, args.mp.p);
   if constexpr (shape == 1) {
-    if (lazy && args.invtab) r = rpm_rows_lazy<true>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
-                                                     reinterpret_cast<int*>(diag));
-    else if (lazy) r = rpm_rows_lazy<false>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
-                                            reinterpret_cast<int*>(diag));
+    if (lazy && args.invtab) r = rpm_rows_lazy<true, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                                           reinterpret_cast<int*>(diag));
+    else if (lazy) r = rpm_rows_lazy<false, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                                  reinterpret_cast<int*>(diag));
     else r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
+  } else if constexpr (shape == 2) {
+    if (lazy && args.invtab) r = rpm_rows_lazy<true, 8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                                           reinterpret_cast<int*>(diag));
+    else if (lazy) r = rpm_rows_lazy<false, 8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                                  reinterpret_cast<int*>(diag));
+    else r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   }
-  else if constexpr (shape == 2) r = rpm_rows_reg<4, 8>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   else r = rpm_rows(W, ld, m, n, args.mp, rp, cp);
   RPM_MARK(2);
   if (args.sym_par && nw >= 16) {  // parallel replay (scratch behind the table region)
@@ -172,12 +179,14 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
   RPM_MARK(4);
   const bool inv = args.invtab != nullptr;
   if constexpr (shape == 1) {
-    if (lazy && inv) lu_lazy<true>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
-    else if (lazy) lu_lazy<false>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    if (lazy && inv) lu_lazy<true, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (lazy) lu_lazy<false, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
     else if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else if constexpr (shape == 2) {
-    if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
+    if (lazy && inv) lu_lazy<true, 8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (lazy) lu_lazy<false, 8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<4, 8, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else {
     for (int t = w; t < m; t += nw) {  // A'[t][u] = A[P^-1(t)][Q(u)]

@@ -757,30 +757,40 @@ __device__ __forceinline__ uint32_t rl_inv(uint32_t d, const ModP& mp, const uin
   if (d == 0u) return 0u;
   return kSmall ? (uint32_t)stab[d] : invmod(d, mp);
 }
-__device__ __forceinline__ unsigned long long rl_sel(const unsigned long long (&a)[4][2], int t, int q) {
-  unsigned long long x0 = a[0][0], x1 = a[0][1];
+template <int NR, int NQ>
+__device__ __forceinline__ unsigned long long rl_sel(const unsigned long long (&a)[NR][NQ], int t, int q) {
+  unsigned long long x[NQ];
 #pragma unroll
-  for (int u = 1; u < 4; ++u) { x0 = t == u ? a[u][0] : x0; x1 = t == u ? a[u][1] : x1; }
-  return q ? x1 : x0;
+  for (int c = 0; c < NQ; ++c) {
+    x[c] = a[0][c];
+#pragma unroll
+    for (int u = 1; u < NR; ++u) x[c] = t == u ? a[u][c] : x[c];
+  }
+  unsigned long long y = x[0];
+#pragma unroll
+  for (int c = 1; c < NQ; ++c) y = q == c ? x[c] : y;
+  return y;
 }
 
-// Column `col` of this warp's four rows, reduced (rows k <= lim give 0).
-template <bool kSmall>
-__device__ __forceinline__ void rl_column(const unsigned long long (&a)[4][2], int col, int lim, int m,
-                                          const ModP& mp, uint32_t e32, uint32_t (&cv)[4]) {
+// Column `col` of this warp's NR rows, reduced by lanes 0..NR-1 (rows k <= lim give 0).
+template <bool kSmall, int NR, int NQ>
+__device__ __forceinline__ void rl_column(const unsigned long long (&a)[NR][NQ], int col, int lim, int m,
+                                          const ModP& mp, uint32_t e32, uint32_t (&cv)[NR]) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int cq = col >> 5, cl = col & 31;
   unsigned long long mine = 0;
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const unsigned long long x = cq ? a[t][1] : a[t][0];
+  for (int t = 0; t < NR; ++t) {
+    unsigned long long x = a[t][0];
+#pragma unroll
+    for (int c = 1; c < NQ; ++c) x = cq == c ? a[t][c] : x;
     const unsigned long long y = __shfl_sync(FULL, x, cl);
     mine = lane == t ? y : mine;
   }
   const uint32_t red = rl_red<kSmall>(mine, mp, e32);
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < NR; ++t) {
     const int k = w + 16 * t;
     const uint32_t v = __shfl_sync(FULL, red, t);
     cv[t] = (k > lim && k < m) ? v : 0u;
@@ -798,19 +808,21 @@ __device__ __forceinline__ void rl_stage_table(uint16_t* stab, const uint16_t* t
 }
 __device__ __forceinline__ void rl_wait_table() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// a) R_A by row-order elimination (same outputs as rpm_rows_reg<2, 4>).
-template <bool kSmall>
+// a) R_A by row-order elimination (same outputs as rpm_rows_reg<NQ, NR>), 16 warps:
+// warp w holds rows w + 16 t (t < NR), lane holds columns lane + 32 q (q < NQ).
+template <bool kSmall, int NR, int NQ>
 __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, const ModP mp, int* rp, int* cp,
-                             const uint16_t* stab, uint32_t* wbuf /* [2][64] */, int* jbuf /* [2] */) {
+                             const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, int* jbuf /* [2] */) {
   const unsigned FULL = 0xffffffffu;
+  constexpr int WC = 32 * NQ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
-  unsigned long long a[4][2];
+  unsigned long long a[NR][NQ];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < NR; ++t) {
     const int k = w + 16 * t;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int c = lane + 32 * q;
       a[t][q] = (k < m && c < n) ? ga[(int64_t)k * lda + c] : 0u;
     }
@@ -823,17 +835,23 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
   auto publish = [&](int i) {
     if (w != (i & 15)) return;
     const int ti = i >> 4;
-    const uint32_t u0 = rl_red<kSmall>(rl_sel(a, ti, 0), mp, e32);
-    const uint32_t u1 = rl_red<kSmall>(rl_sel(a, ti, 1), mp, e32);
-    const unsigned b0 = __ballot_sync(FULL, u0 != 0u && lane < n);
-    const unsigned b1 = __ballot_sync(FULL, u1 != 0u && lane + 32 < n);
-    const int j = b0 ? __ffs(b0) - 1 : b1 ? 32 + __ffs(b1) - 1 : -1;
-    uint32_t* wb = wbuf + (i & 1) * 64;
+    uint32_t u[NQ];
+    int j = -1;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      u[q] = rl_red<kSmall>(rl_sel<NR, NQ>(a, ti, q), mp, e32);
+      const unsigned b = __ballot_sync(FULL, u[q] != 0u && lane + 32 * q < n);
+      if (j < 0 && b) j = 32 * q + __ffs(b) - 1;
+    }
+    uint32_t* wb = wbuf + (i & 1) * WC;
     if (j >= 0) {
-      const uint32_t d = __shfl_sync(FULL, j < 32 ? u0 : u1, j & 31);
+      uint32_t uj = u[0];
+#pragma unroll
+      for (int q = 1; q < NQ; ++q) uj = (j >> 5) == q ? u[q] : uj;
+      const uint32_t d = __shfl_sync(FULL, uj, j & 31);
       const uint32_t iv = rl_inv<kSmall>(d, mp, stab);
-      wb[lane] = u0 ? rl_mul<kSmall>(mp.p - u0, iv, mp) : 0u;
-      wb[lane + 32] = u1 ? rl_mul<kSmall>(mp.p - u1, iv, mp) : 0u;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) wb[lane + 32 * q] = u[q] ? rl_mul<kSmall>(mp.p - u[q], iv, mp) : 0u;
       if (lane == 0) { rp[i] = j; cp[j] = i; }
     }
     if (lane == 0) jbuf[i & 1] = j;
@@ -845,15 +863,16 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
     const int j = jbuf[i & 1];
     if (j >= 0) {
       ++r;
-      uint32_t cv[4];
-      rl_column<kSmall>(a, j, i, m, mp, e32, cv);
-      const uint32_t* wb = wbuf + (i & 1) * 64;
-      const uint32_t w0 = wb[lane], w1 = wb[lane + 32];
+      uint32_t cv[NR];
+      rl_column<kSmall, NR, NQ>(a, j, i, m, mp, e32, cv);
+      const uint32_t* wb = wbuf + (i & 1) * WC;
+      uint32_t wq[NQ];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        a[t][0] += (unsigned long long)cv[t] * w0;
-        a[t][1] += (unsigned long long)cv[t] * w1;
-      }
+      for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
+#pragma unroll
+      for (int t = 0; t < NR; ++t)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) a[t][q] += (unsigned long long)cv[t] * wq[q];
     }
     if (i + 1 < m && r < n) publish(i + 1);
   }
@@ -863,19 +882,20 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
 
 // c) unpivoted LU of A'[k][c] = A[pinv[k]][Q[c]] (r nonzero leading pivots), packed
 // factors written back to ga.  inv_s: r words of shared scratch.
-template <bool kSmall>
+template <bool kSmall, int NR, int NQ>
 __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const int* pinv, const int* Q,
-                        const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][64] */, uint32_t* inv_s) {
+                        const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, uint32_t* inv_s) {
   const unsigned FULL = 0xffffffffu;
+  constexpr int WC = 32 * NQ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
-  unsigned long long a[4][2];
+  unsigned long long a[NR][NQ];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < NR; ++t) {
     const int k = w + 16 * t;
     const uint32_t* src = k < m ? ga + (int64_t)pinv[k] * lda : ga;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int c = lane + 32 * q;
       a[t][q] = (k < m && c < n) ? src[Q[c]] : 0u;
     }
@@ -884,39 +904,45 @@ __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const in
   auto publish = [&](int s) {
     if (w != (s & 15)) return;
     const int ts = s >> 4;
-    const uint32_t u0 = rl_red<kSmall>(rl_sel(a, ts, 0), mp, e32);
-    const uint32_t u1 = rl_red<kSmall>(rl_sel(a, ts, 1), mp, e32);
-    const uint32_t d = __shfl_sync(FULL, s < 32 ? u0 : u1, s & 31);
+    uint32_t u[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) u[q] = rl_red<kSmall>(rl_sel<NR, NQ>(a, ts, q), mp, e32);
+    uint32_t us = u[0];
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) us = (s >> 5) == q ? u[q] : us;
+    const uint32_t d = __shfl_sync(FULL, us, s & 31);
     if (d == 0u) __trap();  // impossible for A' (leading minors 1..r nonzero)
     const uint32_t iv = rl_inv<kSmall>(d, mp, stab);
-    uint32_t* wb = wbuf + (s & 1) * 64;
-    wb[lane] = (lane > s && u0) ? rl_mul<kSmall>(mp.p - u0, iv, mp) : 0u;
-    wb[lane + 32] = (lane + 32 > s && u1) ? rl_mul<kSmall>(mp.p - u1, iv, mp) : 0u;
+    uint32_t* wb = wbuf + (s & 1) * WC;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      wb[lane + 32 * q] = (lane + 32 * q > s && u[q]) ? rl_mul<kSmall>(mp.p - u[q], iv, mp) : 0u;
     if (lane == 0) inv_s[s] = iv;
   };
   if (r > 0) publish(0);
   for (int s = 0; s < r; ++s) {
     __syncthreads();  // pivot row s published
-    uint32_t cv[4];
-    rl_column<kSmall>(a, s, s, m, mp, e32, cv);
-    const uint32_t* wb = wbuf + (s & 1) * 64;
-    const uint32_t w0 = wb[lane], w1 = wb[lane + 32];
+    uint32_t cv[NR];
+    rl_column<kSmall, NR, NQ>(a, s, s, m, mp, e32, cv);
+    const uint32_t* wb = wbuf + (s & 1) * WC;
+    uint32_t wq[NQ];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      a[t][0] += (unsigned long long)cv[t] * w0;
-      a[t][1] += (unsigned long long)cv[t] * w1;
-    }
+    for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) a[t][q] += (unsigned long long)cv[t] * wq[q];
     if (s + 1 < r) publish(s + 1);
   }
   __syncthreads();  // inverses of every pivot published
   // U entries are frozen after their row's pivot step, L entries (c < k) hold the Schur
   // value of their column's step (w_c = 0 afterwards), the trailing block is zero.
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < NR; ++t) {
     const int k = w + 16 * t;
     if (k >= m) continue;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int c = lane + 32 * q;
       if (c >= n) continue;
       uint32_t v = rl_red<kSmall>(a[t][q], mp, e32);
