@@ -111,6 +111,7 @@ struct pluq_ctx {
   int64_t par_trsm = 1;            // speculative LU: the panel's L21 and U12 solves on two streams
   int64_t sym_par = 1;             // rank-profile kernel: parallel symbolic replay (16 warps)
   int64_t tc_trsm = 1;             // 128-wide TRSM as one in-place tensor-core GEMM with I - T^-1
+  int64_t pair_leaves = 1;         // exact recursion: F and G leaves concurrently, one readback
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
@@ -541,6 +542,70 @@ struct Driver {
     return res;
   }
 
+  // Launch the leaf kernels of x on stream st with results at d_res + off (no readback).
+  // Layout at off: [P (m) | Q (n) | rank | generic flag | fail count | fail list (1)].
+  void launch_leaf(const View& x, size_t off, cudaStream_t st) {
+    int* res = c->d_res + off;
+    SmallArgs a;
+    a.a = x.a; a.lda = x.ld; a.bstride = 0; a.m = x.m; a.n = x.n; a.threshold = threshold; a.mp = mp;
+    a.p_out = res; a.q_out = res + x.m; a.r_out = res + x.m + x.n;
+    a.cnt_out = c->d_counts; a.cnt_accumulate = 1;
+    a.invtab = c->invtab(mp.p);
+    a.try_generic = (int)c->try_generic;
+    a.try_depth = 1;
+    a.generic_counts = nullptr;
+    a.generic_flag = a.try_generic ? res + x.m + x.n + 1 : nullptr;
+    a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
+    if (a.try_generic) {
+      a.fail_count = res + x.m + x.n + 2;
+      a.fail_list = res + x.m + x.n + 3;
+      CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), st));
+      const size_t cs = crout_smem_bytes(x.m, x.n);
+      CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
+      crout_fast_kernel<<<1, (unsigned)c->small_threads, cs, st>>>(a);
+      c->check_launch();
+    }
+    launch_exact(c, a, 1, (unsigned)c->small_threads, a.fail_list, a.fail_count, st);
+    ++c->st_small;
+  }
+
+  // F and G of Algorithm 1 are independent (disjoint blocks, both only need A1): when
+  // both are single-CTA leaves they run concurrently on two streams and come back with
+  // ONE readback (recursive.py:211-212).
+  void leaf_pair(const View& f, const View& g, NodeRes& F, NodeRes& G) {
+    const size_t off2 = ((size_t)f.m + f.n + 4 + 31) & ~size_t(31);
+    const size_t tot = off2 + (size_t)g.m + g.n + 4;
+    c->ensure_res(tot);
+    cudaStream_t side = c->side_streams()[3];
+    cudaEvent_t* ev = c->events(2);
+    CU(cudaEventRecord(ev[0], c->stream));
+    CU(cudaStreamWaitEvent(side, ev[0], 0));
+    launch_leaf(f, 0, c->stream);
+    launch_leaf(g, off2, side);
+    CU(cudaEventRecord(ev[1], side));
+    CU(cudaStreamWaitEvent(c->stream, ev[1], 0));
+    CU(cudaMemcpyAsync(c->h_res, c->d_res, tot * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (flagged_depth >= 0)
+      CU(cudaMemcpyAsync(c->h_zflags, c->d_zflags, (size_t)(flagged_depth + 1) * sizeof(int),
+                         cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    for (int dd = 0; dd <= flagged_depth; ++dd) zero_known[dd] = c->h_zflags[dd] == 0;
+    auto parse = [&](const View& x, size_t off, NodeRes& R) {
+      const int* h = c->h_res + off;
+      R.P.assign(h, h + x.m);
+      R.Q.assign(h + x.m, h + x.m + x.n);
+      R.r = h[x.m + x.n];
+      if (c->try_generic && h[x.m + x.n + 1]) {  // generic leaf: charges in closed form
+        generic_counts_rec(x.m, x.n, R.r, threshold, host_counts);
+        ++c->st_generic;
+      }
+    };
+    parse(f, 0, F);
+    parse(g, off2, G);
+  }
+
+  bool pairable(const View& x) const { return x.m > 0 && x.n > 0 && fits_small(x.m, x.n); }
+
   NodeRes leaf_small(const View& x) {
     c->ensure_res((size_t)x.m + x.n + 4);
     SmallArgs a;
@@ -826,9 +891,18 @@ struct Driver {
     charge_mm(host_counts, m - kr, n - kc, r1);
 
     ++depth;
-    NodeRes F = rec(x.sub(r1, kc, kr - r1, n - kc));
+    NodeRes F, G;
+    {
+      const View fv = x.sub(r1, kc, kr - r1, n - kc), gv = x.sub(kr, r1, m - kr, kc - r1);
+      if (c->pair_leaves && pairable(fv) && pairable(gv)) {
+        c->st_nodes += 2;
+        leaf_pair(fv, gv, F, G);
+      } else {
+        F = rec(fv);
+        G = rec(gv);
+      }
+    }
     const int r2 = F.r;
-    NodeRes G = rec(x.sub(kr, r1, m - kr, kc - r1));
     const int r3 = G.r;
     --depth;
     {
@@ -1076,6 +1150,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "par_trsm") c->par_trsm = value;
   else if (k == "sym_par") c->sym_par = value;
   else if (k == "tc_trsm") c->tc_trsm = value;
+  else if (k == "pair_leaves") c->pair_leaves = value;
   else if (k == "tc_trsm_min") c->tc_trsm_min = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
