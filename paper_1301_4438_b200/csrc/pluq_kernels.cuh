@@ -298,9 +298,12 @@ __global__ void crout_fast_kernel(SmallArgs args) {
 // double-buffered vector and scaled by its owner during step t+1, while readers apply
 // inv(U[t][t]) to that single term themselves; the owner of the pivot publishes its
 // inverse before the barrier.  Static shared arrays give immediate-offset LDS.
-template <int M, int N, int NT, bool kFast>
+// kSmall (p < 2^16, with the inverse table): dot-product accumulators stay below 2^38 and
+// are reduced with two 32-bit Barrett steps; products of residues fit 32 bits.
+template <int M, int N, int NT, bool kFast, bool kSmall = false>
 __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   static_assert(M + N - 1 <= NT, "one item per thread per step");
+  static_assert(!kSmall || kFast, "the small-prime path is a fast path");
   constexpr int MN = M < N ? M : N;
   constexpr int LD = N | 1;
   __shared__ uint32_t A[M * LD];
@@ -312,6 +315,11 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   const ModP mp = args.mp;
   const uint16_t* tab = args.invtab;
   uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
+  const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
+  auto mulm = [&](uint32_t a, uint32_t b) -> uint32_t { return kSmall ? reduce32(a * b, mp) : mulmod(a, b, mp); };
+  auto red = [&](uint64_t x) -> uint32_t {
+    return kSmall ? reduce32(reduce32((uint32_t)x, mp) + (uint32_t)(x >> 32) * e32, mp) : reduce64(x, mp);
+  };
   {
     const int w = tid >> 5, ln = tid & 31;
 #pragma unroll 4
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
     const int row = is_u ? t : t + 1 + (tid - nu);
     const int col = is_u ? t + tid : t;
     // scale the L entry of the previous step (nobody reads A[.][t-1] during this step)
-    if (own_i >= 0) A[own_i * LD + t - 1] = mulmod(own_num, inv_prev, mp);
+    if (own_i >= 0) A[own_i * LD + t - 1] = mulm(own_num, inv_prev);
     own_i = -1;
     if (is_u || is_l) {
       uint64_t acc = 0, acc2 = 0;
@@ -351,15 +359,15 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
         for (; kk < kend; ++kk) acc = reduce64(acc + (uint64_t)ri[kk] * cj[kk * LD], mp);
       }
       if (t > 0) {
-        const uint32_t lt = mulmod(Ncol[(t - 1) & 1][row], inv_prev, mp);  // L[row][t-1]
+        const uint32_t lt = mulm(Ncol[(t - 1) & 1][row], inv_prev);  // L[row][t-1]
         acc += (uint64_t)lt * cj[(t - 1) * LD];
       }
-      const uint32_t v = submod(A[row * LD + col], reduce64(acc, mp), mp);
+      const uint32_t v = submod(A[row * LD + col], red(acc), mp);
       if (is_u) {
         A[row * LD + col] = v;
         if (col == t) {
           if (v == 0u) zero_at = t;
-          else invs[t & 1] = tab ? (uint32_t)tab[v] : invmod(v, mp);
+          else invs[t & 1] = (kSmall || tab) ? (uint32_t)tab[v] : invmod(v, mp);
         }
       } else {
         Ncol[t & 1][row] = v;
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
     for (int q = tid; q < (M - t) * (N - t); q += NT) A[(t + q / (N - t)) * LD + t + q % (N - t)] = 0u;
     r = t;
   } else if (own_i >= 0) {
-    A[own_i * LD + MN - 1] = mulmod(own_num, inv_prev, mp);  // last L column
+    A[own_i * LD + MN - 1] = mulm(own_num, inv_prev);  // last L column
   }
   __syncthreads();
   {
@@ -431,7 +439,8 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
 // applies, otherwise the runtime-shape kernel.
 inline bool launch_crout_fixed(const SmallArgs& a, int64_t batch, cudaStream_t st) {
   if (a.m == 64 && a.n == 64) {
-    if (a.mp.kchunk >= 66) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    if (a.mp.mu32 != 0 && a.invtab) crout_fixed_kernel<64, 64, 128, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    else if (a.mp.kchunk >= 66) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else crout_fixed_kernel<64, 64, 128, false><<<(unsigned)batch, 128, 0, st>>>(a);
     return true;
   }
