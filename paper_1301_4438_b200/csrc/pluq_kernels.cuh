@@ -1036,31 +1036,6 @@ __global__ void invtab_kernel(uint16_t* tab, ModP mp) {
     tab[a] = a ? (uint16_t)invmod(a, mp) : 0;
 }
 
-// Diagonal block of the speculative no-pivot LU: Crout in shared memory until the
-// first zero pivot.  A zero pivot raises the stop flag (every later kernel of the
-// speculative schedule becomes a no-op) and records (k0, t) for the host.
-__global__ void __launch_bounds__(256) diag_crout_kernel(View blk, ModP mp, const uint16_t* invtab, int* stop,
-                                                         int* status, int k0) {
-  if (stopped(stop)) return;
-  extern __shared__ __align__(16) uint32_t smem_dyn[];
-  __shared__ BcShared sh;
-  const int m = blk.m, n = blk.n, lds = n | 1;
-  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  for (int i = w; i < m; i += nw)
-    for (int j = ln; j < n; j += 32) smem_dyn[i * lds + j] = blk.at(i, j);
-  __syncthreads();
-  View x{smem_dyn, lds, m, n};
-  const int t = crout_generic<false>(x, mp, invtab, &sh);
-  for (int i = w; i < m; i += nw)
-    for (int j = ln; j < n; j += 32) blk.at(i, j) = smem_dyn[i * lds + j];
-  if (threadIdx.x == 0 && t < min(m, n)) {
-    status[0] = k0;
-    status[1] = t;
-    __threadfence();
-    atomicExch(stop, 1);
-  }
-}
-
 // Diagonal block of the speculative LU, latency-optimised (one CTA of 1024 threads,
 // block <= 128 x 128): Crout with every dot product split over 4 threads (shuffle
 // reduction), the pivot settled first (a zero pivot leaves row/column t untouched for
