@@ -106,7 +106,8 @@ def test_cfg4_shaped_leaves(pb, opts, thr):
 
 
 @pytest.mark.parametrize("opts", [dict(diag_lazy=1), dict(par_trsm=0), dict(diag_lazy=1, par_trsm=0), dict(tc_trsm=0), {}])
-@pytest.mark.parametrize("case", [("full", 400, 400, None), ("rank200", 400, 380, 200), ("rank128", 384, 384, 128)])
+@pytest.mark.parametrize("case", [("full", 400, 400, None), ("rank200", 400, 380, 200), ("rank128", 384, 384, 128),
+                                  ("rank77", 300, 330, 77), ("rank129", 260, 300, 129)])
 def test_speculative_variants(pb, opts, case):
     name, m, n, r = case
     p = 65521
