@@ -146,3 +146,36 @@ def test_tc_gemm_b_layouts(pb, mnb, shape):
         torch.cuda.synchronize()
     want = (C.astype(object) - A.astype(object).dot(B.astype(object))) % p
     assert np.array_equal(tc.cpu().numpy().astype(np.int64), want.astype(np.int64))
+
+
+@pytest.mark.parametrize("p", [65521, 101, 8388593])
+@pytest.mark.parametrize("shape", [(128, 128), (96, 80), (40, 128), (128, 24)])
+def test_batched_nongeneric_shapes(pb, p, shape):
+    """Non-generic batches beyond 64x64: rank-profile kernel shape 2 (lazy phases with and
+    without the shared-memory inverse table) and the runtime-shape generic kernel."""
+    import torch
+
+    m, n = shape
+    rng = np.random.default_rng(m * 1000 + n + p % 997)
+    blocks = []
+    for b in range(6):
+        if b % 3 == 0:
+            a = rng.integers(0, p, (m, n))
+            a[:, :3] = 0  # zero leading columns: not generic
+        elif b % 3 == 1:
+            a = orc.gen_xy_rank(m, n, int(rng.integers(1, min(m, n))), p, b + 5)
+        else:
+            a = rng.integers(0, p, (m, n))  # generic w.h.p.
+        blocks.append(np.asarray(a, dtype=np.int64))
+    batch = np.stack(blocks)
+    t = torch.from_numpy(batch).cuda().to(torch.int32)
+    res = pb.pluq_batched(t, p, 30, with_counts=True)
+    torch.cuda.synchronize()
+    counts = res.counts.cpu().numpy()
+    for b in range(batch.shape[0]):
+        P, Q, r, packed, cnt = _oracle(batch[b], p)
+        assert int(res.ranks[b]) == r, b
+        assert np.array_equal(res.p_sigma[b].cpu().numpy(), P), b
+        assert np.array_equal(res.q_sigma[b].cpu().numpy(), Q), b
+        assert np.array_equal(t[b].cpu().numpy(), packed), b
+        assert tuple(int(v) for v in counts[b]) == cnt, b
