@@ -114,6 +114,8 @@ struct pluq_ctx {
   int64_t sym_par = 1;             // rank-profile kernel: parallel symbolic replay (16 warps)
   int64_t tc_trsm = 1;             // 128-wide TRSM as one in-place tensor-core GEMM with I - T^-1
   int64_t pair_leaves = 1;         // exact recursion: F and G leaves concurrently, one readback
+  int64_t stream_fb = 4;           // batches: CTAs of the concurrent rank-profile consumer (0: after)
+  int64_t stream_fb_spin = 4000000;  // consumer spin bound in cycles (~2 ms) without new work
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
@@ -1156,6 +1158,8 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "sym_par") c->sym_par = value;
   else if (k == "tc_trsm") c->tc_trsm = value;
   else if (k == "pair_leaves") c->pair_leaves = value;
+  else if (k == "stream_fb") c->stream_fb = value;
+  else if (k == "stream_fb_spin") c->stream_fb_spin = value;
   else if (k == "tc_trsm_min") c->tc_trsm_min = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
@@ -1282,24 +1286,51 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     int* flags = nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
     if (a.try_generic) {
-      flags = c->dalloc<int>((size_t)batch + 1 + (size_t)batch);
+      // flags: generic flag [batch] | fail count | fail list [batch] | done count | claim
+      flags = c->dalloc<int>(2 * (size_t)batch + 3);
       a.generic_flag = flags;
       a.fail_count = flags + batch;
       a.fail_list = flags + batch + 1;
+      int* done = flags + 2 * batch + 1;
+      int* claim = done + 1;
+      const bool streaming = c->stream_fb && c->exact_kernel && batch >= 1024;
       CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+      if (streaming) {
+        CU(cudaMemsetAsync(a.fail_list, 0xff, (size_t)batch * sizeof(int), c->stream));  // -1: slot not ready
+        CU(cudaMemsetAsync(done, 0, 2 * sizeof(int), c->stream));
+      }
       const size_t cs = crout_smem_bytes(m, n);
       CU(cudaFuncSetAttribute(crout_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs));
       cudaEvent_t ev[3];
       if (c->time_kernels)
         for (auto& e : ev) { CU(cudaEventCreate(&e)); }
+      SmallArgs g = a;
+      cudaStream_t cons = c->side_streams()[3];
+      cudaEvent_t* sev = c->events(2);
+      if (streaming) {
+        // a few resident consumer CTAs take the failure list while the generic kernel
+        // runs (bounded spin: if they are not co-scheduled they simply give up)
+        a.done_count = done;
+        a.stream_total = (int)batch;
+        g.done_count = done;
+        g.stream_total = (int)batch;
+        g.claim = claim;
+        g.spin_limit = c->stream_fb_spin;
+        CU(cudaEventRecord(sev[0], c->stream));
+        CU(cudaStreamWaitEvent(cons, sev[0], 0));
+        launch_exact(c, g, (unsigned)c->stream_fb, (unsigned)c->batch_threads, a.fail_list, a.fail_count, cons);
+        CU(cudaEventRecord(sev[1], cons));
+      }
       if (c->time_kernels) CU(cudaEventRecord(ev[0], c->stream));
       if (!(c->fixed_kernels && launch_crout_fixed(a, batch, c->stream)))
         crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
       c->check_launch();
       if (c->time_kernels) CU(cudaEventRecord(ev[1], c->stream));
-      // exact recursion only for the blocks that are not generic (persistent grid)
+      // exact recursion only for the blocks that are not generic (persistent grid); in
+      // streaming mode it takes whatever the consumers have not claimed
       const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 2);
-      launch_exact(c, a, grid, (unsigned)c->batch_threads, a.fail_list, a.fail_count, c->stream);
+      launch_exact(c, streaming ? g : a, grid, (unsigned)c->batch_threads, a.fail_list, a.fail_count, c->stream);
+      if (streaming) CU(cudaStreamWaitEvent(c->stream, sev[1], 0));
       if (c->time_kernels) {
         CU(cudaEventRecord(ev[2], c->stream));
         CU(cudaEventSynchronize(ev[2]));

@@ -34,6 +34,10 @@ struct SmallArgs {
   int* fail_count;
   int fail_base;                // index offset of this launch's first block in the list
   int lazy = 1;                 // rank-profile kernel: lazy-reduction register phases (shape 1)
+  int* done_count = nullptr;    // generic kernel: CTAs finished (streaming fallback consumer)
+  int* claim = nullptr;         // rank-profile kernel: next failure-list slot to take (streaming mode)
+  int stream_total = 0;         // CTAs of the generic launch (the consumer exits when all are done)
+  long long spin_limit = 0;     // consumer: give up waiting after this many cycles (no hang)
   int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
   int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
 };
@@ -220,8 +224,54 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
 }
 
 // One CTA per block, or a persistent grid over the failure list of the generic kernel.
+// Streaming mode (args.claim): the failure list is consumed while the generic kernel is
+// still running.  Slots are taken with a CAS on `claim`; a slot is ready when its entry
+// is >= 0 (the list is initialised to -1).  The loop ends when every slot is taken and
+// every generic CTA has finished, or after spin_limit cycles without work (a safety
+// bound: the kernel launched after the generic one on its stream takes what is left).
+__device__ __forceinline__ int rpm_next_slot(const SmallArgs& args, const int* fail_list, const int* fail_count) {
+  __shared__ int s_slot;
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    int got = -1;
+    while (true) {
+      const int have = *reinterpret_cast<const volatile int*>(fail_count);
+      const int q = *reinterpret_cast<volatile int*>(args.claim);
+      if (q < have) {
+        if (atomicCAS(args.claim, q, q + 1) == q) {
+          int v;
+          while ((v = *reinterpret_cast<const volatile int*>(fail_list + q)) < 0) __nanosleep(64);
+          got = v;
+          break;
+        }
+        continue;
+      }
+      if (!args.done_count || *reinterpret_cast<const volatile int*>(args.done_count) >= args.stream_total) {
+        // every generic CTA has finished: one last look at the count
+        if (q >= *reinterpret_cast<const volatile int*>(fail_count)) break;
+        continue;
+      }
+      if (args.spin_limit && clock64() - t0 > args.spin_limit) break;
+      __nanosleep(256);
+    }
+    s_slot = got;
+  }
+  __syncthreads();
+  const int v = s_slot;
+  __syncthreads();
+  return v;
+}
+
 template <int SHAPE>
 __global__ void __launch_bounds__(512, 1) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+  if (args.claim) {
+    for (int blk = rpm_next_slot(args, fail_list, fail_count); blk >= 0;
+         blk = rpm_next_slot(args, fail_list, fail_count)) {
+      rpm_pluq_block<SHAPE>(args, blk);
+      __syncthreads();
+    }
+    return;
+  }
   if (fail_list) {
     const int cnt = *fail_count;
     for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
@@ -401,7 +451,11 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
     if (__syncthreads_or(nz)) {
       if (tid == 0) {
         args.generic_flag[blockIdx.x] = 0;
-        if (args.fail_list) args.fail_list[atomicAdd(args.fail_count, 1)] = args.fail_base + blockIdx.x;
+        if (args.fail_list) {
+          const int slot = atomicAdd(args.fail_count, 1);
+          atomicExch(args.fail_list + slot, args.fail_base + blockIdx.x);  // a consumer may be waiting
+        }
+        if (args.done_count) { __threadfence(); atomicAdd(args.done_count, 1); }
       }
       return;
     }
@@ -423,6 +477,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   if (tid == 0) {
     args.generic_flag[blockIdx.x] = 1;
     args.r_out[blockIdx.x] = r;
+    if (args.done_count) atomicAdd(args.done_count, 1);
     if (args.generic_counts) {
       const unsigned long long* g = args.generic_counts + 4 * r;
       unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);

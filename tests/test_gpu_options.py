@@ -32,7 +32,7 @@ def _oracle(a0, p, thr=30):
 
 
 DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 3, "tc_mnb": 1, "par_trsm": 1, "tc_trsm": 1,
-            "pair_leaves": 1, "small_cap": 128 * 128}
+            "pair_leaves": 1, "stream_fb": 4, "small_cap": 128 * 128}
 
 
 class _opts:
@@ -173,6 +173,36 @@ def test_batched_nongeneric_shapes(pb, p, shape):
     torch.cuda.synchronize()
     counts = res.counts.cpu().numpy()
     for b in range(batch.shape[0]):
+        P, Q, r, packed, cnt = _oracle(batch[b], p)
+        assert int(res.ranks[b]) == r, b
+        assert np.array_equal(res.p_sigma[b].cpu().numpy(), P), b
+        assert np.array_equal(res.q_sigma[b].cpu().numpy(), Q), b
+        assert np.array_equal(t[b].cpu().numpy(), packed), b
+        assert tuple(int(v) for v in counts[b]) == cnt, b
+
+
+@pytest.mark.parametrize("stream_fb", [0, 4, 1])
+def test_streaming_fallback_consumer(pb, stream_fb):
+    """Large batches: the rank-profile consumer runs concurrently with the generic kernel
+    (stream_fb CTAs claiming the failure list) or after it (0) — same bits either way."""
+    import torch
+
+    p = 65521
+    rng = np.random.default_rng(2024 + stream_fb)
+    batch = rng.integers(0, p, (2048, 64, 64))
+    bad = rng.choice(2048, 40, replace=False)
+    for k, b in enumerate(bad):
+        if k % 2:
+            batch[b] = orc.gen_xy_rank(64, 64, int(rng.integers(1, 63)), p, int(b))
+        else:
+            batch[b][:, 0] = 0  # zero leading column: not generic
+    with _opts(stream_fb=stream_fb):
+        t = torch.from_numpy(batch).cuda().to(torch.int32)
+        res = pb.pluq_batched(t, p, 30, with_counts=True)
+        torch.cuda.synchronize()
+    counts = res.counts.cpu().numpy()
+    check = sorted(set(bad.tolist()) | set(rng.choice(2048, 24, replace=False).tolist()))
+    for b in check:
         P, Q, r, packed, cnt = _oracle(batch[b], p)
         assert int(res.ranks[b]) == r, b
         assert np.array_equal(res.p_sigma[b].cpu().numpy(), P), b
