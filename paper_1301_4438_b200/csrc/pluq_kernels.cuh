@@ -371,10 +371,17 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
     return kSmall ? reduce32(reduce32((uint32_t)x, mp) + (uint32_t)(x >> 32) * e32, mp) : reduce64(x, mp);
   };
   {
+    // stage the block with cp.async (4-byte copies: the odd row pitch keeps column walks
+    // conflict-free) so that all of a thread's loads are in flight at once
     const int w = tid >> 5, ln = tid & 31;
-#pragma unroll 4
+#pragma unroll
     for (int i = w; i < M; i += NT / 32)
-      for (int j = ln; j < N; j += 32) A[i * LD + j] = ga[(int64_t)i * args.lda + j];
+#pragma unroll
+      for (int j = ln; j < N; j += 32) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(A + i * LD + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(ga + (int64_t)i * args.lda + j));
+      }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::);
   }
   if (tid == 0) zero_at = -1;
   __syncthreads();
