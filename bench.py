@@ -103,6 +103,11 @@ class ClockSampler:
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            # let the sampler's first NVML queries finish before the timed region starts
+            # (they would otherwise delay the host thread's first timed launches)
+            t0 = time.perf_counter()
+            while len(self.samples) < 2 and time.perf_counter() - t0 < 0.5:
+                time.sleep(0.002)
         return self
 
     def __exit__(self, *a):
@@ -235,8 +240,9 @@ def main():
     def step():
         return pb.pluq_batched(work_buf, P, THRESHOLD)
 
-    for _ in range(max(args.warmup, 3)):
+    for w_ in range(max(args.warmup, 3)):  # same sequence as a timed step (copy, L2 flush, step)
         work_buf.copy_(pristine)
+        flush.fill_(w_ & 255)
         step()
     torch.cuda.synchronize(dev)
 
@@ -260,6 +266,8 @@ def main():
             dist.barrier()
         wall = time.perf_counter() - wall0
         step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
+        if os.environ.get("PLUQ_BENCH_STEPS"):
+            print("step_ms", " ".join(f"{v:.3f}" for v in step_ms), file=sys.stderr)
         ranks = res.ranks.to(torch.int64).cpu().numpy()
         w_step = float(sum(work(M, N, int(r)) for r in ranks))
         # per-kernel device times of one extra (untimed) step, CUDA events inside the library

@@ -129,6 +129,9 @@ struct pluq_ctx {
   int32_t* h_bres = nullptr;        // pinned per-block results (P, Q, rank)
   size_t h_bres_cap = 0;
   uint16_t* d_invtab = nullptr;  // inverse table for invtab_p (p < 2^16)
+  unsigned long long* gcount_tab = nullptr;  // generic-profile charges of the last batch shape
+  int64_t gcount_key[3] = {-1, -1, -1};
+  size_t rpm_smem_set[3] = {0, 0, 0};        // dynamic smem already granted to rpm_pluq_kernel<shape>
   uint32_t invtab_p = 0;
 
   const uint16_t* invtab(uint32_t p) {
@@ -451,7 +454,16 @@ static void generic_counts_rec(int64_t m, int64_t n, int64_t rho, int64_t thr, C
 
 
 // Per-rank table of generic-profile charges, uploaded for the batched kernel.
+// Per-rank closed-form charges of a generic m x n block, on the device.  The table of the
+// last (m, n, threshold) is kept in the context (cached: the batch API is called per step).
 static unsigned long long* upload_generic_counts(pluq_ctx* c, int64_t m, int64_t n, int64_t thr) {
+  if (c->gcount_tab && c->gcount_key[0] == m && c->gcount_key[1] == n && c->gcount_key[2] == thr)
+    return c->gcount_tab;
+  if (c->gcount_tab) {
+    c->sync();
+    CU(cudaFree(c->gcount_tab));
+    c->gcount_tab = nullptr;
+  }
   const int64_t mn = std::min(m, n);
   std::vector<unsigned long long> tab((size_t)(mn + 1) * 4);
   for (int64_t r = 0; r <= mn; ++r) {
@@ -459,9 +471,11 @@ static unsigned long long* upload_generic_counts(pluq_ctx* c, int64_t m, int64_t
     generic_counts_rec(m, n, r, thr, g);
     tab[4 * r] = g.mul; tab[4 * r + 1] = g.add; tab[4 * r + 2] = g.inv; tab[4 * r + 3] = g.red;
   }
-  unsigned long long* dt = c->dalloc<unsigned long long>(tab.size());
-  void* h = c->stage(tab.data(), tab.size() * sizeof(unsigned long long));
-  CU(cudaMemcpyAsync(dt, h, tab.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+  unsigned long long* dt = nullptr;
+  CU(cudaMalloc((void**)&dt, tab.size() * sizeof(unsigned long long)));
+  CU(cudaMemcpy(dt, tab.data(), tab.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  c->gcount_tab = dt;
+  c->gcount_key[0] = m; c->gcount_key[1] = n; c->gcount_key[2] = thr;
   return dt;
 }
 
@@ -496,15 +510,24 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
     }
     switch (shape) {
       case 1:
-        CU(cudaFuncSetAttribute(rpm_pluq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem > c->rpm_smem_set[1]) {
+          CU(cudaFuncSetAttribute(rpm_pluq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          c->rpm_smem_set[1] = smem;
+        }
         rpm_pluq_kernel<1><<<grid, nt, smem, st>>>(al, fl, fc);
         break;
       case 2:
-        CU(cudaFuncSetAttribute(rpm_pluq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem > c->rpm_smem_set[2]) {
+          CU(cudaFuncSetAttribute(rpm_pluq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          c->rpm_smem_set[2] = smem;
+        }
         rpm_pluq_kernel<2><<<grid, nt, smem, st>>>(al, fl, fc);
         break;
       default:
-        CU(cudaFuncSetAttribute(rpm_pluq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (smem > c->rpm_smem_set[0]) {
+          CU(cudaFuncSetAttribute(rpm_pluq_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          c->rpm_smem_set[0] = smem;
+        }
         rpm_pluq_kernel<0><<<grid, nt, smem, st>>>(al, fl, fc);
     }
   } else {
@@ -1106,6 +1129,7 @@ int pluq_destroy(pluq_ctx* c) {
   for (auto s : c->side) if (s) cudaStreamDestroy(s);
   if (c->d_res) cudaFree(c->d_res);
   if (c->h_res) cudaFreeHost(c->h_res);
+  if (c->gcount_tab) cudaFree(c->gcount_tab);
   if (c->d_counts) cudaFree(c->d_counts);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
@@ -1318,13 +1342,18 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
         g.spin_limit = c->stream_fb_spin;
         CU(cudaEventRecord(sev[0], c->stream));
         CU(cudaStreamWaitEvent(cons, sev[0], 0));
-        launch_exact(c, g, (unsigned)c->stream_fb, (unsigned)c->batch_threads, a.fail_list, a.fail_count, cons);
-        CU(cudaEventRecord(sev[1], cons));
       }
       if (c->time_kernels) CU(cudaEventRecord(ev[0], c->stream));
       if (!(c->fixed_kernels && launch_crout_fixed(a, batch, c->stream)))
         crout_fast_kernel<<<(unsigned)batch, (unsigned)c->batch_threads, cs, c->stream>>>(a);
       c->check_launch();
+      if (streaming) {
+        // submitted AFTER the generic kernel: if the two streams share a hardware queue the
+        // consumer simply runs afterwards (it never waits on a kernel that cannot start);
+        // otherwise it gets SMs as the generic grid drains
+        launch_exact(c, g, (unsigned)c->stream_fb, (unsigned)c->batch_threads, a.fail_list, a.fail_count, cons);
+        CU(cudaEventRecord(sev[1], cons));
+      }
       if (c->time_kernels) CU(cudaEventRecord(ev[1], c->stream));
       // exact recursion only for the blocks that are not generic (persistent grid); in
       // streaming mode it takes whatever the consumers have not claimed
@@ -1342,7 +1371,6 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       launch_exact(c, a, (unsigned)batch, (unsigned)c->batch_threads, nullptr, nullptr, c->stream);
     }
     if (!d_counts) c->dfree(cnt);
-    if (gtab) c->dfree(gtab);
     if (flags) c->dfree(flags);
   });
 }
@@ -1544,7 +1572,6 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       for (auto e : tev) cudaEventDestroy(e);
     }
     c->dfree(cnt);
-    if (gtab) c->dfree(gtab);
     if (flags) c->dfree(flags);
     c->dfree(dp);
     c->dfree(dA);
