@@ -297,6 +297,8 @@ def main():
             r2 = pb.pluq_batched(pin_np, P, THRESHOLD)
             e2e_t.append(time.perf_counter() - t0)
         w_e2e = float(sum(work(M, N, int(r)) for r in r2.ranks))
+        if os.environ.get("PLUQ_BENCH_STEPS"):
+            print("e2e_ms", " ".join(f"{1e3 * v:.3f}" for v in e2e_t), file=sys.stderr)
 
     from paper_1301_4438_b200.sharding import reduce_timing
 
