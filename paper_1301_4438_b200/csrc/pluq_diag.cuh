@@ -57,11 +57,13 @@ __global__ void __launch_bounds__(512, 1) diag_reg_kernel(View blk, ModP mp, con
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int r0 = 8 * w, j0 = 4 * lane;
   const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
-  if (kSmall) {
-    const int words = (int)(mp.p + 1) / 2;
-    const uint4* src = reinterpret_cast<const uint4*>(invtab);
-    uint4* dst = reinterpret_cast<uint4*>(tab);
-    for (int q = tid; q < (words + 3) / 4; q += 512) dst[q] = __ldg(src + q);
+  if (kSmall) {  // stage the inverse table with cp.async: every chunk in flight at once
+    const int chunks = (int)((mp.p + 7) / 8);
+    for (int q = tid; q < chunks; q += 512) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(tab + 8 * q);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(invtab + 8 * q));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
   }
   unsigned long long acc[8][4];
 #pragma unroll
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(512, 1) diag_reg_kernel(View blk, ModP mp, con
       out[i * LDO + j] = v;
     }
   }
+  if (kSmall) asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();  // table staged
   auto pinv = [&](uint32_t d) -> uint32_t { return d ? (kSmall ? (uint32_t)tab[d] : invmod(d, mp)) : 0u; };
   auto reload = [&](uint32_t (&c)[8], uint32_t (&wv)[4], int bb) {
