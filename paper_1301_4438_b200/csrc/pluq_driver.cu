@@ -116,6 +116,7 @@ struct pluq_ctx {
   int64_t pair_leaves = 1;         // exact recursion: F and G leaves concurrently, one readback
   int64_t stream_fb = 4;           // batches: CTAs of the concurrent rank-profile consumer (0: after)
   int64_t stream_fb_spin = 4000000;  // consumer spin bound in cycles (~2 ms) without new work
+  int64_t fb_prefix = 1;           // 64x64 batches: the rank-profile kernel resumes after the generic kernel's pivots
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
@@ -1184,6 +1185,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "pair_leaves") c->pair_leaves = value;
   else if (k == "stream_fb") c->stream_fb = value;
   else if (k == "stream_fb_spin") c->stream_fb_spin = value;
+  else if (k == "fb_prefix") c->fb_prefix = value;
   else if (k == "tc_trsm_min") c->tc_trsm_min = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;
@@ -1319,6 +1321,13 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       int* claim = done + 1;
       const bool streaming = c->stream_fb && c->exact_kernel && batch >= 1024;
       CU(cudaMemsetAsync(a.fail_count, 0, sizeof(int), c->stream));
+      uint32_t* prefix = nullptr;
+      if (c->fb_prefix && c->exact_kernel && c->fixed_kernels && m == 64 && n == 64 && a.invtab) {
+        // the 64x64 generic kernel leaves [t | its Crout image] per failure slot
+        a.prefix_slots = (int)std::min<int64_t>(batch, 1024);
+        prefix = c->dalloc<uint32_t>((size_t)a.prefix_slots * kPrefixWords);
+        a.prefix = prefix;
+      }
       if (streaming) {
         CU(cudaMemsetAsync(a.fail_list, 0xff, (size_t)batch * sizeof(int), c->stream));  // -1: slot not ready
         CU(cudaMemsetAsync(done, 0, 2 * sizeof(int), c->stream));
@@ -1360,6 +1369,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
       const unsigned grid = (unsigned)std::min<int64_t>(batch, 148 * 2);
       launch_exact(c, streaming ? g : a, grid, (unsigned)c->batch_threads, a.fail_list, a.fail_count, c->stream);
       if (streaming) CU(cudaStreamWaitEvent(c->stream, sev[1], 0));
+      if (prefix) c->dfree(prefix);
       if (c->time_kernels) {
         CU(cudaEventRecord(ev[2], c->stream));
         CU(cudaEventSynchronize(ev[2]));

@@ -14,6 +14,9 @@ __device__ __forceinline__ bool stopped(const int* stop) {
 // ---------------------------------------------------------------------------------
 // Small-node / batched PLUQ: one CTA per block, block staged through shared memory.
 // ---------------------------------------------------------------------------------
+// Words of one failure-prefix slot (header + the 64 x 65 Crout image of crout_fixed_kernel).
+constexpr int kPrefixWords = 4 + 64 * 65;
+
 struct SmallArgs {
   uint32_t* a;          // first block
   int64_t lda;          // row pitch in global memory
@@ -38,6 +41,8 @@ struct SmallArgs {
   int* claim = nullptr;         // rank-profile kernel: next failure-list slot to take (streaming mode)
   int stream_total = 0;         // CTAs of the generic launch (the consumer exits when all are done)
   long long spin_limit = 0;     // consumer: give up waiting after this many cycles (no hang)
+  uint32_t* prefix = nullptr;   // per failure slot: [t | 64 x 65 Crout image] of the generic kernel
+  int prefix_slots = 0;         // slots available in `prefix`
   int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
   int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
 };
@@ -111,7 +116,7 @@ __device__ void small_pluq_block(const SmallArgs& args, int blk) {
 // SHAPE (one code path per instantiation keeps each kernel small): 1 = registers, n <= 64
 // and <= 4 rows per warp; 2 = registers, n <= 128 and <= 8 rows per warp; 0 = shared memory.
 template <int SHAPE>
-__device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
+__device__ void rpm_pluq_block(const SmallArgs& args, int blk, int slot) {
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   __shared__ Counts s_cnt;
   __shared__ int s_r;
@@ -150,9 +155,21 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk) {
                     (args.invtab != nullptr || args.mp.kchunk >= (shape == 1 ? 66u : 130u));
   uint16_t* stab = reinterpret_cast<uint16_t*>(smem_dyn + ((rpm_smem_words(m, n) + 3) & ~3ll));
   if (lazy && args.invtab) rl_stage_table(stab, args.invtab, args.mp.p);
+  // prefix from the generic kernel (64 x 64 blocks): the first t0 pivots are (k, k); stage
+  // the L/U image (pitch 64) into the unused W region and eliminate only the Schur complement
+  int t0 = 0;
+  const uint32_t* simg = nullptr;
+  if (shape == 1 && lazy && args.invtab && m == 64 && n == 64 && args.prefix && slot >= 0 &&
+      slot < args.prefix_slots) {
+    const uint32_t* src = args.prefix + (size_t)slot * kPrefixWords;
+    t0 = (int)__ldcg(src);
+    for (int idx = tid; idx < 64 * 64; idx += nt) W[idx] = __ldcg(src + 4 + (idx >> 6) * 65 + (idx & 63));
+    simg = W;
+    __syncthreads();
+  }
   if constexpr (shape == 1) {
     if (lazy && args.invtab) r = rpm_rows_lazy<true, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
-                                                           reinterpret_cast<int*>(diag));
+                                                           reinterpret_cast<int*>(diag), simg, t0);
     else if (lazy) r = rpm_rows_lazy<false, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
                                                   reinterpret_cast<int*>(diag));
     else r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
@@ -239,9 +256,9 @@ __device__ __forceinline__ int rpm_next_slot(const SmallArgs& args, const int* f
       const int q = *reinterpret_cast<volatile int*>(args.claim);
       if (q < have) {
         if (atomicCAS(args.claim, q, q + 1) == q) {
-          int v;
-          while ((v = *reinterpret_cast<const volatile int*>(fail_list + q)) < 0) __nanosleep(64);
-          got = v;
+          while (*reinterpret_cast<const volatile int*>(fail_list + q) < 0) __nanosleep(64);
+          __threadfence();  // acquire: the slot's prefix image was written before its entry
+          got = q;
           break;
         }
         continue;
@@ -265,9 +282,8 @@ __device__ __forceinline__ int rpm_next_slot(const SmallArgs& args, const int* f
 template <int SHAPE>
 __global__ void __launch_bounds__(512, 1) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
   if (args.claim) {
-    for (int blk = rpm_next_slot(args, fail_list, fail_count); blk >= 0;
-         blk = rpm_next_slot(args, fail_list, fail_count)) {
-      rpm_pluq_block<SHAPE>(args, blk);
+    for (int q = rpm_next_slot(args, fail_list, fail_count); q >= 0; q = rpm_next_slot(args, fail_list, fail_count)) {
+      rpm_pluq_block<SHAPE>(args, *reinterpret_cast<const volatile int*>(fail_list + q), q);
       __syncthreads();
     }
     return;
@@ -275,12 +291,12 @@ __global__ void __launch_bounds__(512, 1) rpm_pluq_kernel(SmallArgs args, const 
   if (fail_list) {
     const int cnt = *fail_count;
     for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
-      rpm_pluq_block<SHAPE>(args, fail_list[q]);
+      rpm_pluq_block<SHAPE>(args, fail_list[q], q);
       __syncthreads();
     }
     return;
   }
-  rpm_pluq_block<SHAPE>(args, blockIdx.x);
+  rpm_pluq_block<SHAPE>(args, blockIdx.x, -1);
 }
 
 // register shape of rpm_pluq_kernel for an m x n block with `threads` per CTA
@@ -456,12 +472,22 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
       nz |= submod(A[i * LD + j], reduce64(acc, mp), mp) != 0u;
     }
     if (__syncthreads_or(nz)) {
+      // not generic: the first t pivots are (k, k) and their factors are final in A; hand
+      // them to the rank-profile kernel (R_A = diag(I_t, R_S), S the Schur complement)
+      __shared__ int s_slot;
+      if (tid == 0) s_slot = args.fail_list ? atomicAdd(args.fail_count, 1) : -1;
+      __syncthreads();
+      const int slot = s_slot;
+      if (M == 64 && N == 64 && LD == 65 && args.prefix && slot >= 0 && slot < args.prefix_slots) {
+        uint32_t* dst = args.prefix + (size_t)slot * kPrefixWords;
+        for (int idx = tid; idx < M * LD; idx += NT) dst[4 + idx] = A[idx];
+        if (tid == 0) dst[0] = (uint32_t)t;
+        __threadfence();
+      }
+      __syncthreads();
       if (tid == 0) {
         args.generic_flag[blockIdx.x] = 0;
-        if (args.fail_list) {
-          const int slot = atomicAdd(args.fail_count, 1);
-          atomicExch(args.fail_list + slot, args.fail_base + blockIdx.x);  // a consumer may be waiting
-        }
+        if (slot >= 0) atomicExch(args.fail_list + slot, args.fail_base + blockIdx.x);  // a consumer may be waiting
         if (args.done_count) { __threadfence(); atomicAdd(args.done_count, 1); }
       }
       return;

@@ -810,9 +810,13 @@ __device__ __forceinline__ void rl_wait_table() { asm volatile("cp.async.wait_al
 
 // a) R_A by row-order elimination (same outputs as rpm_rows_reg<NQ, NR>), 16 warps:
 // warp w holds rows w + 16 t (t < NR), lane holds columns lane + 32 q (q < NQ).
+// simg / t0 (optional): the first t0 rows have pivots (k, k) and simg (shared memory,
+// pitch 64) holds their unit-lower L and upper U; the elimination then starts at row t0 on
+// the Schur complement S = A22 - L21 U12 (R_A = diag(I_t0, R_S)).
 template <bool kSmall, int NR, int NQ>
 __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, const ModP mp, int* rp, int* cp,
-                             const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, int* jbuf /* [2] */) {
+                             const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, int* jbuf /* [2] */,
+                             const uint32_t* simg = nullptr, int t0 = 0) {
   const unsigned FULL = 0xffffffffu;
   constexpr int WC = 32 * NQ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -824,11 +828,44 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int c = lane + 32 * q;
-      a[t][q] = (k < m && c < n) ? ga[(int64_t)k * lda + c] : 0u;
+      a[t][q] = (k < m && c < n && (!simg || (k >= t0 && c >= t0))) ? ga[(int64_t)k * lda + c] : 0u;
     }
   }
-  for (int t = tid; t < m; t += blockDim.x) rp[t] = -1;
-  for (int t = tid; t < n; t += blockDim.x) cp[t] = -1;
+  if (simg && t0 > 0) {  // S = A22 - L21 U12 on this thread's rows >= t0, columns >= t0
+    unsigned long long s[NR][NQ];
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) s[t][q] = 0;
+    for (int kk = 0; kk < t0; ++kk) {
+      uint32_t u[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        u[q] = c < n ? simg[kk * 64 + c] : 0u;
+      }
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const int k = w + 16 * t;
+        const uint32_t l = k < m ? simg[k * 64 + kk] : 0u;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) s[t][q] += (unsigned long long)l * u[q];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int k = w + 16 * t, c = lane + 32 * q;
+        if (k >= t0 && c >= t0 && k < m && c < n) {
+          const uint32_t d = rl_red<kSmall>(s[t][q], mp, (uint32_t)((1ull << 32) % mp.p));
+          const uint32_t x = (uint32_t)a[t][q];
+          a[t][q] = x >= d ? x - d : x + (mp.p - d);
+        }
+      }
+  }
+  for (int t = tid; t < m; t += blockDim.x) rp[t] = t < t0 ? t : -1;
+  for (int t = tid; t < n; t += blockDim.x) cp[t] = t < t0 ? t : -1;
   if (kSmall) rl_wait_table();
   __syncthreads();  // table staged, rp/cp initialised
   // the owner warp of row i finds its first nonzero column and publishes -row / pivot
@@ -856,9 +893,9 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
     }
     if (lane == 0) jbuf[i & 1] = j;
   };
-  if (m > 0) publish(0);
-  int r = 0;
-  for (int i = 0; i < m && r < n; ++i) {
+  if (t0 < m) publish(t0);
+  int r = t0;
+  for (int i = t0; i < m && r < n; ++i) {
     __syncthreads();  // row i published
     const int j = jbuf[i & 1];
     if (j >= 0) {

@@ -32,7 +32,7 @@ def _oracle(a0, p, thr=30):
 
 
 DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 3, "tc_mnb": 1, "par_trsm": 1, "tc_trsm": 1,
-            "pair_leaves": 1, "stream_fb": 4, "small_cap": 128 * 128}
+            "pair_leaves": 1, "stream_fb": 4, "fb_prefix": 1, "small_cap": 128 * 128}
 
 
 class _opts:
@@ -68,7 +68,7 @@ def _nongeneric_batch(p, n_blocks, seed):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(sym_par=0, rpm_lazy=0), {}])
+@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(sym_par=0, rpm_lazy=0), dict(fb_prefix=0), {}])
 @pytest.mark.parametrize("p", [65521, 8388593, 101])
 def test_rank_profile_kernel_variants(pb, opts, p):
     import torch
@@ -181,8 +181,9 @@ def test_batched_nongeneric_shapes(pb, p, shape):
         assert tuple(int(v) for v in counts[b]) == cnt, b
 
 
+@pytest.mark.parametrize("prefix", [1, 0])
 @pytest.mark.parametrize("stream_fb", [0, 4, 1])
-def test_streaming_fallback_consumer(pb, stream_fb):
+def test_streaming_fallback_consumer(pb, stream_fb, prefix):
     """Large batches: the rank-profile consumer runs concurrently with the generic kernel
     (stream_fb CTAs claiming the failure list) or after it (0) — same bits either way."""
     import torch
@@ -192,11 +193,13 @@ def test_streaming_fallback_consumer(pb, stream_fb):
     batch = rng.integers(0, p, (2048, 64, 64))
     bad = rng.choice(2048, 40, replace=False)
     for k, b in enumerate(bad):
-        if k % 2:
+        if k % 4 == 3:
+            batch[b] = orc.gen_xy_rank(64, 64, 63, p, int(b))  # generic up to the last pivot
+        elif k % 2:
             batch[b] = orc.gen_xy_rank(64, 64, int(rng.integers(1, 63)), p, int(b))
         else:
             batch[b][:, 0] = 0  # zero leading column: not generic
-    with _opts(stream_fb=stream_fb):
+    with _opts(stream_fb=stream_fb, fb_prefix=prefix):
         t = torch.from_numpy(batch).cuda().to(torch.int32)
         res = pb.pluq_batched(t, p, 30, with_counts=True)
         torch.cuda.synchronize()
