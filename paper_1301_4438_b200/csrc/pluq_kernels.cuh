@@ -196,11 +196,15 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk, int slot) {
   RPM_MARK(3);
   if (s_r != r) __trap();  // the replay must find exactly the pivots of R_A
   for (int t = tid; t < m; t += nt) pinv[P[t]] = t;
-  __syncthreads();
+  // the prefix pivots (k, k), k < t0, come first in any quad-recursive order; use the
+  // prefix for the LU too when P and Q indeed fix them
+  bool fixed = true;
+  for (int t = tid; t < t0; t += nt) fixed &= P[t] == t && Q[t] == t;
+  if (!__syncthreads_and(fixed)) t0 = 0;
   RPM_MARK(4);
   const bool inv = args.invtab != nullptr;
   if constexpr (shape == 1) {
-    if (lazy && inv) lu_lazy<true, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    if (lazy && inv) lu_lazy<true, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv, simg, t0);
     else if (lazy) lu_lazy<false, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
     else if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);

@@ -919,14 +919,19 @@ __device__ int rpm_rows_lazy(const uint32_t* ga, int64_t lda, int m, int n, cons
 
 // c) unpivoted LU of A'[k][c] = A[pinv[k]][Q[c]] (r nonzero leading pivots), packed
 // factors written back to ga.  inv_s: r words of shared scratch.
+// simg / t0 (optional, P and Q fix 0..t0-1): the first t0 steps are already done in simg
+// (pitch 64, unit-lower L and U of A in its own order), so A' starts from its step-t0
+// state: U rows and L columns (scale 1) copied, the rest the permuted Schur complement.
 template <bool kSmall, int NR, int NQ>
 __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const int* pinv, const int* Q,
-                        const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, uint32_t* inv_s) {
+                        const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, uint32_t* inv_s,
+                        const uint32_t* simg = nullptr, int t0 = 0) {
   const unsigned FULL = 0xffffffffu;
   constexpr int WC = 32 * NQ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
   unsigned long long a[NR][NQ];
+  if (!simg) t0 = 0;
 #pragma unroll
   for (int t = 0; t < NR; ++t) {
     const int k = w + 16 * t;
@@ -934,8 +939,48 @@ __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const in
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int c = lane + 32 * q;
-      a[t][q] = (k < m && c < n) ? src[Q[c]] : 0u;
+      a[t][q] = (k < m && c < n && k >= t0 && c >= t0) ? src[Q[c]] : 0u;
     }
+  }
+  if (t0 > 0) {
+    unsigned long long s[NR][NQ];
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) s[t][q] = 0;
+    int qc[NQ], pk[NR];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) qc[q] = lane + 32 * q < n ? Q[lane + 32 * q] : 0;
+#pragma unroll
+    for (int t = 0; t < NR; ++t) pk[t] = w + 16 * t < m ? pinv[w + 16 * t] : 0;
+    for (int kk = 0; kk < t0; ++kk) {
+      uint32_t u[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) u[q] = simg[kk * 64 + qc[q]];
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const uint32_t l = simg[pk[t] * 64 + kk];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) s[t][q] += (unsigned long long)l * u[q];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int k = w + 16 * t, c = lane + 32 * q;
+        if (k >= m || c >= n) continue;
+        if (k >= t0 && c >= t0) {
+          const uint32_t d = rl_red<kSmall>(s[t][q], mp, e32);
+          const uint32_t x = (uint32_t)a[t][q];
+          a[t][q] = x >= d ? x - d : x + (mp.p - d);
+        } else if (k < t0 && c >= k) {
+          a[t][q] = simg[k * 64 + qc[q]];  // U row k (P fixes k)
+        } else {
+          a[t][q] = simg[pk[t] * 64 + c];  // L column c < t0, final (scale 1 below)
+        }
+      }
+    for (int c = tid; c < t0; c += blockDim.x) inv_s[c] = 1u;
   }
   __syncthreads();  // every original row is in registers before any packed row is written
   auto publish = [&](int s) {
@@ -956,8 +1001,8 @@ __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const in
       wb[lane + 32 * q] = (lane + 32 * q > s && u[q]) ? rl_mul<kSmall>(mp.p - u[q], iv, mp) : 0u;
     if (lane == 0) inv_s[s] = iv;
   };
-  if (r > 0) publish(0);
-  for (int s = 0; s < r; ++s) {
+  if (t0 < r) publish(t0);
+  for (int s = t0; s < r; ++s) {
     __syncthreads();  // pivot row s published
     uint32_t cv[NR];
     rl_column<kSmall, NR, NQ>(a, s, s, m, mp, e32, cv);
