@@ -116,6 +116,7 @@ struct pluq_ctx {
   int64_t pair_leaves = 1;         // exact recursion: F and G leaves concurrently, one readback
   int64_t stream_fb = 4;           // batches: CTAs of the concurrent rank-profile consumer (0: after)
   int64_t stream_fb_spin = 4000000;  // consumer spin bound in cycles (~2 ms) without new work
+  int64_t rpm_eager = 1;           // rank-profile kernel, p < 2^16: reduced 32-bit registers (else lazy 64-bit)
   int64_t fb_prefix = 1;           // 64x64 batches: the rank-profile kernel resumes after the generic kernel's pivots
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
@@ -500,6 +501,7 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
     const int shape = rpm_shape(a.m, a.n, (int)nt);
     SmallArgs al = a;
     al.lazy = (int)c->rpm_lazy;
+    al.eager = (int)c->rpm_eager;
     size_t smem = rpm_smem_bytes(a.m, a.n, (shape == 1 || shape == 2) && al.lazy && nt == 512 && a.invtab != nullptr);
     // parallel symbolic replay: its scratch follows the table when it still fits
     const size_t par_bytes = (size_t)sym_par_words(a.m, a.n) * 4;
@@ -1186,6 +1188,7 @@ int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   else if (k == "stream_fb") c->stream_fb = value;
   else if (k == "stream_fb_spin") c->stream_fb_spin = value;
   else if (k == "fb_prefix") c->fb_prefix = value;
+  else if (k == "rpm_eager") c->rpm_eager = value;
   else if (k == "tc_trsm_min") c->tc_trsm_min = value;
   else if (k == "trace_pipeline") c->trace_pipeline = value;
   else if (k == "spec_block") c->spec_block = value;

@@ -43,6 +43,7 @@ struct SmallArgs {
   long long spin_limit = 0;     // consumer: give up waiting after this many cycles (no hang)
   uint32_t* prefix = nullptr;   // per failure slot: [t | 64 x 65 Crout image] of the generic kernel
   int prefix_slots = 0;         // slots available in `prefix`
+  int eager = 0;                // rank-profile kernel, p < 2^16: eager (reduced) registers
   int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
   int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
 };
@@ -167,14 +168,19 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk, int slot) {
     simg = W;
     __syncthreads();
   }
+  const bool eager = lazy && args.invtab && args.mp.mu32 && args.eager;
   if constexpr (shape == 1) {
-    if (lazy && args.invtab) r = rpm_rows_lazy<true, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+    if (eager) r = rpm_rows_eager<4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                        reinterpret_cast<int*>(diag), simg, t0);
+    else if (lazy && args.invtab) r = rpm_rows_lazy<true, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
                                                            reinterpret_cast<int*>(diag), simg, t0);
     else if (lazy) r = rpm_rows_lazy<false, 4, 2>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
                                                   reinterpret_cast<int*>(diag));
     else r = rpm_rows_reg<2, 4>(ga, args.lda, m, n, args.mp, rp, cp, rowbuf);
   } else if constexpr (shape == 2) {
-    if (lazy && args.invtab) r = rpm_rows_lazy<true, 8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+    if (eager) r = rpm_rows_eager<8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
+                                        reinterpret_cast<int*>(diag));
+    else if (lazy && args.invtab) r = rpm_rows_lazy<true, 8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
                                                            reinterpret_cast<int*>(diag));
     else if (lazy) r = rpm_rows_lazy<false, 8, 4>(ga, args.lda, m, n, args.mp, rp, cp, stab, rowbuf,
                                                   reinterpret_cast<int*>(diag));
@@ -204,12 +210,14 @@ __device__ void rpm_pluq_block(const SmallArgs& args, int blk, int slot) {
   RPM_MARK(4);
   const bool inv = args.invtab != nullptr;
   if constexpr (shape == 1) {
-    if (lazy && inv) lu_lazy<true, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv, simg, t0);
+    if (eager) lu_eager<4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv, simg, t0);
+    else if (lazy && inv) lu_lazy<true, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv, simg, t0);
     else if (lazy) lu_lazy<false, 4, 2>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
     else if (inv) lu_reg<2, 4, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<2, 4, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
   } else if constexpr (shape == 2) {
-    if (lazy && inv) lu_lazy<true, 8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    if (eager) lu_eager<8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
+    else if (lazy && inv) lu_lazy<true, 8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
     else if (lazy) lu_lazy<false, 8, 4>(ga, args.lda, m, n, r, pinv, Q, args.mp, stab, rowbuf, dinv);
     else if (inv) lu_reg<4, 8, true>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);
     else lu_reg<4, 8, false>(ga, args.lda, m, n, r, pinv, Q, args.mp, args.invtab, rowbuf, diag, dinv, dpre);

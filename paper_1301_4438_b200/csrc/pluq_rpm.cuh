@@ -1035,6 +1035,234 @@ __device__ void lu_lazy(uint32_t* ga, int64_t lda, int m, int n, int r, const in
   }
 }
 
+// Eager variants of rpm_rows_lazy / lu_lazy for p < 2^16 (inverse table in shared memory):
+// every element is kept reduced, a <- (a + c w) mod p with one 32-bit product and one
+// Barrett step ((p-1)^2 + p < 2^32).  The per-step chain then has no 64-bit reductions:
+// the pivot column reaches every lane of its row with one 32-bit shuffle and the pivot
+// row is published straight from registers.
+template <int NR, int NQ>
+__device__ __forceinline__ uint32_t re_sel(const uint32_t (&a)[NR][NQ], int t, int q) {
+  uint32_t x[NQ];
+#pragma unroll
+  for (int c = 0; c < NQ; ++c) {
+    x[c] = a[0][c];
+#pragma unroll
+    for (int u = 1; u < NR; ++u) x[c] = t == u ? a[u][c] : x[c];
+  }
+  uint32_t y = x[0];
+#pragma unroll
+  for (int c = 1; c < NQ; ++c) y = q == c ? x[c] : y;
+  return y;
+}
+// column `col` of this warp's NR rows, on every lane (rows k <= lim give 0)
+template <int NR, int NQ>
+__device__ __forceinline__ void re_column(const uint32_t (&a)[NR][NQ], int col, int lim, int m, uint32_t (&cv)[NR]) {
+  const int w = threadIdx.x >> 5, cq = col >> 5, cl = col & 31;
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    uint32_t x = a[t][0];
+#pragma unroll
+    for (int c = 1; c < NQ; ++c) x = cq == c ? a[t][c] : x;
+    const uint32_t v = __shfl_sync(0xffffffffu, x, cl);
+    const int k = w + 16 * t;
+    cv[t] = (k > lim && k < m) ? v : 0u;
+  }
+}
+// S = X - L21 U12 for this thread's elements k >= t0, c >= t0 (X already in a, reduced);
+// rows of L and columns of U are read through rk / cc (the identity for R_A, P / Q for A')
+template <int NR, int NQ>
+__device__ __forceinline__ void re_schur(uint32_t (&a)[NR][NQ], const uint32_t* simg, int t0, const int (&rk)[NR],
+                                         const int (&cc)[NQ], int m, int n, const ModP& mp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long s[NR][NQ];
+#pragma unroll
+  for (int t = 0; t < NR; ++t)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) s[t][q] = 0;
+  for (int kk = 0; kk < t0; ++kk) {
+    uint32_t u[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) u[q] = simg[kk * 64 + cc[q]];
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      const uint32_t l = simg[rk[t] * 64 + kk];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) s[t][q] += (unsigned long long)l * u[q];
+    }
+  }
+  const uint32_t e32 = (uint32_t)((1ull << 32) % mp.p);
+#pragma unroll
+  for (int t = 0; t < NR; ++t)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int k = w + 16 * t, c = lane + 32 * q;
+      if (k >= t0 && c >= t0 && k < m && c < n) {
+        const uint32_t d = rl_red<true>(s[t][q], mp, e32);
+        a[t][q] = a[t][q] >= d ? a[t][q] - d : a[t][q] + (mp.p - d);
+      }
+    }
+}
+
+template <int NR, int NQ>
+__device__ int rpm_rows_eager(const uint32_t* ga, int64_t lda, int m, int n, const ModP mp, int* rp, int* cp,
+                              const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, int* jbuf /* [2] */,
+                              const uint32_t* simg = nullptr, int t0 = 0) {
+  const unsigned FULL = 0xffffffffu;
+  constexpr int WC = 32 * NQ;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (!simg) t0 = 0;
+  uint32_t a[NR][NQ];
+  int rk[NR], cc[NQ];
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + 16 * t;
+    rk[t] = k < m ? k : 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      cc[q] = c < n ? c : 0;
+      a[t][q] = (k < m && c < n && k >= t0 && c >= t0) ? ga[(int64_t)k * lda + c] : 0u;
+    }
+  }
+  if (t0 > 0) re_schur<NR, NQ>(a, simg, t0, rk, cc, m, n, mp);
+  for (int t = tid; t < m; t += blockDim.x) rp[t] = t < t0 ? t : -1;
+  for (int t = tid; t < n; t += blockDim.x) cp[t] = t < t0 ? t : -1;
+  rl_wait_table();
+  __syncthreads();  // table staged, rp/cp initialised
+  auto publish = [&](int i) {
+    if (w != (i & 15)) return;
+    const int ti = i >> 4;
+    uint32_t u[NQ];
+    int j = -1;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      u[q] = re_sel<NR, NQ>(a, ti, q);
+      const unsigned b = __ballot_sync(FULL, u[q] != 0u && lane + 32 * q < n);
+      if (j < 0 && b) j = 32 * q + __ffs(b) - 1;
+    }
+    uint32_t* wb = wbuf + (i & 1) * WC;
+    if (j >= 0) {
+      uint32_t uj = u[0];
+#pragma unroll
+      for (int q = 1; q < NQ; ++q) uj = (j >> 5) == q ? u[q] : uj;
+      const uint32_t iv = stab[__shfl_sync(FULL, uj, j & 31)];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) wb[lane + 32 * q] = u[q] ? reduce32((mp.p - u[q]) * iv, mp) : 0u;
+      if (lane == 0) { rp[i] = j; cp[j] = i; }
+    }
+    if (lane == 0) jbuf[i & 1] = j;
+  };
+  if (t0 < m) publish(t0);
+  int r = t0;
+  for (int i = t0; i < m && r < n; ++i) {
+    __syncthreads();  // row i published
+    const int j = jbuf[i & 1];
+    if (j >= 0) {
+      ++r;
+      uint32_t cv[NR];
+      re_column<NR, NQ>(a, j, i, m, cv);
+      const uint32_t* wb = wbuf + (i & 1) * WC;
+      uint32_t wq[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
+#pragma unroll
+      for (int t = 0; t < NR; ++t)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
+    }
+    if (i + 1 < m && r < n) publish(i + 1);
+  }
+  __syncthreads();
+  return r;
+}
+
+template <int NR, int NQ>
+__device__ void lu_eager(uint32_t* ga, int64_t lda, int m, int n, int r, const int* pinv, const int* Q,
+                         const ModP mp, const uint16_t* stab, uint32_t* wbuf /* [2][32 NQ] */, uint32_t* inv_s,
+                         const uint32_t* simg = nullptr, int t0 = 0) {
+  const unsigned FULL = 0xffffffffu;
+  constexpr int WC = 32 * NQ;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (!simg) t0 = 0;
+  uint32_t a[NR][NQ];
+  int rk[NR], cc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) cc[q] = lane + 32 * q < n ? Q[lane + 32 * q] : 0;
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + 16 * t;
+    rk[t] = k < m ? pinv[k] : 0;
+    const uint32_t* src = ga + (int64_t)rk[t] * lda;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      a[t][q] = (k < m && c < n && k >= t0 && c >= t0) ? src[cc[q]] : 0u;
+    }
+  }
+  if (t0 > 0) {
+    re_schur<NR, NQ>(a, simg, t0, rk, cc, m, n, mp);
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int k = w + 16 * t, c = lane + 32 * q;
+        if (k >= m || c >= n || (k >= t0 && c >= t0)) continue;
+        a[t][q] = (k < t0 && c >= k) ? simg[k * 64 + cc[q]]    // U row k (P fixes k)
+                                     : simg[rk[t] * 64 + c];   // L column c < t0 (scale 1)
+      }
+    for (int c = tid; c < t0; c += blockDim.x) inv_s[c] = 1u;
+  }
+  __syncthreads();  // every original row is in registers before any packed row is written
+  auto publish = [&](int s) {
+    if (w != (s & 15)) return;
+    const int ts = s >> 4;
+    uint32_t u[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) u[q] = re_sel<NR, NQ>(a, ts, q);
+    uint32_t us = u[0];
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) us = (s >> 5) == q ? u[q] : us;
+    const uint32_t d = __shfl_sync(FULL, us, s & 31);
+    if (d == 0u) __trap();  // impossible for A' (leading minors 1..r nonzero)
+    const uint32_t iv = stab[d];
+    uint32_t* wb = wbuf + (s & 1) * WC;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      wb[lane + 32 * q] = (lane + 32 * q > s && u[q]) ? reduce32((mp.p - u[q]) * iv, mp) : 0u;
+    if (lane == 0) inv_s[s] = iv;
+  };
+  if (t0 < r) publish(t0);
+  for (int s = t0; s < r; ++s) {
+    __syncthreads();  // pivot row s published
+    uint32_t cv[NR];
+    re_column<NR, NQ>(a, s, s, m, cv);
+    const uint32_t* wb = wbuf + (s & 1) * WC;
+    uint32_t wq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
+#pragma unroll
+    for (int t = 0; t < NR; ++t)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
+    if (s + 1 < r) publish(s + 1);
+  }
+  __syncthreads();  // inverses of every pivot published
+#pragma unroll
+  for (int t = 0; t < NR; ++t) {
+    const int k = w + 16 * t;
+    if (k >= m) continue;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int c = lane + 32 * q;
+      if (c >= n) continue;
+      uint32_t v = a[t][q];
+      if (c < k && c < r) v = reduce32(v * inv_s[c], mp);
+      else if (k >= r && c >= r) v = 0u;
+      ga[(int64_t)k * lda + c] = v;
+    }
+  }
+}
+
 // Shared-memory words of rpm_pluq_block for an m x n block.
 __host__ __device__ inline int64_t rpm_smem_words(int64_t m, int64_t n) {
   const int64_t mn = m < n ? m : n;

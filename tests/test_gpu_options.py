@@ -32,7 +32,7 @@ def _oracle(a0, p, thr=30):
 
 
 DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 3, "tc_mnb": 1, "par_trsm": 1, "tc_trsm": 1,
-            "pair_leaves": 1, "stream_fb": 4, "fb_prefix": 1, "small_cap": 128 * 128}
+            "pair_leaves": 1, "stream_fb": 4, "fb_prefix": 1, "rpm_eager": 1, "small_cap": 128 * 128}
 
 
 class _opts:
@@ -68,7 +68,8 @@ def _nongeneric_batch(p, n_blocks, seed):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(sym_par=0, rpm_lazy=0), dict(fb_prefix=0), {}])
+@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(sym_par=0, rpm_lazy=0), dict(fb_prefix=0),
+                                  dict(rpm_eager=0), dict(rpm_eager=0, fb_prefix=0), {}])
 @pytest.mark.parametrize("p", [65521, 8388593, 101])
 def test_rank_profile_kernel_variants(pb, opts, p):
     import torch
@@ -88,7 +89,7 @@ def test_rank_profile_kernel_variants(pb, opts, p):
         assert tuple(int(v) for v in counts[b]) == cnt
 
 
-@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(pair_leaves=0), {}])
+@pytest.mark.parametrize("opts", [dict(sym_par=0), dict(rpm_lazy=0), dict(pair_leaves=0), dict(rpm_eager=0), {}])
 @pytest.mark.parametrize("thr", [30, 4])
 def test_cfg4_shaped_leaves(pb, opts, thr):
     """Prescribed rank profiles: the host recursion ends in shape-2 rank-profile leaves."""
