@@ -1167,8 +1167,9 @@ __device__ int rpm_rows_eager(const uint32_t* ga, int64_t lda, int m, int n, con
       for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
 #pragma unroll
       for (int t = 0; t < NR; ++t)
+        if (w + 16 * t > i)  // warp-uniform: rows <= i are done
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
+          for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
     }
     if (i + 1 < m && r < n) publish(i + 1);
   }
@@ -1242,8 +1243,9 @@ __device__ void lu_eager(uint32_t* ga, int64_t lda, int m, int n, int r, const i
     for (int q = 0; q < NQ; ++q) wq[q] = wb[lane + 32 * q];
 #pragma unroll
     for (int t = 0; t < NR; ++t)
+      if (w + 16 * t > s)  // warp-uniform: rows <= s are final
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
+        for (int q = 0; q < NQ; ++q) a[t][q] = reduce32(a[t][q] + cv[t] * wq[q], mp);
     if (s + 1 < r) publish(s + 1);
   }
   __syncthreads();  // inverses of every pivot published
