@@ -105,7 +105,7 @@ struct pluq_ctx {
   int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
-  int64_t host_chunks = 16;        // pipeline depth of the host-buffer batched path
+  int64_t host_chunks = 24;        // pipeline depth of the host-buffer batched path
   int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
   int64_t exact_kernel = 1;        // non-generic blocks: 1 = rank-profile kernel, 0 = recursion
   int64_t trace_pipeline = 0;      // print the host-batch pipeline timeline to stderr
