@@ -213,3 +213,25 @@ def test_streaming_fallback_consumer(pb, stream_fb, prefix):
         assert np.array_equal(res.q_sigma[b].cpu().numpy(), Q), b
         assert np.array_equal(t[b].cpu().numpy(), packed), b
         assert tuple(int(v) for v in counts[b]) == cnt, b
+
+
+def test_prefix_slots_overflow(pb):
+    """More failing blocks than prefix slots (1024): the blocks beyond the pool are
+    factored from scratch by the rank-profile kernel; every block still matches."""
+    import torch
+
+    p = 65521
+    rng = np.random.default_rng(99)
+    nb = 1300
+    batch = rng.integers(0, p, (nb, 64, 64))
+    for b in range(nb):  # every block fails somewhere: zero column c (pivot c is zero)
+        batch[b][:, int(rng.integers(0, 64))] = 0
+    t = torch.from_numpy(batch).cuda().to(torch.int32)
+    res = pb.pluq_batched(t, p, 30)
+    torch.cuda.synchronize()
+    for b in list(range(0, nb, 37)) + list(range(nb - 12, nb)):
+        P, Q, r, packed, _ = _oracle(batch[b], p)
+        assert int(res.ranks[b]) == r, b
+        assert np.array_equal(res.p_sigma[b].cpu().numpy(), P), b
+        assert np.array_equal(res.q_sigma[b].cpu().numpy(), Q), b
+        assert np.array_equal(t[b].cpu().numpy(), packed), b
