@@ -21,6 +21,12 @@
 //      on its pattern) -> P, Q, rank, OpCounts;
 //   c) fraction-free right-looking LU of A' (gathered straight from global memory),
 //      normalised once at the end with all inverses computed in parallel.
+// Register-resident versions of a) and c) (16 warps, rows w + 16 t): lazy 64-bit
+// accumulators (rpm_rows_lazy / lu_lazy) or, for p < 2^16, reduced 32-bit residues
+// (rpm_rows_eager / lu_eager).  Both can resume from a prefix handed over by the 64x64
+// generic kernel: when its t-th leading minor is the first zero one, the first t pivots
+// are (k, k), R_A = diag(I_t, R_S) for the Schur complement S, and the LU of A' starts
+// at step t (the diagonal pivots come first in the quad-recursive order; checked).
 #pragma once
 #include "pluq_small.cuh"
 
