@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
           acc += (uint64_t)ri[kk] * cj[kk * LD];
           acc2 += (uint64_t)ri[kk + 1] * cj[(kk + 1) * LD];
         }
-        for (; kk < kend; ++kk) acc += (uint64_t)ri[kk] * cj[kk * LD];
+        if (kk < kend) acc += (uint64_t)ri[kk] * cj[kk * LD];  // at most one term left
         acc += acc2;  // kFast: <= MN products of (p-1)^2 plus one more term fit in 64 bits
       } else {
         for (; kk < kend; ++kk) acc = reduce64(acc + (uint64_t)ri[kk] * cj[kk * LD], mp);
