@@ -35,10 +35,10 @@ THRESHOLD = 30
 METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
 # dram__bytes_read.sum + dram__bytes_write.sum of the generic kernel per launch from the committed
 # ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
-TRAFFIC = 78_523_392  # 67.27 MB read + 11.26 MB write (profiles/r1/prof_crout_v24_raw.txt)
+TRAFFIC = 78_077_696  # 67.27 MB read + 10.81 MB write (profiles/r1/prof_crout_v25_raw.txt)
 # the generic kernel is issue/latency bound, not HBM bound: ncu --set full of the same kernel
-# (profiles/r1/prof_crout_v24_raw.txt): issue slots busy 63.9 %, IPC 2.55 of 4 per SM
-ISSUE_BUSY, IPC = 0.639, 2.55
+# (profiles/r1/prof_crout_v25_raw.txt): issue slots busy 63.7 %, IPC 2.54 of 4 per SM
+ISSUE_BUSY, IPC = 0.637, 2.54
 UNIT = "Gfield-op/s"
 
 
