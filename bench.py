@@ -1,24 +1,34 @@
 #!/usr/bin/env python
 """Benchmark of the B200 PLUQ-mod-p hot path (contract: one JSON line on rank 0).
 
-Metric (BASELINE.json): effective field-op/s  W / t,  W = 2mnr - (m+n) r^2 + 2 r^3 / 3.
-Headline workload (BASELINE configs[1]): a batch of 4096 independent 64x64 matrices over
-GF(65521) per GPU, entries uniform in [0, p) from a seeded PCG64 stream (synthetic; no
-dataset is involved).  Batches shard by rank with no data-path collective ("weak").
+Metric (BASELINE.json): effective field-op/s  W / t,  W = 2mnr - (m+n) r^2 + 2 r^3 / 3,
+reported at 1/2/4/8 GPUs.
+
+Headline workload (the largest BASELINE config that fits one B200, configs[4]): ONE
+65536 x 65536 matrix over GF(65521) of rank 32768, A = X Y mod p with X, Y uniform from
+the SURVEY §8(d) PCG64 stream (seed 0) and random row/column permutations (synthetic; no
+dataset is involved).  At N > 1 GPUs the same matrix is factored by `pluq_distributed`
+on a 2D process grid (1x2, 2x2, 2x4): total work is fixed ("strong").  cfg1-cfg4 are
+reported as nested objects (`configs`), each with its own steps, per-step times and clocks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg5|cfg4|cfg3|cfg2|cfg1] [--no-secondary] [--no-cpu]
 
---impl reference times the reference algorithm's CPU implementation (the oracle port
-of /root/reference/pkg/src/pluq, numpy + OpenBLAS, all host cores via a process pool)
-on a bounded sample of the same workload.
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks (one process per GPU) and fails loudly if fewer GPUs are visible.
+--impl reference times the reference algorithm's CPU implementation (the oracle port of
+/root/reference/pkg/src/pluq, numpy + OpenBLAS on every host core) on a bounded sample of
+the same workload family.
 """
 
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -28,48 +38,55 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-P = 65521
-M = N = 64
-BATCH = 4096
-THRESHOLD = 30
 METRIC = "PLUQ mod p effective Gfield-op/s, (2mnr-(m+n)r^2+2r^3/3)/t"
-# dram__bytes_read.sum + dram__bytes_write.sum of the generic kernel per launch from the committed
-# ncu --set full capture (profiles/r1/NOTES.md); None until captured for the current kernel
-TRAFFIC = 78_077_696  # 67.27 MB read + 10.81 MB write (profiles/r1/prof_crout_v25_raw.txt)
-# the generic kernel is issue/latency bound, not HBM bound: ncu --set full of the same kernel
-# (profiles/r1/prof_crout_v25_raw.txt): issue slots busy 63.7 %, IPC 2.54 of 4 per SM
-ISSUE_BUSY, IPC = 0.637, 2.54
 UNIT = "Gfield-op/s"
+THRESHOLD = 30
+
+# BASELINE.json configs (SURVEY §8(d) generators, seed 0)
+CONFIGS = {
+    "cfg1": dict(kind="xy", m=512, n=512, r=384, p=65521,
+                 desc="cfg1: one 512x512 matrix over GF(65521), rank 384 (X Y, permuted)"),
+    "cfg2": dict(kind="batch", batch=4096, m=64, n=64, p=65521,
+                 desc="cfg2: batch of 4096 independent 64x64 matrices over GF(65521) per GPU"),
+    "cfg3": dict(kind="uniform", m=8192, n=8192, p=65521, desc="cfg3: one 8192x8192 matrix over GF(65521), uniform"),
+    "cfg4": dict(kind="profile", m=16384, n=32768, r=8192, p=8388593,
+                 desc="cfg4: one 16384x32768 matrix over GF(8388593), rank 8192, prescribed rank profiles"),
+    "cfg5": dict(kind="xy", m=65536, n=65536, r=32768, p=65521,
+                 desc="cfg5: one 65536x65536 matrix over GF(65521), rank 32768 (X Y, permuted)"),
+}
+HEADLINE = "cfg5"
+GRIDS = {1: None, 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel
+# (tc_modgemm_kernel<2,1,1> at the cfg5 trailing-update shape) from the committed
+# ncu --set full capture (profiles/r2/NOTES.md); None until captured
+TRAFFIC = None
+TRAFFIC_SHAPE = None
 
 
 def work(m, n, r):
     return 2.0 * m * n * r - (m + n) * float(r) ** 2 + 2.0 * float(r) ** 3 / 3.0
 
 
+def limbs(p):
+    return 1 if p - 1 < 256 else (int(p - 1).bit_length() + 7) // 8
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
-
-
-def config_dict(n_gpus):
-    return {
-        "workload": f"cfg2: batch of {BATCH} independent {M}x{N} matrices over GF({P}) per GPU, threshold {THRESHOLD}",
-        "batch_per_gpu": BATCH, "global_batch": BATCH * n_gpus, "m": M, "n": N, "p": P,
-        "threshold": THRESHOLD, "parallelism": f"batch-sharded x{n_gpus}",
-        "l2": "inputs (67 MB int32) < L2: a 512 MB buffer is written between timed steps (L2 flush)",
-    }
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------------------------------
-# clocks sampled during the timed region (NVML)
+# clocks sampled during a timed region (NVML)
 # ---------------------------------------------------------------------------------------
 class ClockSampler:
     REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
         0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
         0x100: "display_clock_setting",
     }
@@ -93,7 +110,7 @@ class ClockSampler:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
-                    if mask & bit and bit != 0x1:
+                    if mask & bit:
                         self.reasons.add(name)
             except Exception:
                 pass
@@ -103,8 +120,6 @@ class ClockSampler:
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-            # let the sampler's first NVML queries finish before the timed region starts
-            # (they would otherwise delay the host thread's first timed launches)
             t0 = time.perf_counter()
             while len(self.samples) < 2 and time.perf_counter() - t0 < 0.5:
                 time.sleep(0.002)
@@ -116,106 +131,293 @@ class ClockSampler:
             self.t.join()
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        med = float(statistics.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
 
 
 # ---------------------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference algorithm; test infrastructure)
+# CPU side: the oracle port of the reference (test infrastructure; only these legs use it)
 # ---------------------------------------------------------------------------------------
-def _cpu_worker(args):
-    seed, count = args
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+CPU_SAMPLE = dict(m=4096, n=4096, r=2048, p=65521)  # cfg5's construction, bounded to a few s
+
+
+def _cpu_sample_once(seed=0):
     from oracle import pluq_oracle as orc
 
-    batch = orc.gen_cfg2(seed=seed, batch=count)
-    w = 0.0
+    s = CPU_SAMPLE
+    a = orc.gen_xy_rank(s["m"], s["n"], s["r"], s["p"], seed).astype(np.float64)
     t0 = time.perf_counter()
-    for b in range(count):
-        x = batch[b].astype(np.float64)
-        _, _, r, _ = orc.pluq(x, P, THRESHOLD)
-        w += work(M, N, r)
-    return w, time.perf_counter() - t0
+    _, _, r, _ = orc.pluq(a, s["p"], THRESHOLD)
+    return work(s["m"], s["n"], r), time.perf_counter() - t0
 
 
-def cpu_reference_step(pool, workers, per_worker, seed):
-    t0 = time.perf_counter()
-    res = list(pool.map(_cpu_worker, [(seed * 1000 + i, per_worker) for i in range(workers)]))
-    dt = time.perf_counter() - t0
-    return sum(r[0] for r in res), dt
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([i.get("num_threads", 1) for i in threadpool_info() if i.get("internal_api") == "openblas"] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline_leg(min_seconds=10.0):
+    """The oracle on this host's cores (OpenBLAS threads = all cores) on cfg5's generator at
+    a bounded size, repeated until ~min_seconds of CPU work."""
+    ws, ts = [], []
+    while sum(ts) < min_seconds and len(ts) < 8:
+        w, t = _cpu_sample_once(len(ts))
+        ws.append(w)
+        ts.append(t)
+    s = CPU_SAMPLE
+    return {"value": sum(ws) / sum(ts) / 1e9, "unit": UNIT, "cores": int(_blas_threads()), "kind": "port",
+            "sample": f"{len(ts)} x oracle pluq of cfg5's construction at {s['m']}x{s['n']} rank {s['r']} "
+                      f"(GF({s['p']}), seeds 0..{len(ts) - 1}; {sum(ts):.1f} s); cfg5 itself needs > 96 GiB "
+                      f"host RAM and hours on the CPU (BASELINE.md)"}
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: rank 0 times the oracle port on every host core; others exit."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import multiprocessing as mp
-
-    workers = os.cpu_count() or 1
-    per_worker = max(2, 256 // workers)
-    ctx = mp.get_context("fork")
-    with ctx.Pool(workers, initializer=os.environ.__setitem__, initargs=("OPENBLAS_NUM_THREADS", "1")) as pool:
-        for w in range(args.warmup):
-            cpu_reference_step(pool, workers, per_worker, 100 + w)
-        ws, ts = [], []
-        for s in range(args.steps):
-            w, dt = cpu_reference_step(pool, workers, per_worker, s)
-            ws.append(w)
-            ts.append(dt)
+    for w in range(args.warmup):
+        _cpu_sample_once(100 + w)
+    ws, ts = [], []
+    for s in range(args.steps):
+        w, t = _cpu_sample_once(s)
+        ws.append(w)
+        ts.append(t)
     value = sum(ws) / sum(ts) / 1e9
-    sample = f"{workers * per_worker} cfg2 matrices ({M}x{N}, GF({P})) per step, {workers} processes"
+    cs = CPU_SAMPLE
+    sample = (f"per step: oracle pluq of cfg5's construction (X Y mod p, permuted) at {cs['m']}x{cs['n']} rank "
+              f"{cs['r']}, GF({cs['p']}), threshold {THRESHOLD}; the full 65536^2 cfg5 does not fit the host")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PCG64)",
-        "config": config_dict(args.gpus), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8(d) PCG64 stream)",
+        "config": config_dict(args.config, args.gpus), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(_blas_threads()), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_leg(seconds=12.0):
-    """Oracle on this host: single process (the reference decomposes one matrix at a time,
-    SPEC.md:343-344), bounded to ~`seconds` of work."""
-    from oracle import pluq_oracle as orc
-
-    batch = orc.gen_cfg2(seed=999, batch=4096)
-    w, n_done = 0.0, 0
-    t0 = time.perf_counter()
-    while n_done < 4096 and (time.perf_counter() - t0) < seconds:
-        x = batch[n_done].astype(np.float64)
-        _, _, r, _ = orc.pluq(x, P, THRESHOLD)
-        w += work(M, N, r)
-        n_done += 1
-    dt = time.perf_counter() - t0
-    try:
-        from threadpoolctl import threadpool_info
-
-        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("internal_api") == "openblas"] or [1])
-    except Exception:
-        cores = 1
-    return {"value": w / dt / 1e9, "unit": UNIT, "cores": int(cores), "kind": "port",
-            "sample": f"{n_done} cfg2 matrices factored one after another by the numpy oracle ({dt:.1f} s)"}
+def config_dict(name, n_gpus):
+    c = CONFIGS[name]
+    d = {"workload": c["desc"] + ", threshold 30, seed 0 (SURVEY §8(d) PCG64 stream)", "p": c["p"],
+         "m": c["m"], "n": c["n"], "threshold": THRESHOLD}
+    if "r" in c:
+        d["rank"] = c["r"]
+    if c["kind"] == "batch":
+        d.update(batch_per_gpu=c["batch"], global_batch=c["batch"] * n_gpus, parallelism=f"batch-sharded x{n_gpus}",
+                 l2="inputs (67 MB int32) < L2: a 512 MB buffer is written between timed steps (L2 flush)")
+    else:
+        grid = GRIDS.get(n_gpus)
+        d["parallelism"] = "single GPU" if grid is None else f"2D grid {grid[0]}x{grid[1]} (pluq_distributed)"
+        d["l2"] = (f"input {c['m'] * c['n'] * 4 / 2**30:.2f} GiB int32 "
+                   + ("> L2 (126 MB): no flush needed" if c["m"] * c["n"] * 4 > 126e6 else
+                      "< L2: a 512 MB buffer is written between timed steps (L2 flush)"))
+    return d
 
 
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
+def gen_device(name, dev, seed=0):
+    from paper_1301_4438_b200 import gen
+
+    c = CONFIGS[name]
+    if c["kind"] == "xy":
+        return gen.gen_xy_rank_device(c["m"], c["n"], c["r"], c["p"], seed=seed, device=dev), None
+    if c["kind"] == "uniform":
+        return gen.gen_cfg3_device(seed=seed, n=c["m"], p=c["p"], device=dev), None
+    if c["kind"] == "profile":
+        a, rows, cols = gen.gen_cfg4_device(c["m"], c["n"], c["r"], c["p"], seed=seed, device=dev)
+        return a, (rows, cols)
+    return gen.gen_cfg2_device(seed=seed, batch=c["batch"], m=c["m"], n=c["n"], p=c["p"], device=dev), None
+
+
+def time_single(pb, name, a0, dev, steps, warmup, world=1, grid=None, with_clocks=True):
+    """Device-resident factorizations of one matrix: per-step CUDA events around pluq()."""
+    import torch
+    import torch.distributed as dist
+
+    c = CONFIGS[name]
+    p = c["p"]
+    field = pb.PrimeField(p)
+    rank = dist.get_rank() if world > 1 else 0
+    buf = torch.empty_like(a0) if a0 is not None else None
+    dm = pb.DenseMatrix(field, buf.copy_(a0)) if buf is not None else None
+    small = c["m"] * c["n"] * 4 < 126e6
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if small else None
+
+    def step():
+        if world > 1:
+            return pb.pluq_distributed(dm, c["m"], c["n"], p, THRESHOLD, grid=grid)
+        return pb.pluq(dm, THRESHOLD)
+
+    def restore(s):
+        if buf is not None:
+            buf.copy_(a0)
+        if flush is not None:
+            flush.fill_(s & 255)
+
+    for w in range(max(warmup, 3)):
+        restore(w)
+        step()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    sampler = ClockSampler(dev.index) if with_clocks else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        wall0 = time.perf_counter()
+        for s in range(steps):
+            restore(s)
+            ev[s][0].record(stream)
+            f = step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    finally:
+        if sampler:
+            sampler.__exit__()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    r = f.rank if hasattr(f, "rank") else int(f)
+    launches = pb.last_stats()["launches"] if rank == 0 else 0
+    return dict(step_ms=step_ms, rank=r, factors=f if rank == 0 else None, wall=wall,
+                clocks=sampler.summary() if sampler else None, launches=launches, stats=pb.last_stats(), buf=buf)
+
+
+def roofline_step(pb, name, a0, int8_peak):
+    """One extra, untimed factorization with the library's per-launch CUDA events on the
+    tensor-core GEMM (option tc_time): achieved int8 TOP/s of the dominant kernel =
+    summed algorithmic int8 ops (2 m n k L^2 per launch) / summed launch durations."""
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    c = CONFIGS[name]
+    ctx = _native.context(a0.device.index)
+    x = a0.clone()
+    ctx.set_option("tc_time", 1)
+    try:
+        pb.pluq(pb.DenseMatrix(pb.PrimeField(c["p"]), x), THRESHOLD)
+        torch.cuda.synchronize()
+        st = pb.last_stats()
+    finally:
+        ctx.set_option("tc_time", 0)
+    del x
+    n_l = max(1, st["tc_timed_launches"])
+    t_avg = st["tc_timed_ns"] / 1e9 / n_l
+    ops_avg = st["tc_timed_int8_ops"] / n_l
+    achieved = ops_avg / t_avg / 1e12 if t_avg > 0 else 0.0
+    return {"bound": "tensor", "kernel": f"tc_modgemm_kernel<{limbs(c['p'])},1,{int(limbs(c['p']) == 2)}> "
+                                         "(tcgen05.mma kind::i8 limb GEMM, C <- C - A B mod p)",
+            "achieved": achieved, "peak": int8_peak, "unit": "TOP/s (int8)", "frac": achieved / int8_peak,
+            "traffic": TRAFFIC, "traffic_shape": TRAFFIC_SHAPE,
+            "launches_per_step": st["tc_timed_launches"], "avg_launch_ms": t_avg * 1e3,
+            "avg_int8_ops_per_launch": ops_avg,
+            "gemm_share_of_step": None,
+            "peak_kind": "measured on this B200 (pluq_measure_peaks: back-to-back tcgen05.mma.kind::i8 "
+                         "128x256x32, one CTA per SM); MEASURED_PEAKS.json has no int8 entry",
+            "note": "achieved = algorithmic int8 ops per launch (2 m n k L^2, L = limbs of p) / average launch "
+                    "duration, CUDA events on the launching stream during one extra factorization"}
+
+
+def e2e_single(pb, name, host_pristine, steps, warmup):
+    """The public API on HOST buffers in the reference's dtype (float64 for p=65521):
+    pluq(DenseMatrix(field, numpy)) copies in, factors and writes back into the array."""
+    c = CONFIGS[name]
+    field = pb.PrimeField(c["p"])
+    host = np.empty_like(host_pristine)
+    pool = cf.ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1)))
+    rows = host.shape[0]
+    parts = np.array_split(np.arange(rows), max(1, min(64, rows)))
+
+    def restore():  # parallel host copy (outside the timed region)
+        list(pool.map(lambda ix: np.copyto(host[ix[0]:ix[-1] + 1], host_pristine[ix[0]:ix[-1] + 1]),
+                      [ix for ix in parts if len(ix)]))
+
+    restore()
+    dm = pb.DenseMatrix(field, host)  # validated once (field.asarray); refilled in place per step
+    ts = []
+    for s in range(warmup + steps):
+        if s:
+            restore()
+        t0 = time.perf_counter()
+        f = pb.pluq(dm, THRESHOLD)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            ts.append(dt)
+    pool.shutdown()
+    return ts, f.rank, host.nbytes
+
+
+def measure_peaks_live(dev):
+    from paper_1301_4438_b200 import _native
+
+    ctx = _native.context(dev.index)
+    return max((ctx.measure_peaks() for _ in range(3)), key=lambda d: d["int8_tops"])
+
+
+def launch_ranks(args):
+    """--gpus N outside torchrun: one process per GPU via torch.distributed.run (127.0.0.1)."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and not os.environ.get("PLUQ_BENCH_ALLOW_CPU_RANKS"):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {have} visible\n")
+        sys.exit(1)
+    port = os.environ.get("PLUQ_BENCH_PORT", str(29500 + (os.getpid() % 1000)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))))
+
+
+def selftest_ranks(args):
+    """Plumbing check of the multi-rank bench without GPUs (gloo): launcher, barrier and the
+    max-over-ranks / summed-work reduction; prints the contract line with n_gpus = world."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist.init_process_group("gloo")
+    rank = dist.get_rank()
+    dist.barrier()
+    t = torch.tensor([0.01 * (rank + 1), 1.0e9], dtype=torch.float64)
+    dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+    dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": float(t[1] / t[0] / 1e9), "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "selftest": True}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--selftest-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    if args.selftest_ranks:
+        return selftest_ranks(args)
 
     import torch
     import torch.distributed as dist
@@ -223,246 +425,278 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(1)
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        sys.stderr.write("bench.py: no CUDA device for this rank\n")
+        sys.exit(1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        if world not in GRIDS:
+            raise SystemExit(f"no process grid for {world} ranks")
 
     import paper_1301_4438_b200 as pb
 
-    # seeded synthetic cfg2 batch (PCG64, uniform in [0, p)); the oracle is not used here
-    host = np.random.default_rng(rank).integers(0, P, (BATCH, M, N), dtype=np.int64)
-    pristine = torch.from_numpy(host).to(dev).to(torch.int32)
-    work_buf = torch.empty_like(pristine)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        return pb.pluq_batched(work_buf, P, THRESHOLD)
-
-    for w_ in range(max(args.warmup, 3)):  # same sequence as a timed step (copy, L2 flush, step)
-        work_buf.copy_(pristine)
-        flush.fill_(w_ & 255)
-        step()
-    torch.cuda.synchronize(dev)
-
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ranks_total = 0
-    hbm, bf16, peak_kind = peaks()
-    with ClockSampler(local) as clocks:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        wall0 = time.perf_counter()
-        for s in range(args.steps):
-            work_buf.copy_(pristine)
-            flush.fill_(s & 255)           # evict the batch from L2 between timed steps
-            starts[s].record(stream)
-            res = step()
-            ends[s].record(stream)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-        wall = time.perf_counter() - wall0
-        step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
-        if os.environ.get("PLUQ_BENCH_STEPS"):
-            print("step_ms", " ".join(f"{v:.3f}" for v in step_ms), file=sys.stderr)
-        ranks = res.ranks.to(torch.int64).cpu().numpy()
-        w_step = float(sum(work(M, N, int(r)) for r in ranks))
-        # per-kernel device times of one extra (untimed) step, CUDA events inside the library
-        from paper_1301_4438_b200 import _native
-
-        kctx = _native.context(local)
-        kctx.set_option("time_kernels", 1)
-        work_buf.copy_(pristine)
-        flush.fill_(7)
-        step()
-        kst = kctx.stats()
-        kctx.set_option("time_kernels", 0)
-
-        # ---- e2e through the public API with pinned host buffers (H2D + D2H inside) ----
-        pinned = torch.empty((BATCH, M, N), dtype=torch.float64, pin_memory=True)
-        host_f64 = host.astype(np.float64)
-        pin_np = pinned.numpy()
-        for _ in range(2):
-            pin_np[...] = host_f64
-            pb.pluq_batched(pin_np, P, THRESHOLD)
-        e2e_t = []
-        for s in range(max(3, args.steps // 2)):
-            pin_np[...] = host_f64
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            r2 = pb.pluq_batched(pin_np, P, THRESHOLD)
-            e2e_t.append(time.perf_counter() - t0)
-        w_e2e = float(sum(work(M, N, int(r)) for r in r2.ranks))
-        if os.environ.get("PLUQ_BENCH_STEPS"):
-            print("e2e_ms", " ".join(f"{1e3 * v:.3f}" for v in e2e_t), file=sys.stderr)
-
-    from paper_1301_4438_b200.sharding import reduce_timing
-
-    t_dev, w_all = reduce_timing(sum(step_ms) / 1e3, w_step, dev)        # max time, summed work
-    t_e2e, w_e2e_all = reduce_timing(sum(e2e_t), w_e2e, dev)
-    value = w_all * args.steps / t_dev / 1e9
-    e2e_value = w_e2e_all * len(e2e_t) / t_e2e / 1e9
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    avg_launch = t_dev / args.steps
-    t_gen = kst["t_generic_ns"] / 1e9 if kst["t_generic_ns"] > 0 else avg_launch
-    alg_bytes = BATCH * M * N * 4 * 2 + BATCH * (M + N + 1) * 4
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded PCG64, uniform in [0,p))",
-        "config": config_dict(world),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": BATCH * M * N * 8,
-                "d2h_bytes_per_step": BATCH * M * N * 8 + BATCH * (M + N + 1) * 8,
-                "path": "pluq_batched(pinned float64 numpy batch) -> C ABI pluq_factor_batched_host_f64",
-                "ms_per_step": 1e3 * t_e2e / len(e2e_t)},
-        "gpu_launches": args.steps * int(kst["launches"]),
-        "roofline": {"bound": "hbm", "kernel": "crout_fixed_kernel<64,64,128>", "achieved": alg_bytes / t_gen / 1e9,
-                     "peak": hbm, "unit": "GB/s", "frac": alg_bytes / t_gen / 1e9 / hbm, "traffic": TRAFFIC,
-                     "traffic_unit": "bytes per launch (ncu --set full, dram read+write; output writes partly still in L2)",
-                     "issue_slots_busy": ISSUE_BUSY, "ipc_of_4": IPC,
-                     "alg_bytes": alg_bytes,
-                     "peak_kind": peak_kind, "kernel_ms": t_gen * 1e3,
-                     "fallback_kernel_ms": kst["t_fallback_ns"] / 1e6,
-                     "note": "algorithmic bytes = read+write of 4096 int32 64x64 blocks + P/Q/rank; the "
-                             "generic-profile Crout kernel is latency/issue bound (64-pivot chain per matrix); "
-                             "rpm_pluq_kernel finishes the few non-generic matrices (rank-profile route); see DESIGN.md"},
-        "clocks": clocks.summary(),
-        "wall_s_timed_region": wall,
-    }
-    if not args.no_cpu and world == 1:
-        line["cpu_baseline"] = cpu_baseline_leg()
-    if not args.no_secondary and world == 1:
-        line["secondary"] = secondary(pb, dev, hbm, bf16, peak_kind)
-    print(json.dumps(line), flush=True)
+    name = args.config
+    c = CONFIGS[name]
+    if c["kind"] == "batch":
+        line = bench_batch(pb, args, dev, world, rank)
+    else:
+        line = bench_single(pb, name, args, dev, world, rank)
+    if rank == 0:
+        if not args.no_secondary and world == 1:
+            line["configs"] = secondary(pb, dev, name)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def secondary(pb, dev, hbm, bf16, peak_kind):
-    """The modular GEMM's tensor roofline, cfg3 (8192^2), cfg1, and cfg4/cfg5 at full size."""
+def bench_single(pb, name, args, dev, world, rank):
+    import torch
+
+    from paper_1301_4438_b200.sharding import reduce_timing
+
+    c = CONFIGS[name]
+    grid = GRIDS.get(world)
+    t_gen0 = time.perf_counter()
+    a0, extra = gen_device(name, dev) if rank == 0 else (None, None)
+    t_gen = time.perf_counter() - t_gen0
+    res = time_single(pb, name, a0, dev, args.steps, max(args.warmup, 3), world, grid)
+    t_dev, w_all = reduce_timing(sum(res["step_ms"]) / 1e3, work(c["m"], c["n"], res["rank"]) if rank == 0 else 0.0,
+                                 dev)
+    value = w_all * args.steps / t_dev / 1e9
+    line = None
+    if rank == 0:
+        f = res["factors"]
+        from paper_1301_4438_b200 import verify
+
+        checks = {"structure": bool(verify.structure_ok(f))}
+        del res["buf"]
+        torch.cuda.empty_cache()
+        checks["freivalds"] = bool(verify.freivalds(a0, f, probes=2))
+        if extra is not None:
+            checks["row_profile"] = pb.row_rank_profile(f) == tuple(int(v) for v in extra[0])
+            checks["col_profile"] = pb.col_rank_profile(f) == tuple(int(v) for v in extra[1])
+        del f, res["factors"]
+        pk = measure_peaks_live(dev)
+        int8_peak = pk["int8_tops"]
+        L = limbs(c["p"])
+        roof = roofline_step(pb, name, a0, int8_peak) if world == 1 else None
+        if roof is not None:
+            roof["gemm_share_of_step"] = None  # from the ncu launch list (profiles/), not measurable here
+        ms = 1e3 * t_dev / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 residues (u8-limb int8 tensor-core GEMM, int32/64 accumulation)",
+            "data": "synthetic (SURVEY §8(d) PCG64 stream, seed 0; generated in %.1f s)" % t_gen,
+            "config": config_dict(name, world),
+            "rank": res["rank"], "checks": checks,
+            "step_ms": [round(v, 4) for v in res["step_ms"]],
+            "median_ms": statistics.median(res["step_ms"]),
+            "gpu_launches": int(res["launches"]) * args.steps,
+            "roofline": roof,
+            "whole_pluq_roofline": {"bound": "tensor", "achieved": value, "unit": UNIT,
+                                    "peak": int8_peak * 1e3 / (L * L), "frac": value / (int8_peak * 1e3 / (L * L)),
+                                    "note": f"a field MAC is L^2 = {L * L} int8 MACs on the limb path: "
+                                            "field-op/s ceiling = int8 peak / L^2"},
+            "measured_peaks": {"int8_tcgen05_tops": int8_peak, "fp64_dmma_tflops": pk["fp64_tflops"]},
+            "clocks": res["clocks"], "wall_s_timed_region": res["wall"],
+            "driver_stats": {k: v for k, v in res["stats"].items() if not k.startswith("t_") and "timed" not in k},
+        }
+    # ---- e2e: the public API on host buffers (H2D and D2H inside every step) ----
+    if world == 1:
+        host = a0.cpu().numpy().astype(np.float64)
+        del a0
+        torch.cuda.empty_cache()
+        ts, r2, nbytes = e2e_single(pb, name, host, max(1, args.e2e_steps), 1)
+        del host
+        e2e_value = work(c["m"], c["n"], r2) * len(ts) / sum(ts) / 1e9
+        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                       "path": "pluq(DenseMatrix(PrimeField(p), float64 numpy)) -> C ABI pluq_factor_host_f64",
+                       "steps": len(ts), "ms_per_step": 1e3 * sum(ts) / len(ts),
+                       "step_ms": [round(1e3 * v, 2) for v in ts]}
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline_leg()
+    elif rank == 0:
+        line["e2e"] = None
+    return line
+
+
+def bench_batch(pb, args, dev, world, rank):
+    """cfg2 as the measured workload (batch-sharded across ranks, no data-path collective)."""
+    from paper_1301_4438_b200 import gen
+    from paper_1301_4438_b200.sharding import reduce_timing
+
+    c = CONFIGS["cfg2"]
+    res = time_batch(pb, gen.gen_cfg2_device(seed=rank, device=dev), dev, args.steps, max(args.warmup, 3), world)
+    t_dev, w_all = reduce_timing(sum(res["step_ms"]) / 1e3, res["work"], dev)
+    e2e_ts, w_e2e = e2e_batch(pb, seed=rank, steps=max(3, args.steps // 2), world=world)
+    t_e2e, w_e2e_all = reduce_timing(sum(e2e_ts), w_e2e, dev)
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": w_all * args.steps / t_dev / 1e9, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": 1e3 * t_dev / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (SURVEY §8(d) PCG64 stream, seed = rank)", "config": config_dict("cfg2", world),
+        "step_ms": [round(v, 4) for v in res["step_ms"]], "clocks": res["clocks"],
+        "gpu_launches": res["launches"] * args.steps,
+        "e2e": {"value": w_e2e_all * len(e2e_ts) / t_e2e / 1e9, "unit": UNIT,
+                "h2d_bytes_per_step": c["batch"] * c["m"] * c["n"] * 8,
+                "d2h_bytes_per_step": c["batch"] * c["m"] * c["n"] * 8 + c["batch"] * (c["m"] + c["n"] + 1) * 8,
+                "path": "pluq_batched(float64 numpy batch) -> C ABI pluq_factor_batched_host_f64"},
+    }
+    if not args.no_cpu and world == 1:
+        line["cpu_baseline"] = cpu_baseline_leg()
+    return line
+
+
+def time_batch(pb, t0, dev, steps, warmup, world=1, with_clocks=True):
+    import torch
+    import torch.distributed as dist
+
+    c = CONFIGS["cfg2"]
+    buf = torch.empty_like(t0)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for w in range(warmup):
+        buf.copy_(t0)
+        flush.fill_(w & 255)
+        pb.pluq_batched(buf, c["p"], THRESHOLD)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    sampler = ClockSampler(dev.index) if with_clocks else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for s in range(steps):
+            buf.copy_(t0)
+            flush.fill_(s & 255)
+            ev[s][0].record(stream)
+            res = pb.pluq_batched(buf, c["p"], THRESHOLD)
+            ev[s][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    finally:
+        if sampler:
+            sampler.__exit__()
+    ranks = res.ranks.to(torch.int64).cpu().numpy()
+    return dict(step_ms=[a.elapsed_time(b) for a, b in ev], work=float(sum(work(c["m"], c["n"], int(r)) for r in ranks)),
+                clocks=sampler.summary() if sampler else None, launches=int(pb.last_stats()["launches"]))
+
+
+def e2e_batch(pb, seed, steps, world):
+    import torch
+    import torch.distributed as dist
+
+    c = CONFIGS["cfg2"]
+    host = np.random.default_rng(seed).integers(0, c["p"], (c["batch"], c["m"], c["n"])).astype(np.float64)
+    buf = np.empty_like(host)
+    for _ in range(2):
+        np.copyto(buf, host)
+        pb.pluq_batched(buf, c["p"], THRESHOLD)
+    ts = []
+    for _ in range(steps):
+        np.copyto(buf, host)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = pb.pluq_batched(buf, c["p"], THRESHOLD)
+        ts.append(time.perf_counter() - t0)
+    return ts, float(sum(work(c["m"], c["n"], int(v)) for v in r.ranks))
+
+
+def secondary(pb, dev, headline):
+    """The other BASELINE configs at full size on this GPU, each with its own timed steps,
+    clocks and checks, plus the modular GEMM at the LU's trailing-update shape."""
+    import torch
+
+    from paper_1301_4438_b200 import verify
+
+    out = {}
+    plan = {"cfg1": (10, 3), "cfg2": (20, 5), "cfg3": (10, 3), "cfg4": (3, 1), "cfg5": (3, 1)}
+    for name, (steps, warm) in plan.items():
+        if name == headline:
+            continue
+        c = CONFIGS[name]
+        try:
+            if c["kind"] == "batch":
+                from paper_1301_4438_b200 import gen
+
+                r = time_batch(pb, gen.gen_cfg2_device(seed=0, device=dev), dev, steps, warm)
+                ms = sum(r["step_ms"]) / steps
+                out[name] = {"value": r["work"] / (ms / 1e3) / 1e9, "unit": UNIT, "steps": steps,
+                             "ms_per_step": ms, "step_ms": [round(v, 4) for v in r["step_ms"]],
+                             "clocks": r["clocks"], "gpu_launches_per_step": r["launches"]}
+                ts, w = e2e_batch(pb, 0, 5, 1)
+                out[name]["e2e"] = {"value": w * len(ts) / sum(ts) / 1e9, "unit": UNIT,
+                                    "ms_per_step": 1e3 * sum(ts) / len(ts)}
+                continue
+            a0, extra = gen_device(name, dev)
+            r = time_single(pb, name, a0, dev, steps, warm)
+            f = r["factors"]
+            checks = {"structure": bool(verify.structure_ok(f)), "freivalds": bool(verify.freivalds(a0, f, probes=2))}
+            if extra is not None:
+                checks["row_profile"] = pb.row_rank_profile(f) == tuple(int(v) for v in extra[0])
+                checks["col_profile"] = pb.col_rank_profile(f) == tuple(int(v) for v in extra[1])
+            ms = sum(r["step_ms"]) / steps
+            val = work(c["m"], c["n"], r["rank"]) / (ms / 1e3) / 1e9
+            L = limbs(c["p"])
+            out[name] = {"value": val, "unit": UNIT, "rank": r["rank"], "steps": steps, "ms_per_step": ms,
+                         "step_ms": [round(v, 4) for v in r["step_ms"]], "clocks": r["clocks"], "checks": checks,
+                         "gpu_launches_per_step": r["launches"],
+                         "driver_stats": {k: v for k, v in r["stats"].items() if not k.startswith("t_")
+                                          and "timed" not in k}}
+            if name in ("cfg3", "cfg4", "cfg5"):
+                pk = measure_peaks_live(dev)["int8_tops"]
+                out[name]["frac_of_tensor_roofline"] = val * 1e9 / (pk * 1e12 / (L * L))
+            del a0, f, r
+            torch.cuda.empty_cache()
+        except Exception as e:  # a secondary config must not kill the headline line
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+    out["modgemm"] = modgemm_lines(dev)
+    return out
+
+
+def modgemm_lines(dev):
+    """The dominant kernel alone at the LU's own shapes (CUDA events, 10 reps after 3)."""
     import torch
     from paper_1301_4438_b200 import _native
 
-    out = {}
-    # --- modular GEMM, top-level cfg3 shape (4096^3, p=65521 -> 2 limbs, 4 int8 MMAs per product)
-    m = n = k = 4096
-    g = torch.Generator(device="cpu").manual_seed(0)
-    A = torch.randint(0, P, (m, k), generator=g, dtype=torch.int32).to(dev)
-    B = torch.randint(0, P, (k, n), generator=g, dtype=torch.int32).to(dev)
-    C = torch.randint(0, P, (m, n), generator=g, dtype=torch.int32).to(dev)
     ctx = _native.context(dev.index)
-    for _ in range(3):
-        ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, P)
-    torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    ev0.record()
-    for _ in range(reps):
-        st = ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, P)
-    ev1.record()
-    torch.cuda.synchronize(dev)
-    _native.raise_for(st, ctx, "tc gemm")
-    t = ev0.elapsed_time(ev1) / 1e3 / reps
-    ctx.set_option("tc_time", 1)  # one extra call: the MMA kernel alone, without the limb split
-    ctx.lib.pluq_modgemm_sub_tc(ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, P)
-    t_mma = ctx.stats()["t_tc_mma_ns"] / 1e9
-    ctx.set_option("tc_time", 0)
-    limbs = 2
-    # SURVEY §8d: the int8 (tcgen05 kind::i8) and FP64 peaks are microbenchmarked on this box
-    pk = max((ctx.measure_peaks() for _ in range(3)), key=lambda d: d["int8_tops"])
-    int8_peak = pk["int8_tops"]
-    achieved = 2.0 * m * n * k * limbs * limbs / t / 1e12
-    out["measured_peaks"] = {"int8_tcgen05_tops": int8_peak, "fp64_dmma_tflops": pk["fp64_tflops"],
-                             "how": "pluq_measure_peaks: back-to-back tcgen05.mma.kind::i8 128x256x32 per SM; "
-                                    "mma.sync m8n8k4 f64 on all SMs"}
-    out["modgemm_4096"] = {
-        "shape": [m, n, k], "ms": t * 1e3, "field_op_per_s": 2.0 * m * n * k / t / 1e9,
-        "int8_tops": achieved,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOP/s",
-                     "frac": achieved / int8_peak, "peak_kind": "measured (tcgen05 kind::i8 microbenchmark)",
-                     "frac_vs_2x_bf16": achieved / (2.0 * bf16),
-                     "mma_kernel_ms": t_mma * 1e3,
-                     "mma_kernel_frac": (2.0 * m * n * k * limbs * limbs / t_mma / 1e12 / int8_peak) if t_mma > 0 else None,
-                     "note": "int8 ops = 2mnk * L^2 (L = 2 limbs for p = 65521); includes the limb-split "
-                             "conversion passes"},
-    }
-    del A, B, C
-    # --- cfg3: 8192^2 full-rank generic, device resident
-    n3 = 8192
-    a3 = np.random.default_rng(0).integers(0, P, (n3, n3), dtype=np.int64)
-    t3 = torch.from_numpy(a3).to(dev).to(torch.int32)
-    x = torch.empty_like(t3)
-    times = []
-    for it in range(3):
-        x.copy_(t3)
+    pk = measure_peaks_live(dev)["int8_tops"]
+    out = {}
+    for (m, n, k, p) in ((4096, 4096, 4096, 65521), (16384, 16384, 2048, 65521), (63488, 63488, 2048, 65521)):
+        g = torch.Generator(device="cpu").manual_seed(0)
+        A = torch.randint(0, p, (m, k), generator=g, dtype=torch.int32).to(dev)
+        B = torch.randint(0, p, (k, n), generator=g, dtype=torch.int32).to(dev)
+        C = torch.randint(0, p, (m, n), generator=g, dtype=torch.int32).to(dev)
+        args = (ctx.handle, C.data_ptr(), n, A.data_ptr(), k, B.data_ptr(), n, m, n, k, p)
+        for _ in range(3):
+            ctx.lib.pluq_modgemm_sub_tc(*args)
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        f = pb.pluq(pb.DenseMatrix(pb.PrimeField(P), x))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10 if m < 60000 else 3
+        e0.record()
+        for _ in range(reps):
+            st = ctx.lib.pluq_modgemm_sub_tc(*args)
+        e1.record()
         torch.cuda.synchronize(dev)
-        times.append(time.perf_counter() - t0)
-    w3 = work(n3, n3, f.rank)
-    # whole-PLUQ roofline (SURVEY §8d): a field MAC (2 field ops) is L^2 int8 MACs (2 L^2 int8
-    # ops) on the tensor pipe, so the field-op/s ceiling is int8_peak / L^2 (L = 2 for p = 65521,
-    # 3 for p = 8388593)
-    def tensor_frac(value_gfops, limbs_):
-        return value_gfops * 1e9 / (int8_peak * 1e12 / (limbs_ * limbs_))
-
-    out["cfg3_8192"] = {"rank": f.rank, "s_best": min(times), "s_median": statistics.median(times),
-                        "value": w3 / min(times) / 1e9, "unit": UNIT, "stats": pb.last_stats(),
-                        "frac_of_tensor_roofline": tensor_frac(w3 / min(times) / 1e9, 2)}
-    # --- cfg1: 512^2 rank 384
-    from paper_1301_4438_b200 import gen as dgen
-
-    t1 = dgen.gen_xy_rank_device(512, 512, 384, P, seed=0).to(dev)
-    x1 = torch.empty_like(t1)
-    times = []
-    for it in range(5):
-        x1.copy_(t1)
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        f1 = pb.pluq(pb.DenseMatrix(pb.PrimeField(P), x1))
-        torch.cuda.synchronize(dev)
-        times.append(time.perf_counter() - t0)
-    out["cfg1_512"] = {"rank": f1.rank, "s_best": min(times), "value": work(512, 512, f1.rank) / min(times) / 1e9,
-                       "unit": UNIT}
-    del x, t3, x1, t1
-    # --- cfg4 / cfg5 at their full BASELINE sizes (device-generated; checked by size-independent
-    # properties: packed structure, Freivalds reconstruction, cfg4's prescribed rank profiles)
-    from paper_1301_4438_b200 import gen, verify
-
-    for name, m_, n_, r_, p_ in (("cfg4_full", 16384, 32768, 8192, 8388593), ("cfg5_full", 65536, 65536, 32768, P)):
-        if name == "cfg4_full":
-            a0, rows, cols = gen.gen_cfg4_device(m_, n_, r_, p_, seed=0)
-        else:
-            a0, rows, cols = gen.gen_xy_rank_device(m_, n_, r_, p_, seed=0), None, None
-        times = []
-        for it in range(2):
-            xa = a0.clone()
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            f = pb.pluq(pb.DenseMatrix(pb.PrimeField(p_), xa))
-            torch.cuda.synchronize(dev)
-            times.append(time.perf_counter() - t0)
-            if it == 0:
-                del xa
-        checks = {"structure": bool(verify.structure_ok(f)), "freivalds": bool(verify.freivalds(a0, f, probes=2))}
-        if rows is not None:
-            checks["row_profile"] = pb.row_rank_profile(f) == tuple(int(v) for v in rows)
-            checks["col_profile"] = pb.col_rank_profile(f) == tuple(int(v) for v in cols)
-        val = work(m_, n_, f.rank) / min(times) / 1e9
-        out[name] = {"shape": [m_, n_], "p": p_, "rank": f.rank, "s_best": min(times),
-                     "value": val, "unit": UNIT, "checks": checks, "stats": pb.last_stats(),
-                     "frac_of_tensor_roofline": tensor_frac(val, 2 if p_ < 65536 else 3)}
-        del a0, f, xa
+        _native.raise_for(st, ctx, "tc gemm")
+        t = e0.elapsed_time(e1) / 1e3 / reps
+        L = limbs(p)
+        ach = 2.0 * m * n * k * L * L / t / 1e12
+        out[f"{m}x{n}x{k}"] = {"ms": t * 1e3, "int8_tops": ach, "frac_of_int8_peak": ach / pk,
+                               "note": "includes the limb-split passes of A and B"}
+        del A, B, C
         torch.cuda.empty_cache()
     return out
 

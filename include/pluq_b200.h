@@ -47,10 +47,15 @@ int pluq_set_stream(pluq_ctx* ctx, void* stream);
 /* Tuning knobs (0 = keep default): largest node m*n handled whole by one CTA in
  * shared memory, and whether the tensor-core GEMM may be used (1/0). */
 int pluq_set_option(pluq_ctx* ctx, const char* key, int64_t value);
+/* Current value of an option (PLUQ_EINVAL for an unknown key). */
+int pluq_get_option(pluq_ctx* ctx, const char* key, int64_t* value);
 const char* pluq_last_error(pluq_ctx* ctx);
 
 /* pluq(a, threshold) — recursive.py:159-183 (+ _pluq_rec :186-256).
  * dA: device uint32 m x n (pitch ld), overwritten in place by [L\U, V; M, 0].
+ * Entries must be canonical residues in [0, p): otherwise PLUQ_EINVAL and dA is left
+ * untouched (field.py:140-147; option check_inputs).  The same holds for the batched and
+ * host-buffer entry points (the batched host one raises after the fact: see below).
  * p_sigma (m) / q_sigma (n): HOST int64 outputs. rank: host output. */
 int pluq_factor(pluq_ctx* ctx, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p,
                 int64_t threshold, int64_t* p_sigma, int64_t* q_sigma, int64_t* rank,
@@ -80,6 +85,8 @@ int pluq_factor_host_f64(pluq_ctx* ctx, double* hA, int64_t m, int64_t n, int64_
 int pluq_factor_host_i64(pluq_ctx* ctx, int64_t* hA, int64_t m, int64_t n, int64_t p,
                          int64_t threshold, int64_t* p_sigma, int64_t* q_sigma, int64_t* rank,
                          int64_t* counts);
+/* Non-canonical entries (outside [0, p), non-integral, NaN) give PLUQ_EINVAL after the
+ * pipelined call; the buffer's contents are then unspecified. */
 int pluq_factor_batched_host_f64(pluq_ctx* ctx, double* hA, int64_t batch, int64_t m, int64_t n,
                                  int64_t p, int64_t threshold, int64_t* p_sigma,
                                  int64_t* q_sigma, int64_t* ranks);
@@ -117,6 +124,11 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
  * multi-GPU driver for the "Schur complement vanishes" test (recursive.py:188-189 zero blocks). */
 int pluq_nonzero(pluq_ctx* ctx, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t* out);
 
+/* PLUQ_OK iff every entry of the device view (uint32, pitch ld) is a canonical residue in
+ * [0, p); PLUQ_EINVAL otherwise.  The check field.asarray makes when a DenseMatrix is built
+ * (field.py:140-147), for device-resident matrices; one HBM read of the view. */
+int pluq_check_residues(pluq_ctx* ctx, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p);
+
 /* Microbenchmarked peaks of this device (SURVEY §8d roofline denominators):
  * out[0] = tcgen05 kind::i8 dense TOP/s (128x256x32 MMAs, one CTA per SM),
  * out[1] = FP64 DMMA (mma.sync m8n8k4) TFLOP/s.  Diagnostics; not on the factorization path. */
@@ -124,8 +136,9 @@ int pluq_measure_peaks(pluq_ctx* ctx, double* out, int64_t nout);
 
 /* Statistics of the last call: launches, host syncs, nodes, small-node kernels, base-case
  * kernels, tensor-core / SIMT GEMMs, zero-block skips, generic leaves, speculative ok/fail,
- * generic- and fallback-kernel ns of a batch (option time_kernels), and the MMA-kernel ns of
- * the last tensor-core GEMM (option tc_time). */
+ * generic- and fallback-kernel ns of a batch (option time_kernels), the MMA-kernel ns of
+ * the last tensor-core GEMM (option tc_time), and — option tc_time, summed over the call —
+ * MMA-kernel launches, their CUDA-event ns and their algorithmic int8 ops (2 m n k L^2). */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);
 
 #ifdef __cplusplus

@@ -47,6 +47,7 @@ __all__ = [
     "gen_cfg5",
     "gen_xy_rank",
     "effective_work",
+    "pluq_batch",
 ]
 
 _F64_EXACT = 1 << 53
@@ -517,3 +518,41 @@ def gen_cfg5(seed=0, n=65536, r=32768, p=65521):
 def effective_work(m, n, r) -> float:
     """BASELINE metric numerator W = 2mnr - (m+n) r^2 + 2 r^3 / 3."""
     return 2.0 * m * n * r - (m + n) * float(r) ** 2 + 2.0 * float(r) ** 3 / 3.0
+
+
+def _pluq_batch_worker(args):
+    """One process of pluq_batch: factor blocks[i] in place, return the per-block results."""
+    blocks, p, threshold = args
+    out = []
+    for a in blocks:
+        x = np.asarray(a).astype(field_dtype(p))
+        c = Counts()
+        pp, qq, r, _ = pluq(x, p, threshold, c)
+        out.append((np.asarray(pp), np.asarray(qq), r, x.astype(np.int64), c.as_tuple()))
+    return out
+
+
+def pluq_batch(batch: np.ndarray, p: int, threshold: int = 30, processes: int | None = None):
+    """The reference's per-matrix loop over a batch (cfg2), spread over a spawn-started
+    process pool (each process single-threaded; one decomposition is
+    single-threaded, distinct ones are independent).  Returns a list of
+    (P.sigma, Q.sigma, r, packed int64, counts) per block."""
+    import multiprocessing as mp
+    import os
+
+    n = len(batch)
+    procs = max(1, min(processes or os.cpu_count() or 1, n))
+    if procs == 1:
+        return _pluq_batch_worker((batch, p, threshold))
+    parts = np.array_split(np.arange(n), procs)
+    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"  # inherited by the spawned children
+    try:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            res = pool.map(_pluq_batch_worker, [(batch[ix], p, threshold) for ix in parts])
+    finally:
+        if env_old is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = env_old
+    return [r for part in res for r in part]

@@ -7,7 +7,7 @@ sm_100a CUDA in ``libpluq_b200.so`` (C ABI: include/pluq_b200.h).
 """
 
 from .field import ABSOLUTE_MODULUS_BOUND, DEFAULT_MODULUS_BOUND, PrimeField, inverse_mod, is_prime
-from .kernels import CudaKernels, device_matmul_mod
+from .kernels import ClassicalKernels, CudaKernels, device_matmul_mod
 from .matrix import DenseMatrix, OpCounts, Permutation, PluqFactors, apply_cols, apply_rows, perm_block_diag
 from .distributed import pluq_distributed
 from .rank_profile import col_rank_profile, leading_rank_profiles, row_rank_profile
@@ -31,6 +31,7 @@ __version__ = "0.1.0"
 __all__ = [
     "ABSOLUTE_MODULUS_BOUND",
     "BatchedPluq",
+    "ClassicalKernels",
     "CudaKernels",
     "DEFAULT_MODULUS_BOUND",
     "DEFAULT_THRESHOLD",

@@ -26,6 +26,8 @@ SIGNATURES = {
     "pluq_destroy": (ctypes.c_int, [_p]),
     "pluq_set_stream": (ctypes.c_int, [_p, _p]),
     "pluq_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i64]),
+    "pluq_get_option": (ctypes.c_int, [_p, ctypes.c_char_p, _pi64]),
+    "pluq_check_residues": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64]),
     "pluq_last_error": (ctypes.c_char_p, [_p]),
     "pluq_last_stats": (ctypes.c_int, [_p, _pi64, _i64]),
     "pluq_measure_peaks": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_double), _i64]),
@@ -117,12 +119,18 @@ class Context:
     def set_option(self, key: str, value: int) -> None:
         raise_for(self.lib.pluq_set_option(self.handle, key.encode(), int(value)), self, f"option {key}")
 
+    def get_option(self, key: str) -> int:
+        out = ctypes.c_int64()
+        raise_for(self.lib.pluq_get_option(self.handle, key.encode(), ctypes.byref(out)), self, f"option {key}")
+        return int(out.value)
+
     def stats(self) -> dict:
-        buf = (ctypes.c_int64 * 14)()
-        self.lib.pluq_last_stats(self.handle, buf, 14)
+        buf = (ctypes.c_int64 * 17)()
+        self.lib.pluq_last_stats(self.handle, buf, 17)
         keys = ["launches", "host_syncs", "nodes", "small_node_kernels", "basecase_kernels",
                 "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves", "speculative_ok",
-                "speculative_fail", "t_generic_ns", "t_fallback_ns", "t_tc_mma_ns"]
+                "speculative_fail", "t_generic_ns", "t_fallback_ns", "t_tc_mma_ns",
+                "tc_timed_launches", "tc_timed_ns", "tc_timed_int8_ops"]
         return dict(zip(keys, list(buf)))
 
     def measure_peaks(self) -> dict:

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/pluq_b200.h"
@@ -120,6 +121,9 @@ struct pluq_ctx {
   int64_t fb_prefix = 1;           // 64x64 batches: the rank-profile kernel resumes after the generic kernel's pivots
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
+  int64_t check_inputs = 1;        // device inputs: range-check residues first (field.py:140-147 -> EINVAL)
+  int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
+  cudaMemPool_t pool = nullptr;    // the context's own stream-ordered pool (not the device default pool)
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
@@ -170,7 +174,12 @@ struct pluq_ctx {
     return h_bres;
   }
 
-  void reset_stats() { st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok = st_spec_fail = 0; }
+  void reset_stats() {
+    st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok =
+        st_spec_fail = 0;
+    tc.acc_launches = 0;
+    tc.acc_ms = tc.acc_ops = 0.0;
+  }
 
   void sync() {
     CU(cudaStreamSynchronize(stream));
@@ -206,7 +215,7 @@ struct pluq_ctx {
   T* dalloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    CU(cudaMallocAsync(&p, count * sizeof(T), stream));
+    CU(cudaMallocFromPoolAsync(&p, count * sizeof(T), pool, stream));
     return reinterpret_cast<T*>(p);
   }
   void dfree(void* p) {
@@ -216,7 +225,7 @@ struct pluq_ctx {
   T* dalloc_on(size_t count, cudaStream_t s) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    CU(cudaMallocAsync(&p, count * sizeof(T), s));
+    CU(cudaMallocFromPoolAsync(&p, count * sizeof(T), pool, s));
     return reinterpret_cast<T*>(p);
   }
   void dfree_on(void* p, cudaStream_t s) {
@@ -1028,12 +1037,29 @@ int validate(int64_t m, int64_t n, int64_t p) {
   return kOk;
 }
 
+// Restores the caller's current device on scope exit (the ABI must not change it).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) {
+      cudaError_t e = cudaSetDevice(dev);
+      if (e != cudaSuccess) throw PluqError(kCuda, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 int guarded(pluq_ctx* ctx, F&& f) {
   if (!ctx) return kInvalid;
   try {
-    CU(cudaSetDevice(ctx->device));
+    DeviceGuard dg(ctx->device);
     f();
+    if (ctx->pool) cudaMemPoolTrimTo(ctx->pool, (size_t)std::max<int64_t>(0, ctx->pool_keep_mb) << 20);
     return kOk;
   } catch (const PluqError& e) {
     ctx->err = e.what();
@@ -1045,6 +1071,21 @@ int guarded(pluq_ctx* ctx, F&& f) {
     ctx->err = e.what();
     return kCuda;
   }
+}
+
+// PLUQ_EINVAL unless every entry of the device view is a canonical residue in [0, p): the
+// reference rejects such input when the DenseMatrix is built (field.py:140-147, ValueError),
+// before anything is modified.  One read of the view (HBM-bound).
+void check_residues(pluq_ctx* c, const View& x, uint32_t p) {
+  if (!c->check_inputs || x.m <= 0 || x.n <= 0) return;
+  CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  const int n4 = std::max(1, x.n / 4);
+  dim3 grid((unsigned)std::min(4, (n4 + 255) / 256), (unsigned)std::min(x.m, 4096));
+  range_check_kernel<<<grid, 256, 0, c->stream>>>(x, p, c->d_flag);
+  c->check_launch();
+  CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
 }
 
 void finish_counts(pluq_ctx* c, const Counts& hc, int64_t* counts) {
@@ -1101,10 +1142,18 @@ int pluq_create(pluq_ctx** out, int device, void* stream) {
     CU(cudaHostAlloc((void**)&c->h_stop, 4 * sizeof(int), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_zflags, pluq_ctx::kMaxDepth * sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_zflags, pluq_ctx::kMaxDepth * sizeof(int), cudaHostAllocDefault));
-    cudaMemPool_t pool;
-    CU(cudaDeviceGetDefaultMemPool(&pool, device));
+    // the context's own pool: freed blocks are kept for reuse between calls (release
+    // threshold = max) and trimmed to pool_keep_mb after each API call (guarded); the
+    // device's default pool, which other libraries share, is left untouched
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    CU(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thr = ~0ull;
-    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CU(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->tc.pool = c->pool;
     c->ensure_res(1 << 16);
     // rec_smem recurses on the device: give each thread room for the deepest
     // small-node recursion (threshold 1 on a 128x128 node is ~8 frames).
@@ -1142,6 +1191,10 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->h_stop) cudaFreeHost(c->h_stop);
   if (c->h_zflags) cudaFreeHost(c->h_zflags);
   if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->pool) {
+    cudaDeviceSynchronize();  // stream-ordered frees on the side streams have completed
+    cudaMemPoolDestroy(c->pool);
+  }
   delete c;
   return kOk;
 }
@@ -1152,52 +1205,48 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   return kOk;
 }
 
+// Every tuning knob: option name -> context field (pluq_set_option / pluq_get_option).
+#define PLUQ_OPTIONS(X)                                                                             \
+  X(small_cap, c->small_cap) X(small_threads, c->small_threads) X(batch_threads, c->batch_threads)  \
+  X(use_tc, c->use_tc) X(tc_min_dim, c->tc_min_dim) X(tc_min_k, c->tc_min_k)                        \
+  X(tc_k_pass, c->tc.k_pass_override) X(tc_cfg, c->tc.variant) X(tc_mnb, c->tc.mn_b)               \
+  X(tc_group, c->tc.raster_group) X(tc_cpf, c->tc.c_prefetch) X(tc_grid, c->tc.grid_override)      \
+  X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma)                        \
+  X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
+  X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
+  X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
+  X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
+  X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
+  X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
+  X(rpm_eager, c->rpm_eager) X(tc_trsm_min, c->tc_trsm_min) X(trace_pipeline, c->trace_pipeline)    \
+  X(spec_block, c->spec_block) X(spec_check, c->spec_check) X(spec_panel, c->spec_panel)            \
+  X(spec_panel_big, c->spec_panel_big) X(spec_big_elems, c->spec_big_elems)                         \
+  X(check_inputs, c->check_inputs) X(pool_keep_mb, c->pool_keep_mb)
+
 int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return kInvalid;
-  std::string k(key);
-  if (k == "small_cap") c->small_cap = value;
-  else if (k == "small_threads") c->small_threads = value;
-  else if (k == "batch_threads") c->batch_threads = value;
-  else if (k == "use_tc") c->use_tc = value;
-  else if (k == "tc_min_dim") c->tc_min_dim = value;
-  else if (k == "tc_min_k") c->tc_min_k = value;
-  else if (k == "tc_k_pass") c->tc.k_pass_override = value;
-  else if (k == "tc_cfg") c->tc.variant = (int)value;
-  else if (k == "tc_mnb") c->tc.mn_b = (int)value;
-  else if (k == "tc_group") c->tc.raster_group = (int)value;
-  else if (k == "tc_cpf") c->tc.c_prefetch = (int)value;
-  else if (k == "tc_grid") c->tc.grid_override = (int)value;
-  else if (k == "tc_dbg") c->tc.dbg = (int)value;
-  else if (k == "tc_vec") c->tc.vec_limbs = (int)value;
-  else if (k == "tc_time") c->tc.time_mma = (int)value;
-  else if (k == "try_generic") c->try_generic = value;
-  else if (k == "time_kernels") c->time_kernels = value;
-  else if (k == "fixed_kernels") c->fixed_kernels = value;
-  else if (k == "host_chunks") c->host_chunks = value;
-  else if (k == "chunk_shape") c->chunk_shape = value;
-  else if (k == "diag_lazy") c->diag_lazy = value;
-  else if (k == "lookahead") c->lookahead = value;
-  else if (k == "la_reserve") c->la_reserve = value;
-  else if (k == "exact_kernel") c->exact_kernel = value;
-  else if (k == "rpm_threads") c->rpm_threads = value;
-  else if (k == "rpm_lazy") c->rpm_lazy = value;
-  else if (k == "par_trsm") c->par_trsm = value;
-  else if (k == "sym_par") c->sym_par = value;
-  else if (k == "tc_trsm") c->tc_trsm = value;
-  else if (k == "pair_leaves") c->pair_leaves = value;
-  else if (k == "stream_fb") c->stream_fb = value;
-  else if (k == "stream_fb_spin") c->stream_fb_spin = value;
-  else if (k == "fb_prefix") c->fb_prefix = value;
-  else if (k == "rpm_eager") c->rpm_eager = value;
-  else if (k == "tc_trsm_min") c->tc_trsm_min = value;
-  else if (k == "trace_pipeline") c->trace_pipeline = value;
-  else if (k == "spec_block") c->spec_block = value;
-  else if (k == "spec_check") c->spec_check = value;
-  else if (k == "spec_panel") c->spec_panel = value;
-  else if (k == "spec_panel_big") c->spec_panel_big = value;
-  else if (k == "spec_big_elems") c->spec_big_elems = value;
-  else return kInvalid;
-  return kOk;
+  const std::string k(key);
+#define PLUQ_SET(name, field)                  \
+  if (k == #name) {                            \
+    field = (std::decay_t<decltype(field)>)value; \
+    return kOk;                                \
+  }
+  PLUQ_OPTIONS(PLUQ_SET)
+#undef PLUQ_SET
+  return kInvalid;
+}
+
+int pluq_get_option(pluq_ctx* c, const char* key, int64_t* value) {
+  if (!c || !key || !value) return kInvalid;
+  const std::string k(key);
+#define PLUQ_GET(name, field)    \
+  if (k == #name) {              \
+    *value = (int64_t)(field);   \
+    return kOk;                  \
+  }
+  PLUQ_OPTIONS(PLUQ_GET)
+#undef PLUQ_GET
+  return kInvalid;
 }
 
 const char* pluq_last_error(pluq_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -1207,6 +1256,22 @@ int pluq_nonzero(pluq_ctx* c, const uint32_t* dA, int64_t ld, int64_t m, int64_t
   return guarded(c, [&] {
     Ops ops{c, ModP::make(2)};
     *out = (m > 0 && n > 0) ? (ops.nonzero(View{const_cast<uint32_t*>(dA), ld, (int)m, (int)n}) ? 1 : 0) : 0;
+  });
+}
+
+int pluq_check_residues(pluq_ctx* c, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p) {
+  if (int v = validate(m, n, p)) return v;
+  if (m > 0 && n > 0 && (!dA || ld < n)) return kInvalid;
+  return guarded(c, [&] {
+    const int64_t keep = c->check_inputs;
+    c->check_inputs = 1;
+    try {
+      check_residues(c, View{const_cast<uint32_t*>(dA), ld, (int)m, (int)n}, (uint32_t)p);
+    } catch (...) {
+      c->check_inputs = keep;
+      throw;
+    }
+    c->check_inputs = keep;
   });
 }
 
@@ -1261,11 +1326,12 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[14] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+  int64_t v[17] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
                    c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail,
                    (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f),
-                   (int64_t)(c->tc.mma_ms * 1e6f)};
-  for (int64_t i = 0; i < nout && i < 14; ++i) out[i] = v[i];
+                   (int64_t)(c->tc.mma_ms * 1e6f), c->tc.acc_launches, (int64_t)(c->tc.acc_ms * 1e6),
+                   (int64_t)c->tc.acc_ops};
+  for (int64_t i = 0; i < nout && i < 17; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -1274,14 +1340,20 @@ int pluq_factor(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int
   if (threshold < 1) return kInvalid;
   if (int v = validate(m, n, p)) return v;
   if (ld < n || !rank || (m && !psig) || (n && !qsig)) return kInvalid;
-  return guarded(c, [&] { factor_device(c, dA, ld, m, n, p, threshold, psig, qsig, rank, counts, false); });
+  return guarded(c, [&] {
+    check_residues(c, View{dA, ld, (int)m, (int)n}, (uint32_t)p);
+    factor_device(c, dA, ld, m, n, p, threshold, psig, qsig, rank, counts, false);
+  });
 }
 
 int pluq_factor_iterative(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p,
                           int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
   if (int v = validate(m, n, p)) return v;
   if (ld < n || !rank || (m && !psig) || (n && !qsig)) return kInvalid;
-  return guarded(c, [&] { factor_device(c, dA, ld, m, n, p, 1, psig, qsig, rank, counts, true); });
+  return guarded(c, [&] {
+    check_residues(c, View{dA, ld, (int)m, (int)n}, (uint32_t)p);
+    factor_device(c, dA, ld, m, n, p, 1, psig, qsig, rank, counts, true);
+  });
 }
 
 int64_t pluq_batched_max_elems(pluq_ctx*, int64_t m, int64_t n) {
@@ -1295,8 +1367,10 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
   if (int v = validate(m, n, p)) return v;
   if (block_smem_bytes(m, n, threshold) > kMaxDynSmem) return kUnsupported;
   if (batch == 0) return kOk;
-  c->reset_stats();
+  if (stride < m * n) return kInvalid;
   return guarded(c, [&] {
+    c->reset_stats();
+    if (m > 0 && n > 0) check_residues(c, View{dA, stride, (int)batch, (int)(m * n)}, (uint32_t)p);
     SmallArgs a;
     a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
@@ -1400,9 +1474,17 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
     if (cnt) CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
     if (cnt) {
-      if (is_f64) from_f64_kernel<<<grid, 256, 0, c->stream>>>((const double*)raw, dA, cnt);
-      else from_i64_kernel<<<grid, 256, 0, c->stream>>>((const int64_t*)raw, dA, cnt);
+      CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+      if (is_f64) from_f64_kernel<<<grid, 256, 0, c->stream>>>((const double*)raw, dA, cnt, (uint32_t)p, c->d_flag);
+      else from_i64_kernel<<<grid, 256, 0, c->stream>>>((const int64_t*)raw, dA, cnt, (uint32_t)p, c->d_flag);
       c->check_launch();
+      CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      if (*c->h_flag) {  // nothing was modified: the host buffer is only written at the end
+        c->dfree(dA);
+        c->dfree(raw);
+        throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+      }
     }
     factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
     if (cnt) {
@@ -1512,6 +1594,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     int* flags = a.try_generic ? c->dalloc<int>(2 * (size_t)batch + nchunks) : nullptr;
     a.fail_list = nullptr; a.fail_count = nullptr; a.fail_base = 0;
     if (flags) CU(cudaMemsetAsync(flags + batch, 0, sizeof(int) * nchunks, c->stream));
+    CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaEventRecord(ev0, sin));
     int64_t last = 0;
@@ -1524,7 +1607,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
       CU(cudaStreamWaitEvent(c->stream, ev_in[k], 0));
       const int64_t cntk = nb * mn;
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cntk + 255) / 256));
-      from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw + b0 * mn, dA + b0 * mn, cntk);
+      from_f64_kernel<<<grid, 256, 0, c->stream>>>(raw + b0 * mn, dA + b0 * mn, cntk, (uint32_t)p, c->d_flag);
       c->check_launch();
       // chunk k's results are one contiguous record [P (nb x m) | Q (nb x n) | rank (nb)]
       // so that a single D2H copy returns them
@@ -1589,6 +1672,11 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     c->dfree(dp);
     c->dfree(dA);
     c->dfree(raw);  // stream-ordered: every stream that used these buffers has been synchronised
+    // non-canonical entries (flagged by the conversions): ValueError like the reference's
+    // DenseMatrix construction; blocks holding them were factored as if they were 0
+    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
     if (tr)
       fprintf(stderr, "pipeline: frees %.3f ms\n",
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count());

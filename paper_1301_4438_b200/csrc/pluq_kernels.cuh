@@ -347,7 +347,10 @@ __global__ void crout_fast_kernel(SmallArgs args) {
   const int r = crout_generic<true>(x, args.mp, args.invtab, &sh);
   if (threadIdx.x == 0) {
     args.generic_flag[blockIdx.x] = r >= 0;
-    if (r < 0 && args.fail_list) args.fail_list[atomicAdd(args.fail_count, 1)] = args.fail_base + blockIdx.x;
+    if (r < 0 && args.fail_list) atomicExch(args.fail_list + atomicAdd(args.fail_count, 1), args.fail_base + blockIdx.x);
+    // streaming batches: the concurrent rank-profile consumer exits once every generic CTA
+    // has reported (rpm_next_slot), so failing CTAs count as done too
+    if (r < 0 && args.done_count) { __threadfence(); atomicAdd(args.done_count, 1); }
   }
   if (r < 0) return;
   for (int i = w; i < m; i += nw)
@@ -358,6 +361,7 @@ __global__ void crout_fast_kernel(SmallArgs args) {
   for (int t = threadIdx.x; t < n; t += blockDim.x) qo[t] = t;
   if (threadIdx.x == 0) {
     args.r_out[blockIdx.x] = r;
+    if (args.done_count) atomicAdd(args.done_count, 1);
     if (args.generic_counts) {
       const unsigned long long* g = args.generic_counts + 4 * r;
       unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);
@@ -1376,22 +1380,54 @@ inline size_t diag_fast_smem(int64_t bs, bool tab) {
   return (size_t)(((bs * (bs | 1)) + 3) & ~3ll) * 4 + (tab ? 65536 * 2 : 0);
 }
 
-// Host-format conversion: float64 / int64 residues <-> uint32 device storage.
-__global__ void from_f64_kernel(const double* in, uint32_t* out, int64_t count) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = (uint32_t)in[t];
+// Host-format conversion: float64 / int64 residues <-> uint32 device storage.  The
+// reference validates canonical residues when a DenseMatrix is built (field.py:140-147,
+// ValueError); here the conversion flags any entry outside [0, p) (or a non-integral /
+// NaN double) and stores 0 for it, and the caller raises PLUQ_EINVAL before factoring.
+__global__ void from_f64_kernel(const double* in, uint32_t* out, int64_t count, uint32_t p, int* bad) {
+  bool b = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = in[t];
+    const bool ok = v >= 0.0 && v < (double)p && v == floor(v);
+    out[t] = ok ? (uint32_t)v : 0u;
+    b |= !ok;
+  }
+  if (bad && __syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 __global__ void to_f64_kernel(const uint32_t* in, double* out, int64_t count) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
     out[t] = (double)in[t];
 }
-__global__ void from_i64_kernel(const int64_t* in, uint32_t* out, int64_t count) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = (uint32_t)in[t];
+__global__ void from_i64_kernel(const int64_t* in, uint32_t* out, int64_t count, uint32_t p, int* bad) {
+  bool b = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = in[t];
+    const bool ok = v >= 0 && v < (int64_t)p;
+    out[t] = ok ? (uint32_t)v : 0u;
+    b |= !ok;
+  }
+  if (bad && __syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 __global__ void to_i64_kernel(const uint32_t* in, int64_t* out, int64_t count) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
     out[t] = (int64_t)in[t];
+}
+
+// flag <- 1 if a device view holds an entry >= p (uint32 storage: a negative int32 tensor
+// entry reads as >= 2^31 > p).  One read of the view, 16-byte loads when rows are aligned.
+__global__ void range_check_kernel(View x, uint32_t p, int* flag) {
+  bool bad = false;
+  const bool vec = (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.a) & 15) == 0;
+  const int n4 = vec ? x.n / 4 : 0;
+  for (int64_t i = blockIdx.y; i < x.m; i += gridDim.y) {
+    const uint32_t* xr = x.row((int)i);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += gridDim.x * blockDim.x) {
+      const uint4 q = reinterpret_cast<const uint4*>(xr)[j];
+      bad |= (q.x >= p) | (q.y >= p) | (q.z >= p) | (q.w >= p);
+    }
+    for (int j = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) bad |= xr[j] >= p;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 }  // namespace pluq

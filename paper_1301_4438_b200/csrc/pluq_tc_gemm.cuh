@@ -562,6 +562,11 @@ struct TcGemm {
   int raster_group = 8;         // option tc_group: tile rows per rasterisation group (0: row-major tiles)
   int c_prefetch = 1;           // option tc_cpf: L2 prefetch of the C tile while its MMAs run
   float mma_ms = 0.f;           // summed MMA-kernel time of the last call when timed
+  cudaMemPool_t pool = nullptr; // the owning context's memory pool (limb-plane scratch)
+  // option tc_time: MMA-kernel launches, their summed CUDA-event time and algorithmic int8
+  // ops (2 m n k L^2 per pass) since the context's last reset_stats (bench roofline)
+  int64_t acc_launches = 0;
+  double acc_ms = 0.0, acc_ops = 0.0;
 
   static int limbs(uint32_t p) {
     int bits = 0;
@@ -629,8 +634,8 @@ struct TcGemm {
     const int64_t k_first = std::min<int64_t>(k, kp);
     const int kpad_max = (int)((k_first + TC_BK - 1) / TC_BK * TC_BK);
     uint8_t *da = nullptr, *db = nullptr;
-    if (cudaMallocAsync((void**)&da, (size_t)L * m_pad * kpad_max, st) != cudaSuccess ||
-        cudaMallocAsync((void**)&db, (size_t)L * n_pad * kpad_max, st) != cudaSuccess) {
+    if (cudaMallocFromPoolAsync((void**)&da, (size_t)L * m_pad * kpad_max, pool, st) != cudaSuccess ||
+        cudaMallocFromPoolAsync((void**)&db, (size_t)L * n_pad * kpad_max, pool, st) != cudaSuccess) {
       last_error = "workspace allocation failed";
       return kNoMemory;
     }
@@ -690,6 +695,9 @@ struct TcGemm {
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         mma_ms += ms;
+        acc_ms += ms;
+        acc_ops += 2.0 * m * n * (double)kc * L * L;
+        ++acc_launches;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
       }

@@ -145,3 +145,9 @@ def device_matmul_mod(x: np.ndarray, y: np.ndarray, p: int) -> np.ndarray:
     _native.raise_for(st, ctx, "matmul_mod")
     out = tc.to("cpu").numpy().astype(np.int64)
     return (p - out) % p
+
+
+# The reference exports its kernel strategy as ``ClassicalKernels`` (pluq/__init__.py:11,49;
+# kernels.py:30-120); user code written against it (``pluq.ClassicalKernels(field)``) gets the
+# CUDA strategy, which has the same interface and charges.
+ClassicalKernels = CudaKernels

@@ -25,6 +25,18 @@ from .matrix import DenseMatrix, OpCounts, Permutation, PluqFactors, apply_cols,
 DEFAULT_THRESHOLD = 30
 
 
+def _torch_dtype(dtype):
+    """torch dtype of a Workspace request: torch dtypes as given, numpy dtypes mapped, and
+    None -> int32 (device residues are int32 whatever the host field dtype)."""
+    import torch
+
+    if dtype is None:
+        return torch.int32
+    if isinstance(dtype, torch.dtype):
+        return dtype
+    return torch.from_numpy(np.zeros(0, dtype=np.dtype(dtype))).dtype
+
+
 class Workspace:
     """Source of auxiliary element buffers (recursive.py:36-48); device tensors here."""
 
@@ -32,7 +44,7 @@ class Workspace:
         import torch
 
         shape = (shape,) if isinstance(shape, int) else tuple(shape)
-        return torch.zeros(shape, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+        return torch.zeros(shape, dtype=_torch_dtype(dtype), device=torch.device("cuda", torch.cuda.current_device()))
 
     def release(self, buf) -> None:
         pass
@@ -187,7 +199,7 @@ def _rec_dev(x, p, threshold, counts, kernels, ws):
     u2 = x[r1:r1 + r2, kc:kc + r2]
     l3 = x[kr:kr + r3, r1:r1 + r3]
     kernels.trsm_right_upper(x[kr:kr + r3, kc:kc + r2], u2, counts)
-    scratch = ws.element_buffer((r3, r2))
+    scratch = ws.element_buffer((r3, r2), x.dtype)
     scratch.copy_(x[kr:kr + r3, kc:kc + r2])
     kernels.trsm_left_unit_lower(l3, scratch, counts)
     kernels.trsm_right_upper(x[kr + r3:, kc:kc + r2], u2, counts)
@@ -234,8 +246,8 @@ def pluq(
     kernels = kernels if kernels is not None else CudaKernels(a.field)
     ws = workspace if workspace is not None else Workspace()
     dev = a if a.on_device else a.to_device()
-    rowbuf = ws.element_buffer(a.n)
-    colbuf = ws.element_buffer(a.m)
+    rowbuf = ws.element_buffer(a.n, dev.data.dtype)
+    colbuf = ws.element_buffer(a.m, dev.data.dtype)
     try:
         p_perm, q_perm, rank = _rec_dev(dev.data, a.p, threshold, counts, kernels, ws)
     finally:

@@ -1,0 +1,135 @@
+"""Error behaviour and hygiene at the C-ABI boundary (SURVEY §8(b) error conventions).
+
+The reference rejects non-canonical entries when a DenseMatrix is built
+(/root/reference/pkg/src/pluq/field.py:140-147, ValueError) before anything is modified;
+the device paths do the same through the range check in the C ABI.
+"""
+
+import ctypes
+import time
+
+import numpy as np
+import pytest
+
+from oracle import pluq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb(cuda_ok):
+    import paper_1301_4438_b200 as mod
+    from paper_1301_4438_b200 import _native
+
+    _native.load_library()
+    return mod
+
+
+@pytest.mark.parametrize("bad", [65521, 70000, -1, -65521])
+def test_device_densematrix_rejects_noncanonical(pb, bad):
+    import torch
+
+    t = torch.randint(0, 65521, (300, 200), dtype=torch.int32, device="cuda")
+    t[123, 77] = bad
+    with pytest.raises(ValueError):
+        pb.DenseMatrix(pb.PrimeField(65521), t)
+
+
+def test_c_abi_factor_rejects_and_leaves_input(pb):
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    t = torch.randint(0, p, (256, 256), dtype=torch.int32, device="cuda")
+    t[200, 3] = p + 5
+    before = t.clone()
+    ctx = _native.context()
+    psig = np.zeros(256, np.int64)
+    qsig = np.zeros(256, np.int64)
+    rank = np.zeros(1, np.int64)
+    st = ctx.lib.pluq_factor(ctx.handle, t.data_ptr(), 256, 256, 256, p, 30, _native.i64p(psig),
+                             _native.i64p(qsig), _native.i64p(rank), None)
+    assert st == _native.PLUQ_EINVAL
+    assert torch.equal(t, before)
+
+
+@pytest.mark.parametrize("dtype,bad", [(np.float64, 0.5), (np.float64, float("nan")), (np.float64, -3.0),
+                                       (np.float64, 65521.0), (np.int64, 65521), (np.int64, -2)])
+def test_c_abi_host_buffers_reject_and_leave_input(pb, dtype, bad):
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    a = np.random.default_rng(1).integers(0, p, (150, 170)).astype(dtype)
+    a[17, 33] = bad
+    before = a.copy()
+    ctx = _native.context()
+    psig = np.zeros(150, np.int64)
+    qsig = np.zeros(170, np.int64)
+    rank = np.zeros(1, np.int64)
+    fn = ctx.lib.pluq_factor_host_f64 if dtype == np.float64 else ctx.lib.pluq_factor_host_i64
+    st = fn(ctx.handle, a.ctypes.data, 150, 170, p, 30, _native.i64p(psig), _native.i64p(qsig), _native.i64p(rank), None)
+    assert st == _native.PLUQ_EINVAL
+    assert np.array_equal(a, before, equal_nan=True)
+
+
+def test_batched_rejects_noncanonical(pb):
+    import torch
+
+    t = torch.randint(0, 65521, (64, 64, 64), dtype=torch.int32, device="cuda")
+    t[40, 5, 6] = -7
+    before = t.clone()
+    with pytest.raises(ValueError):
+        pb.pluq_batched(t, 65521, 30)
+    assert torch.equal(t, before)
+    h = np.random.default_rng(2).integers(0, 65521, (32, 64, 64)).astype(np.float64)
+    h[31, 63, 63] = 1e9
+    with pytest.raises(ValueError):
+        pb.pluq_batched(h, 65521, 30)
+
+
+def test_current_device_and_options_roundtrip(pb):
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    torch.cuda.set_device(0)
+    a = pb.DenseMatrix(pb.PrimeField(101), torch.randint(0, 101, (64, 80), dtype=torch.int32, device="cuda"))
+    pb.pluq(a)
+    assert torch.cuda.current_device() == 0
+    ctx = _native.context()
+    old = ctx.get_option("spec_panel")
+    ctx.set_option("spec_panel", 512)
+    assert ctx.get_option("spec_panel") == 512
+    ctx.set_option("spec_panel", old)
+    with pytest.raises(ValueError):
+        ctx.get_option("no_such_option")
+
+
+def test_classical_kernels_alias(pb):
+    assert pb.ClassicalKernels is pb.CudaKernels
+    k = pb.ClassicalKernels(pb.PrimeField(65521))
+    assert hasattr(k, "mm_acc") and hasattr(k, "trsm_left_unit_lower") and hasattr(k, "trsm_right_upper")
+
+
+@pytest.mark.parametrize("m,n", [(48, 48), (40, 56)])
+def test_streaming_batch_non_64_blocks_bounded_time(pb, m, n):
+    """Batches of >= 1024 blocks run the concurrent rank-profile consumer; for shapes other
+    than 64x64 (crout_fast_kernel) it must see every generic CTA finish and exit at once
+    instead of waiting out its spin bound."""
+    import torch
+
+    p = 65521
+    host = np.random.default_rng(m * n).integers(0, p, (1536, m, n))
+    host[::97] = np.stack([orc.gen_xy_rank(m, n, 10, p, s) for s in range(0, 1536, 97)])  # non-generic blocks
+    t = torch.from_numpy(host).cuda().to(torch.int32)
+    w = t.clone()
+    pb.pluq_batched(w, p, 30)  # warm-up (module load, attributes)
+    torch.cuda.synchronize()
+    w.copy_(t)
+    t0 = time.perf_counter()
+    res = pb.pluq_batched(w, p, 30)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    assert dt < 0.05, dt
+    for b in list(range(0, 1536, 97)) + [1, 500, 1535]:
+        P, Q, r, _ = orc.pluq(host[b].astype(np.float64), p, 30)
+        assert int(res.ranks[b]) == r and np.array_equal(res.p_sigma[b].cpu().numpy(), P)

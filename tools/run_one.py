@@ -112,10 +112,16 @@ elif mode == "cfg5":
     div = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     m = 65536 // div; r = 32768 // div
     a0 = gen.gen_xy_rank_device(m, m, r, P, seed=0)
-    for it in range(int(sys.argv[3]) if len(sys.argv) > 3 else 1):
-        x = a0.clone(); torch.cuda.synchronize(); t0 = time.perf_counter()
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    x = torch.empty_like(a0)
+    for it in range(reps):
+        x.copy_(a0); torch.cuda.synchronize()
+        last = it == reps - 1 and os.environ.get("PLUQ_PROFILE_LAST")
+        if last: torch.cuda.profiler.start()   # ncu --profile-from-start off: only this pluq()
+        t0 = time.perf_counter()
         f = pb.pluq(pb.DenseMatrix(pb.PrimeField(P), x)); torch.cuda.synchronize()
-        print(f"cfg5/{div}: {1e3*(time.perf_counter()-t0):.1f} ms rank {f.rank}", flush=True)
+        if last: torch.cuda.profiler.stop()
+        print(f"cfg5/{div}: {1e3*(time.perf_counter()-t0):.1f} ms rank {f.rank} {pb.last_stats()}", flush=True)
 elif mode == "e2emed":
     # median of 10 untraced host-buffer batched calls per option setting
     import statistics
