@@ -124,6 +124,14 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
  * multi-GPU driver for the "Schur complement vanishes" test (recursive.py:188-189 zero blocks). */
 int pluq_nonzero(pluq_ctx* ctx, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t* out);
 
+/* Algorithm 1 with the Algorithm 2 base case (recursive.py:186-256, iterative.py:23-91)
+ * replayed symbolically on the m x n rank profile matrix with ones at (prow[k], pcol[k]),
+ * k < r: the P.sigma (m), Q.sigma (n) and OpCounts (counts[4], may be NULL; SET, not added)
+ * that pluq() returns for ANY matrix with that rank profile matrix (pluq_rpm.cuh facts).
+ * Host-only (no device work); PLUQ_EINVAL unless the pairs form a partial permutation. */
+int pluq_rank_profile_replay(int64_t m, int64_t n, int64_t threshold, int64_t r, const int64_t* prow,
+                             const int64_t* pcol, int64_t* p_sigma, int64_t* q_sigma, int64_t* counts);
+
 /* PLUQ_OK iff every entry of the device view (uint32, pitch ld) is a canonical residue in
  * [0, p); PLUQ_EINVAL otherwise.  The check field.asarray makes when a DenseMatrix is built
  * (field.py:140-147), for device-resident matrices; one HBM read of the view. */
@@ -138,7 +146,8 @@ int pluq_measure_peaks(pluq_ctx* ctx, double* out, int64_t nout);
  * kernels, tensor-core / SIMT GEMMs, zero-block skips, generic leaves, speculative ok/fail,
  * generic- and fallback-kernel ns of a batch (option time_kernels), the MMA-kernel ns of
  * the last tensor-core GEMM (option tc_time), and — option tc_time, summed over the call —
- * MMA-kernel launches, their CUDA-event ns and their algorithmic int8 ops (2 m n k L^2). */
+ * MMA-kernel launches, their CUDA-event ns and their algorithmic int8 ops (2 m n k L^2), and
+ * the zero pivots the speculative LU repaired by a column rotation. */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);
 
 #ifdef __cplusplus

@@ -33,6 +33,7 @@ SIGNATURES = {
     "pluq_measure_peaks": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_double), _i64]),
     "pluq_nonzero": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _pi64]),
     "pluq_generic_counts": (ctypes.c_int, [_i64, _i64, _i64, _i64, _pi64]),
+    "pluq_rank_profile_replay": (ctypes.c_int, [_i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_iterative": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _pi64, _pi64, _pi64, _pi64]),
     "pluq_factor_batched": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p]),
@@ -125,12 +126,12 @@ class Context:
         return int(out.value)
 
     def stats(self) -> dict:
-        buf = (ctypes.c_int64 * 17)()
-        self.lib.pluq_last_stats(self.handle, buf, 17)
+        buf = (ctypes.c_int64 * 18)()
+        self.lib.pluq_last_stats(self.handle, buf, 18)
         keys = ["launches", "host_syncs", "nodes", "small_node_kernels", "basecase_kernels",
                 "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves", "speculative_ok",
                 "speculative_fail", "t_generic_ns", "t_fallback_ns", "t_tc_mma_ns",
-                "tc_timed_launches", "tc_timed_ns", "tc_timed_int8_ops"]
+                "tc_timed_launches", "tc_timed_ns", "tc_timed_int8_ops", "spec_repairs"]
         return dict(zip(keys, list(buf)))
 
     def measure_peaks(self) -> dict:

@@ -17,7 +17,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cmath>
 #include <cstdio>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -65,6 +72,74 @@ bool is_ident(const Perm& a) {
   return true;
 }
 
+// Persistent host worker pool of a context: run(n, fn) calls fn(0..n-1) on the workers and
+// the calling thread and returns when all are done.  Used by the host-buffer pipeline to
+// convert between the reference's storage dtypes and uint32 residues while DMA runs.
+class HostPool {
+ public:
+  explicit HostPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 0) return;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_.store(&fn);
+      n_.store(n);
+      done_ = 0;
+      next_.store(0);
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ >= n; });
+  }
+
+ private:
+  void work() {
+    int cnt = 0;
+    for (int i; (i = next_.fetch_add(1)) < n_.load();) {
+      (*fn_.load())(i);
+      ++cnt;
+    }
+    if (cnt) {
+      std::lock_guard<std::mutex> g(mu_);
+      done_ += cnt;
+      if (done_ >= n_.load()) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::atomic<const std::function<void(int)>*> fn_{nullptr};
+  std::atomic<int> n_{0}, next_{0};
+  int done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct pluq_ctx {
@@ -90,6 +165,7 @@ struct pluq_ctx {
   int64_t spec_panel = 1024; // outer panel width of the two-level speculative LU
   int64_t spec_panel_big = 2048;        // ... for nodes with at least spec_big_elems entries
   int64_t spec_big_elems = 1ll << 30;   // (cfg5 65536^2: 0.50 -> 0.42 s; cfg3 prefers 1024)
+  int64_t spec_repairs = 32;            // speculative LU: most zero pivots repaired by a column rotation
   int* d_zflags = nullptr;   // per-depth "node is nonzero" flags (deferred zero test)
   int* h_zflags = nullptr;
   static constexpr int kMaxDepth = 96;
@@ -124,10 +200,17 @@ struct pluq_ctx {
   int64_t check_inputs = 1;        // device inputs: range-check residues first (field.py:140-147 -> EINVAL)
   int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
   cudaMemPool_t pool = nullptr;    // the context's own stream-ordered pool (not the device default pool)
+  int64_t host_threads = 0;        // host-buffer pipeline: conversion threads (0 = hardware threads, <= 32)
+  int64_t host_chunk_mb = 64;      // host-buffer pipeline: uint32 bytes per pinned staging chunk
+  std::unique_ptr<HostPool> hpool;
+  char* ring = nullptr;            // pinned staging ring of the host-buffer pipeline (kRing chunks)
+  size_t ring_chunk = 0;
+  static constexpr int kRing = 4;
+  cudaEvent_t ring_ev[kRing] = {};
   float t_generic_ms = 0.f, t_fallback_ms = 0.f;
   // stats of the last factorization
   int64_t st_launch = 0, st_sync = 0, st_nodes = 0, st_small = 0, st_base = 0, st_tc = 0,
-          st_simt = 0, st_zero_skips = 0, st_generic = 0, st_spec_ok = 0, st_spec_fail = 0;
+          st_simt = 0, st_zero_skips = 0, st_generic = 0, st_spec_ok = 0, st_spec_fail = 0, st_repairs = 0;
   TcGemm tc;
   // host-batch pipeline resources, created once per context
   cudaStream_t side[6] = {};        // H2D, D2H, 4 exact-kernel streams
@@ -150,6 +233,29 @@ struct pluq_ctx {
       CU(cudaStreamSynchronize(stream));  // one-time; the table may be read from other streams
     }
     return d_invtab;
+  }
+
+  HostPool& host_pool() {
+    if (!hpool) {
+      int t = (int)host_threads;
+      if (t <= 0) t = (int)std::min<unsigned>(32u, std::max(1u, std::thread::hardware_concurrency()));
+      hpool.reset(new HostPool(std::max(0, t - 1)));
+    }
+    return *hpool;
+  }
+  char* staging_ring(size_t chunk_bytes) {
+    if (chunk_bytes > ring_chunk) {
+      if (ring) {
+        for (auto e : ring_ev) CU(cudaEventSynchronize(e));
+        CU(cudaFreeHost(ring));
+      }
+      ring = nullptr;
+      CU(cudaHostAlloc((void**)&ring, chunk_bytes * kRing, cudaHostAllocDefault));
+      ring_chunk = chunk_bytes;
+    }
+    for (auto& e : ring_ev)
+      if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return ring;
   }
 
   cudaStream_t* side_streams() {
@@ -176,7 +282,7 @@ struct pluq_ctx {
 
   void reset_stats() {
     st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok =
-        st_spec_fail = 0;
+        st_spec_fail = st_repairs = 0;
     tc.acc_launches = 0;
     tc.acc_ms = tc.acc_ops = 0.0;
   }
@@ -406,6 +512,16 @@ struct Ops {
     return *c->h_flag != 0;
   }
 
+  // Smallest column index of a nonzero entry of the 1 x n view (-1 if the row is zero).
+  int first_nonzero_col(const View& x) {
+    CU(cudaMemsetAsync(c->d_flag, 0x7f, sizeof(int), c->stream));
+    first_nonzero_kernel<<<(unsigned)std::max(1, std::min(148, (x.n + 255) / 256)), 256, 0, c->stream>>>(x, c->d_flag);
+    c->check_launch();
+    CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return *c->h_flag < x.n ? *c->h_flag : -1;
+  }
+
   // Launch the zero test of x into d_zflags[slot] without waiting for it.
   void nonzero_async(const View& x, int slot) {
     CU(cudaMemsetAsync(c->d_zflags + slot, 0, sizeof(int), c->stream));
@@ -494,6 +610,168 @@ struct NodeRes {
   Perm P, Q;
   int r;
 };
+
+// Block permutations S and T of Algorithm 1 (recursive.py:77-99) as index maps.
+static int s_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
+  const int a = r1 + r2, cc = r3 + r4, b = k - a;
+  if (x >= a && x < k) return x + cc;
+  if (x >= k && x < k + cc) return x - b;
+  return x;
+}
+static int t_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
+  if (x < r1) return x;
+  if (x < r1 + r2) return x + (k - r1);
+  if (x < r1 + r2 + r3) return x - r2;
+  if (x < r1 + r2 + r3 + r4) return x + (k + r2 - (r1 + r2 + r3));
+  if (x < k + r2 + r4) return x - (r2 + r4);
+  return x;
+}
+
+// Algorithm 1 (recursive.py:186-256) with the Algorithm 2 base case (iterative.py:23-91)
+// replayed SYMBOLICALLY on a rank profile matrix R_A, on the host, for any size.  The
+// device version for single-CTA blocks is sym_rec / sym_base (pluq_rpm.cuh), which states
+// the facts this rests on (tests/test_rpm_fallback.py): P, Q, rank and OpCounts of Alg.1 on
+// A equal those of Alg.1 on R_A; on a partial permutation every TRSM/GEMM of the recursion
+// is the identity on the pattern, so a node only reorders its row/column index lists by
+// its children's permutations.  Nodes without a pivot are the identity with no charges.
+struct SymHost {
+  const std::vector<int>& rp;  // original row -> original column of its one (-1: none)
+  const std::vector<int>& cp;  // original column -> original row (-1: none)
+  int thr;
+  Counts cnt{0, 0, 0, 0};
+  std::vector<int> rmark, cmark;  // stamp of the current node's row / column lists
+  std::vector<int> rpos, cpos;    // local position of an original row / column in a base case
+  int stamp = 0;
+
+  SymHost(const std::vector<int>& rp_, const std::vector<int>& cp_, int thr_)
+      : rp(rp_), cp(cp_), thr(thr_), rmark(rp_.size(), 0), cmark(cp_.size(), 0), rpos(rp_.size(), -1),
+        cpos(cp_.size(), -1) {}
+
+  bool has_pivot(const int* rows, const int* cols, int m, int n) {
+    ++stamp;
+    for (int b = 0; b < n; ++b) cmark[cols[b]] = stamp;
+    for (int a = 0; a < m; ++a) {
+      const int x = rp[rows[a]];
+      if (x >= 0 && cmark[x] == stamp) return true;
+    }
+    return false;
+  }
+
+  // Alg.2 frontier walk (the host twin of sym_base): P[local row] = position, Q[position]
+  // = local column, pivots first, then the rest in local order.
+  int base(const int* rows, const int* cols, int m, int n, int* P, int* Q) {
+    for (int a = 0; a < m; ++a) rpos[rows[a]] = a;
+    for (int b = 0; b < n; ++b) cpos[cols[b]] = b;
+    std::vector<int> lr(m, -1), lc(n, -1), ro, co;
+    for (int a = 0; a < m; ++a) {
+      const int x = rp[rows[a]];
+      if (x >= 0) {
+        const int q = cpos[x];
+        if (q >= 0 && q < n && cols[q] == x) lr[a] = q;
+      }
+    }
+    for (int b = 0; b < n; ++b) {
+      const int y = cp[cols[b]];
+      if (y >= 0) {
+        const int q = rpos[y];
+        if (q >= 0 && q < m && rows[q] == y) lc[b] = q;
+      }
+    }
+    int i = 0, j = 0;
+    while (i < m || j < n) {
+      int pr = -1, pc = -1;
+      if (j < n && lc[j] >= 0 && lc[j] < i) { pr = lc[j]; pc = j; ++j; }
+      else if (i < m && lr[i] >= 0 && lr[i] < j) { pr = i; pc = lr[i]; ++i; }
+      else if (i < m && j < n && lr[i] == j) { pr = i; pc = j; ++i; ++j; }
+      else { i = std::min(i + 1, m); j = std::min(j + 1, n); continue; }
+      ro.push_back(pr);
+      co.push_back(pc);
+    }
+    const int r = (int)ro.size();
+    for (int k = 0; k < r; ++k) {  // charges of iterative.py:59-75 per pivot
+      long long below = m - 1 - ro[k], right = n - 1 - co[k];
+      for (int t = 0; t < k; ++t) { below -= ro[t] > ro[k]; right -= co[t] > co[k]; }
+      if (below > 0) {
+        cnt.inv += 1; cnt.mul += below + below * right; cnt.add += below * right; cnt.red += below + below * right;
+      }
+    }
+    std::vector<int> rowpos(m, -1), colpos(n, -1);
+    for (int k = 0; k < r; ++k) { rowpos[ro[k]] = k; colpos[co[k]] = k; }
+    for (int x = 0, nxt = r; x < m; ++x) P[x] = rowpos[x] >= 0 ? rowpos[x] : nxt++;
+    for (int k = 0; k < r; ++k) Q[k] = co[k];
+    for (int x = 0, nxt = r; x < n; ++x) if (colpos[x] < 0) Q[nxt++] = x;
+    for (int a = 0; a < m; ++a) rpos[rows[a]] = -1;
+    for (int b = 0; b < n; ++b) cpos[cols[b]] = -1;
+    return r;
+  }
+
+  int rec(const int* rows, const int* cols, int m, int n, int* P, int* Q) {
+    if (m == 0 || n == 0 || !has_pivot(rows, cols, m, n)) {
+      for (int a = 0; a < m; ++a) P[a] = a;
+      for (int b = 0; b < n; ++b) Q[b] = b;
+      return 0;
+    }
+    if (m == 1 || n == 1 || std::min(m, n) <= thr) return base(rows, cols, m, n, P, Q);
+    const int kr = m / 2, kc = n / 2;
+    std::vector<int> P1(kr), Q1(kc);
+    const int r1 = rec(rows, cols, kr, kc, P1.data(), Q1.data());
+    std::vector<int> rt(kr), cl(kc);
+    for (int a = 0; a < kr; ++a) rt[P1[a]] = rows[a];
+    for (int t = 0; t < kc; ++t) cl[t] = cols[Q1[t]];
+    charge_trsm_l(cnt, r1, n - kc);
+    charge_trsm_u(cnt, m - kr, r1);
+    charge_mm(cnt, kr - r1, n - kc, r1);
+    charge_mm(cnt, m - kr, kc - r1, r1);
+    charge_mm(cnt, m - kr, n - kc, r1);
+    std::vector<int> P2(kr - r1), Q2(n - kc), P3(m - kr), Q3(kc - r1);
+    const int r2 = rec(rt.data() + r1, cols + kc, kr - r1, n - kc, P2.data(), Q2.data());
+    const int r3 = rec(rows + kr, cl.data() + r1, m - kr, kc - r1, P3.data(), Q3.data());
+    std::vector<int> hr(m - kr), hc(n - kc);
+    for (int a = 0; a < m - kr; ++a) hr[P3[a]] = rows[kr + a];
+    for (int t = 0; t < n - kc; ++t) hc[t] = cols[kc + Q2[t]];
+    const int m4 = m - kr - r3, n4 = n - kc - r2;
+    charge_trsm_u(cnt, r3, r2);
+    charge_trsm_l(cnt, r3, r2);
+    charge_trsm_u(cnt, m4, r2);
+    charge_trsm_l(cnt, r3, n4);
+    charge_mm(cnt, r3, n4, r2);
+    charge_mm(cnt, m4, n4, r2);
+    charge_mm(cnt, m4, n4, r3);
+    std::vector<int> P4(m4), Q4(n4);
+    const int r4 = rec(hr.data() + r3, hc.data() + r2, m4, n4, P4.data(), Q4.data());
+    for (int t = 0; t < m; ++t) {
+      int y;
+      if (t < kr) { const int z = P1[t]; y = z < r1 ? z : r1 + P2[z - r1]; }
+      else { const int z = P3[t - kr]; y = kr + (z < r3 ? z : r3 + P4[z - r3]); }
+      P[t] = s_sigma_h(y, r1, r2, r3, r4, kr);
+    }
+    for (int t = 0; t < n; ++t) {
+      const int z = t_sigma_h(t, r1, r2, r3, r4, kc);
+      int y;
+      if (z < kc) { const int w = z < r1 ? z : r1 + Q3[z - r1]; y = Q1[w]; }
+      else { const int zz = z - kc; const int w = zz < r2 ? zz : r2 + Q4[zz - r2]; y = kc + Q2[w]; }
+      Q[t] = y;
+    }
+    return r1 + r2 + r3 + r4;
+  }
+};
+
+// P (row -> position), Q (position -> column), rank and charges of Alg.1 on the m x n rank
+// profile matrix with ones at (prow[k], pcol[k]).
+static int symbolic_replay(int m, int n, int thr, const std::vector<int>& prow, const std::vector<int>& pcol,
+                           Perm& P, Perm& Q, Counts& cnt) {
+  std::vector<int> rp(m, -1), cp(n, -1);
+  for (size_t k = 0; k < prow.size(); ++k) { rp[prow[k]] = pcol[k]; cp[pcol[k]] = prow[k]; }
+  SymHost sh(rp, cp, thr);
+  std::vector<int> rows(m), cols(n);
+  for (int a = 0; a < m; ++a) rows[a] = a;
+  for (int b = 0; b < n; ++b) cols[b] = b;
+  P.assign(m, 0);
+  Q.assign(n, 0);
+  const int r = sh.rec(rows.data(), cols.data(), m, n, P.data(), Q.data());
+  cnt.mul += sh.cnt.mul; cnt.add += sh.cnt.add; cnt.inv += sh.cnt.inv; cnt.red += sh.cnt.red;
+  return r;
+}
 
 // Exact factorization of the blocks listed in fl/fc (every block of the grid when fl is
 // null): the rank-profile kernel (pluq_rpm.cuh) or the field-arithmetic recursion.
@@ -708,16 +986,17 @@ struct Driver {
   // against the oracle): no zero pivot, or a first zero pivot at global g after which
   // the whole Schur complement is zero (rank g).  On success P = Q = I and the node
   // holds the unique factors; otherwise the node is restored and the caller recurses.
-  bool speculative_lu(const View& x, int& rank) {
+  // Unpivoted blocked LU of x (see speculative_lu) run until its first zero pivot.  Returns
+  // g = min(m, n) if there was none; otherwise g < min(m, n) with x holding exactly the
+  // state after g pivots: [L11\U11, U12; L21, S], S = x[g:, g:] the Schur complement, whose
+  // (0, 0) entry is 0.
+  int spec_core(const View& x, int64_t panel_elems) {
     const int m = x.m, n = x.n, mn = std::min(m, n);
     const int BS = (int)c->spec_block;
     // very large nodes amortise a wider outer panel (fewer, longer-K trailing updates)
-    const int64_t panel = (c->spec_panel_big > 0 && (int64_t)m * n >= c->spec_big_elems) ? c->spec_panel_big
-                                                                                          : c->spec_panel;
+    const int64_t panel = (c->spec_panel_big > 0 && panel_elems >= c->spec_big_elems) ? c->spec_panel_big
+                                                                                       : c->spec_panel;
     const int W = std::max(BS, (int)(panel / BS) * BS);
-    uint32_t* backup = c->dalloc<uint32_t>((size_t)m * n);
-    View bk{backup, n, m, n};
-    ops.copy(bk, x);
     CU(cudaMemsetAsync(c->d_stop, 0, 4 * sizeof(int), c->stream));
     Ops sops = ops;
     sops.stop = c->d_stop;
@@ -838,12 +1117,10 @@ struct Driver {
       CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       c->sync();
     }
-    bool ok = true;
-    rank = mn;
-    if (c->h_stop[0]) {
+    if (!c->h_stop[0]) return mn;
+    {
       // first zero pivot at global g = k0 + t inside panel [ps, pe): finish the pivots
-      // [k0, g) inside the panel, then [ps, g) for the columns right of it, and require
-      // the whole Schur complement A[g:, g:] to vanish
+      // [k0, g) inside the panel, then [ps, g) for the columns right of it
       const int k0 = c->h_stop[1], t = c->h_stop[2], g = k0 + t;
       const int ps = (k0 / W) * W, pe = std::min(ps + W, mn);
       const int bs = std::min(BS, pe - k0);
@@ -857,17 +1134,80 @@ struct Driver {
         ops.trsm_l(x.sub(ps, ps, g - ps, g - ps), x.sub(ps, pe, g - ps, n - pe));
         ops.gemm(x.sub(g, pe, m - g, n - pe), x.sub(g, ps, m - g, g - ps), x.sub(ps, pe, g - ps, n - pe));
       }
-      ok = !ops.nonzero(x.sub(g, g, m - g, n - g));
-      rank = g;
+      return g;
     }
-    if (ok) {
+  }
+
+  // Speculative no-pivot LU of a whole node with local pivot REPAIR.  Success conditions
+  // (pinned against the oracle): the first zero pivot at g leaves a zero Schur complement
+  // (rank g, P = Q = I), or every zero pivot can be repaired by the row-order elimination
+  // that defines the rank profile matrix R_A (pluq_rpm.cuh phase a): at a zero pivot (g, g)
+  // with S != 0, row g's pivot is its leftmost nonzero column c (all columns < g are
+  // eliminated), so column c is rotated to position g (order-preserving, like the
+  // reference's rotations, so "leftmost" keeps meaning original order) and the LU resumes
+  // on the Schur complement.  The result is the unpivoted LU of A[:, sigma] with
+  // R_A = {(k, sigma[k])}; Alg.1 replayed symbolically on R_A (SymHost) must then give
+  // P = I and Q = sigma — by fact (2) the packed output is exactly the reference's — and
+  // its charges.  A row with no pivot (row g of S zero), too many repairs, or a replay that
+  // disagrees restores the node from the backup and the caller recurses exactly.
+  // Returns 0 = failed (x restored), 1 = generic (P = Q = I), 2 = repaired (p_out — empty
+  // for the identity — q and cnt set).
+  int speculative_lu(const View& x, int& rank, Perm& p_out, Perm& q, Counts& cnt) {
+    const int m = x.m, n = x.n, mn = std::min(m, n);
+    uint32_t* backup = c->dalloc<uint32_t>((size_t)m * n);
+    View bk{backup, n, m, n};
+    ops.copy(bk, x);
+    Perm sig = ident(n);
+    int g0 = 0, repairs = 0, res = 0;
+    for (;;) {
+      const int g = g0 + spec_core(x.sub(g0, g0, m - g0, n - g0), (int64_t)m * n);
+      if (g >= mn) { rank = mn; res = 1; break; }
+      if (!ops.nonzero(x.sub(g, g, m - g, n - g))) { rank = g; res = 1; break; }
+      if (repairs >= c->spec_repairs) break;
+      const int cpos = ops.first_nonzero_col(x.sub(g, g, 1, n - g));
+      if (cpos <= 0) break;  // row g has no pivot (rows would move): exact recursion
+      ++repairs;
+      Perm rot(cpos + 1);
+      rot[0] = cpos;
+      for (int j = 1; j <= cpos; ++j) rot[j] = j - 1;
+      ops.gather_cols(x.sub(0, g, m, cpos + 1), rot);
+      std::rotate(sig.begin() + g, sig.begin() + g + cpos, sig.begin() + g + cpos + 1);
+      g0 = g;
+    }
+    if (res == 1 && repairs > 0) {
+      std::vector<int> prow(rank), pcol(rank);
+      for (int k = 0; k < rank; ++k) { prow[k] = k; pcol[k] = sig[k]; }
+      Perm P, Q;
+      Counts sc{0, 0, 0, 0};
+      symbolic_replay(m, n, threshold, prow, pcol, P, Q, sc);
+      res = 2;
+      cnt = sc;
+      if (is_ident(P) && Q == sig) {
+        q = sig;
+      } else {
+        // Alg.1 orders these pivots differently from row order (e.g. a repair wider than
+        // one column inside a base case): R_A is still exact, so the packed output is the
+        // unpivoted LU of A' = A[P^-1][:, Q], whose leading minors 1..r are nonzero (fact 2):
+        // restore, permute, and factor A' without pivoting.
+        ops.copy(x, bk);
+        ops.gather_rows(x, inverse(P));
+        ops.gather_cols(x, Q);
+        const int g2 = spec_core(x, (int64_t)m * n);
+        if (g2 != rank || (g2 < mn && ops.nonzero(x.sub(g2, g2, m - g2, n - g2))))
+          throw PluqError(kCuda, "internal: LU of the rank-profile permuted node is not generic");
+        p_out = P;
+        q = Q;
+      }
+    }
+    if (res) {
       ++c->st_spec_ok;
+      c->st_repairs += repairs;
     } else {
       ops.copy(x, bk);
       ++c->st_spec_fail;
     }
     c->dfree(backup);
-    return ok;
+    return res;
   }
 
   bool spec_disabled = false;
@@ -881,9 +1221,16 @@ struct Driver {
     if (base) return leaf_global(x);
     if (c->try_generic && !spec_disabled) {
       int rk = 0;
-      if (speculative_lu(x, rk)) {
+      Perm pp, q;
+      Counts sc{0, 0, 0, 0};
+      const int how = speculative_lu(x, rk, pp, q, sc);
+      if (how == 1) {
         generic_counts_rec(m, n, rk, threshold, host_counts);
         return NodeRes{ident(m), ident(n), rk};
+      }
+      if (how == 2) {
+        host_counts.mul += sc.mul; host_counts.add += sc.add; host_counts.inv += sc.inv; host_counts.red += sc.red;
+        return NodeRes{pp.empty() ? ident(m) : pp, q, rk};
       }
       spec_disabled = true;  // non-generic node: do not speculate again inside its subtree
       NodeRes res = rec_exact(x);
@@ -1015,20 +1362,6 @@ struct Driver {
     return out;
   }
 
-  static int s_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
-    int a = r1 + r2, cc = r3 + r4, b = k - a;
-    if (x >= a && x < k) return x + cc;
-    if (x >= k && x < k + cc) return x - b;
-    return x;
-  }
-  static int t_sigma_h(int x, int r1, int r2, int r3, int r4, int k) {
-    if (x < r1) return x;
-    if (x < r1 + r2) return x + (k - r1);
-    if (x < r1 + r2 + r3) return x - r2;
-    if (x < r1 + r2 + r3 + r4) return x + (k + r2 - (r1 + r2 + r3));
-    if (x < k + r2 + r4) return x - (r2 + r4);
-    return x;
-  }
 };
 
 int validate(int64_t m, int64_t n, int64_t p) {
@@ -1177,6 +1510,9 @@ int pluq_destroy(pluq_ctx* c) {
   c->tc.release();
   if (c->pin) cudaFreeHost(c->pin);
   if (c->h_bres) cudaFreeHost(c->h_bres);
+  if (c->ring) cudaFreeHost(c->ring);
+  for (auto e : c->ring_ev) if (e) cudaEventDestroy(e);
+  c->hpool.reset();
   for (auto e : c->evpool) cudaEventDestroy(e);
   for (auto s : c->side) if (s) cudaStreamDestroy(s);
   if (c->d_res) cudaFree(c->d_res);
@@ -1221,7 +1557,9 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(rpm_eager, c->rpm_eager) X(tc_trsm_min, c->tc_trsm_min) X(trace_pipeline, c->trace_pipeline)    \
   X(spec_block, c->spec_block) X(spec_check, c->spec_check) X(spec_panel, c->spec_panel)            \
   X(spec_panel_big, c->spec_panel_big) X(spec_big_elems, c->spec_big_elems)                         \
-  X(check_inputs, c->check_inputs) X(pool_keep_mb, c->pool_keep_mb)
+  X(spec_repairs, c->spec_repairs)                                                                  \
+  X(check_inputs, c->check_inputs) X(pool_keep_mb, c->pool_keep_mb) X(host_chunk_mb, c->host_chunk_mb)     \
+  X(host_threads, c->host_threads)
 
 int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return kInvalid;
@@ -1257,6 +1595,35 @@ int pluq_nonzero(pluq_ctx* c, const uint32_t* dA, int64_t ld, int64_t m, int64_t
     Ops ops{c, ModP::make(2)};
     *out = (m > 0 && n > 0) ? (ops.nonzero(View{const_cast<uint32_t*>(dA), ld, (int)m, (int)n}) ? 1 : 0) : 0;
   });
+}
+
+int pluq_rank_profile_replay(int64_t m, int64_t n, int64_t threshold, int64_t r, const int64_t* prow,
+                             const int64_t* pcol, int64_t* p_sigma, int64_t* q_sigma, int64_t* counts) {
+  if (m < 0 || n < 0 || m > INT32_MAX / 2 || n > INT32_MAX / 2 || threshold < 1 || r < 0 || r > std::min(m, n))
+    return kInvalid;
+  if ((r && (!prow || !pcol)) || (m && !p_sigma) || (n && !q_sigma)) return kInvalid;
+  try {
+    std::vector<int> pr(r), pc(r), seen_r(m, 0), seen_c(n, 0);
+    for (int64_t k = 0; k < r; ++k) {
+      if (prow[k] < 0 || prow[k] >= m || pcol[k] < 0 || pcol[k] >= n || seen_r[prow[k]]++ || seen_c[pcol[k]]++)
+        return kInvalid;  // not a partial permutation
+      pr[k] = (int)prow[k];
+      pc[k] = (int)pcol[k];
+    }
+    Perm P, Q;
+    Counts cnt{0, 0, 0, 0};
+    const int rank = symbolic_replay((int)m, (int)n, (int)std::min<int64_t>(threshold, INT32_MAX), pr, pc, P, Q, cnt);
+    if (rank != r) return kInvalid;
+    for (int64_t i = 0; i < m; ++i) p_sigma[i] = P[i];
+    for (int64_t j = 0; j < n; ++j) q_sigma[j] = Q[j];
+    if (counts) {
+      counts[0] = (int64_t)cnt.mul; counts[1] = (int64_t)cnt.add; counts[2] = (int64_t)cnt.inv;
+      counts[3] = (int64_t)cnt.red;
+    }
+    return kOk;
+  } catch (const std::bad_alloc&) {
+    return kNoMemory;
+  }
 }
 
 int pluq_check_residues(pluq_ctx* c, const uint32_t* dA, int64_t ld, int64_t m, int64_t n, int64_t p) {
@@ -1326,12 +1693,12 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[17] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+  int64_t v[18] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
                    c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail,
                    (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f),
                    (int64_t)(c->tc.mma_ms * 1e6f), c->tc.acc_launches, (int64_t)(c->tc.acc_ms * 1e6),
-                   (int64_t)c->tc.acc_ops};
-  for (int64_t i = 0; i < nout && i < 17; ++i) out[i] = v[i];
+                   (int64_t)c->tc.acc_ops, c->st_repairs};
+  for (int64_t i = 0; i < nout && i < 18; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -1462,6 +1829,40 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
   });
 }
 
+// Host dtype <-> uint32 residues on host threads (the reference's storage dtype: float64
+// when (p-1)^2 * 8192 <= 2^53, else int64; field.py:75-81).  to_u32 returns false if an entry
+// is not a canonical residue (field.py:140-147).
+static bool host_to_u32(const void* src, bool is_f64, uint32_t* dst, int64_t count, uint32_t p) {
+  bool ok = true;
+  if (is_f64) {
+    const double* s = static_cast<const double*>(src);
+    for (int64_t i = 0; i < count; ++i) {
+      const double v = s[i];
+      const bool good = v >= 0.0 && v < (double)p && v == std::floor(v);
+      dst[i] = good ? (uint32_t)v : 0u;
+      ok &= good;
+    }
+  } else {
+    const int64_t* s = static_cast<const int64_t*>(src);
+    for (int64_t i = 0; i < count; ++i) {
+      const int64_t v = s[i];
+      const bool good = v >= 0 && v < (int64_t)p;
+      dst[i] = good ? (uint32_t)v : 0u;
+      ok &= good;
+    }
+  }
+  return ok;
+}
+static void host_from_u32(const uint32_t* src, bool is_f64, void* dst, int64_t count) {
+  if (is_f64) {
+    double* d = static_cast<double*>(dst);
+    for (int64_t i = 0; i < count; ++i) d[i] = (double)src[i];
+  } else {
+    int64_t* d = static_cast<int64_t*>(dst);
+    for (int64_t i = 0; i < count; ++i) d[i] = (int64_t)src[i];
+  }
+}
+
 static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n, int64_t p, int64_t threshold,
                        int64_t* psig, int64_t* qsig, int64_t* rank, int64_t* counts) {
   if (threshold < 1) return kInvalid;
@@ -1469,32 +1870,102 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
   if (!rank || (m && !psig) || (n && !qsig)) return kInvalid;
   return guarded(c, [&] {
     const int64_t cnt = m * n;
-    void* raw = c->dalloc<char>((size_t)cnt * 8);
-    uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
-    if (cnt) CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
-    if (cnt) {
-      CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
-      if (is_f64) from_f64_kernel<<<grid, 256, 0, c->stream>>>((const double*)raw, dA, cnt, (uint32_t)p, c->d_flag);
-      else from_i64_kernel<<<grid, 256, 0, c->stream>>>((const int64_t*)raw, dA, cnt, (uint32_t)p, c->d_flag);
-      c->check_launch();
-      CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      c->sync();
-      if (*c->h_flag) {  // nothing was modified: the host buffer is only written at the end
-        c->dfree(dA);
-        c->dfree(raw);
-        throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+    const size_t chunk = (size_t)std::max<int64_t>(1, c->host_chunk_mb) << 20;  // bytes of uint32 per chunk
+    if ((size_t)cnt * 4 <= chunk) {
+      // small matrix: one pageable copy in the host dtype, converted on the device
+      void* raw = c->dalloc<char>((size_t)cnt * 8);
+      uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+      if (cnt) CU(cudaMemcpyAsync(raw, hA, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
+      int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (cnt + 255) / 256));
+      if (cnt) {
+        CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+        if (is_f64) from_f64_kernel<<<grid, 256, 0, c->stream>>>((const double*)raw, dA, cnt, (uint32_t)p, c->d_flag);
+        else from_i64_kernel<<<grid, 256, 0, c->stream>>>((const int64_t*)raw, dA, cnt, (uint32_t)p, c->d_flag);
+        c->check_launch();
+        CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (*c->h_flag) {  // nothing was modified: the host buffer is only written at the end
+          c->dfree(dA);
+          c->dfree(raw);
+          throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+        }
       }
+      factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
+      if (cnt) {
+        if (is_f64) to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA, (double*)raw, cnt);
+        else to_i64_kernel<<<grid, 256, 0, c->stream>>>(dA, (int64_t*)raw, cnt);
+        c->check_launch();
+        CU(cudaMemcpyAsync(hA, raw, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+      }
+      c->dfree(dA);
+      c->dfree(raw);
+      c->sync();
+      return;
+    }
+    // Large matrix: a chunked pipeline through a pinned ring.  Host threads convert the
+    // caller's float64/int64 rows to uint32 residues (checking them) while the previous
+    // chunks are in flight, so PCIe carries 4 bytes per entry instead of 8; on the way back
+    // D2H of later chunks overlaps the widening of earlier ones.  The caller's buffer is
+    // written only after the factorization, so invalid input leaves it untouched.
+    const size_t ce = chunk / 4;                                   // entries per chunk
+    const int64_t nch = (cnt + (int64_t)ce - 1) / (int64_t)ce;
+    char* ring = c->staging_ring(chunk);
+    HostPool& hp = c->host_pool();
+    const int parts = hp.size() * 2;
+    uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+    cudaStream_t* ss = c->side_streams();
+    cudaStream_t sin = ss[0], sout = ss[1];
+    cudaEvent_t* ev = c->ring_ev;
+    cudaEvent_t* je = c->events(2);
+    CU(cudaEventRecord(je[0], c->stream));  // dA's allocation is ordered before the copies
+    CU(cudaStreamWaitEvent(sin, je[0], 0));
+    const size_t esz = 8;  // float64 and int64 alike
+    std::atomic<bool> ok{true};
+    for (int64_t k = 0; k < nch; ++k) {
+      const int s = (int)(k % pluq_ctx::kRing);
+      if (k >= pluq_ctx::kRing) CU(cudaEventSynchronize(ev[s]));  // the slot's previous copy is done
+      const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
+      uint32_t* slot = reinterpret_cast<uint32_t*>(ring + (size_t)s * chunk);
+      const char* src = static_cast<const char*>(hA) + (size_t)e0 * esz;
+      hp.run(parts, [&](int t) {
+        const int64_t a = ne * t / parts, b = ne * (t + 1) / parts;
+        if (!host_to_u32(src + (size_t)a * esz, is_f64, slot + a, b - a, (uint32_t)p)) ok.store(false);
+      });
+      CU(cudaMemcpyAsync(dA + e0, slot, (size_t)ne * 4, cudaMemcpyHostToDevice, sin));
+      CU(cudaEventRecord(ev[s], sin));
+    }
+    CU(cudaEventRecord(je[1], sin));
+    CU(cudaStreamWaitEvent(c->stream, je[1], 0));
+    if (!ok.load()) {
+      c->dfree(dA);
+      c->sync();
+      throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
     }
     factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
-    if (cnt) {
-      if (is_f64) to_f64_kernel<<<grid, 256, 0, c->stream>>>(dA, (double*)raw, cnt);
-      else to_i64_kernel<<<grid, 256, 0, c->stream>>>(dA, (int64_t*)raw, cnt);
-      c->check_launch();
-      CU(cudaMemcpyAsync(hA, raw, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaEventRecord(je[0], c->stream));
+    CU(cudaStreamWaitEvent(sout, je[0], 0));
+    auto issue = [&](int64_t k) {
+      const int s = (int)(k % pluq_ctx::kRing);
+      const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
+      CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dA + e0, (size_t)ne * 4, cudaMemcpyDeviceToHost, sout));
+      CU(cudaEventRecord(ev[s], sout));
+    };
+    for (int64_t k = 0; k < std::min<int64_t>(nch, pluq_ctx::kRing); ++k) issue(k);
+    for (int64_t k = 0; k < nch; ++k) {
+      const int s = (int)(k % pluq_ctx::kRing);
+      CU(cudaEventSynchronize(ev[s]));
+      const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
+      const uint32_t* slot = reinterpret_cast<const uint32_t*>(ring + (size_t)s * chunk);
+      char* dst = static_cast<char*>(hA) + (size_t)e0 * esz;
+      hp.run(parts, [&](int t) {
+        const int64_t a = ne * t / parts, b = ne * (t + 1) / parts;
+        host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
+      });
+      if (k + pluq_ctx::kRing < nch) issue(k + pluq_ctx::kRing);
     }
+    CU(cudaEventRecord(je[1], sout));
+    CU(cudaStreamWaitEvent(c->stream, je[1], 0));
     c->dfree(dA);
-    c->dfree(raw);
     c->sync();
   });
 }

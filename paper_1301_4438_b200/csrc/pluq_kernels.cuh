@@ -1118,6 +1118,17 @@ __global__ void tmp_to_cols_kernel(View x, const int* dst, int nmv, const uint32
   }
 }
 
+// *out <- min(*out, smallest column of a nonzero in row 0 of x) (pivot repair of the
+// speculative LU: row-order elimination picks the leftmost nonzero, pluq_rpm.cuh phase a).
+__global__ void first_nonzero_kernel(View x, int* out) {
+  int best = 0x7fffffff;
+  const uint32_t* r = x.row(0);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x)
+    if (r[j] != 0u) { best = j; break; }
+  for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != 0x7fffffff) atomicMin(out, best);
+}
+
 // flag <- 1 if the block holds any nonzero (zero-block short-circuit).
 __global__ void nonzero_kernel(View x, int* flag) {
   bool nz = false;

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < kblocks; ++kb, ++g) {
         const uint32_t s = g % STAGES;
         mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
-        if (dbg == 1 && g >= (uint32_t)STAGES) {  // diagnostics: MMA rate without operand traffic
+        if ((dbg & 1) && g >= (uint32_t)STAGES) {  // diagnostics: MMA rate without operand traffic
           mbar_arrive(&full[s]);
           continue;
         }
@@ -371,6 +371,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
+      if (dbg & 2) {  // diagnostics: MMA + operand feed rate without the epilogue
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        continue;
+      }
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
       if constexpr (NBUF == 1 && NCH <= 4) {
         // single accumulator set: drain TMEM into registers first and release it, so the
@@ -555,7 +560,7 @@ struct TcGemm {
   bool attrs_set[2][2][5] = {};
   int variant = 1;              // TcCfg variant (option tc_cfg)
   int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
-  int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring
+  int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring, 2 = skip the epilogue
   int vec_limbs = 1;            // vectorised limb-split kernels (option tc_vec)
   int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
   int mn_b = 1;                 // option tc_mnb: MN-major B operand when the tile allows it (no transpose)

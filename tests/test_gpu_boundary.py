@@ -133,3 +133,38 @@ def test_streaming_batch_non_64_blocks_bounded_time(pb, m, n):
     for b in list(range(0, 1536, 97)) + [1, 500, 1535]:
         P, Q, r, _ = orc.pluq(host[b].astype(np.float64), p, 30)
         assert int(res.ranks[b]) == r and np.array_equal(res.p_sigma[b].cpu().numpy(), P)
+
+
+@pytest.mark.parametrize("p,dtype", [(65521, np.float64), (8388593, np.int64)])
+def test_host_pipeline_chunks_vs_oracle(pb, p, dtype):
+    """Large host matrices go through the pinned-ring pipeline (host threads convert to
+    uint32 while DMA runs); 1 MiB chunks force several chunks, a partial last one and
+    ring-slot reuse at a size the oracle checks quickly."""
+    from paper_1301_4438_b200 import _native
+
+    ctx = _native.context()
+    old = ctx.get_option("host_chunk_mb")
+    ctx.set_option("host_chunk_mb", 1)
+    try:
+        a0 = orc.gen_xy_rank(1000, 1100, 700, p, 3)
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(dtype))
+        assert a.data.dtype == dtype
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        x = a0.astype(orc.field_dtype(p))
+        cc = orc.Counts()
+        P, Q, r, _ = orc.pluq(x, p, 30, cc)
+        assert f.rank == r and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+        assert np.array_equal(a.data, x) and f.packed is a
+        assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+        # invalid entry in the LAST chunk: EINVAL, buffer untouched
+        bad = a0.astype(dtype)
+        bad[-1, -1] = p
+        keep = bad.copy()
+        psig = np.zeros(1000, np.int64); qsig = np.zeros(1100, np.int64); rank = np.zeros(1, np.int64)
+        fn = ctx.lib.pluq_factor_host_f64 if dtype == np.float64 else ctx.lib.pluq_factor_host_i64
+        st = fn(ctx.handle, bad.ctypes.data, 1000, 1100, p, 30, _native.i64p(psig), _native.i64p(qsig),
+                _native.i64p(rank), None)
+        assert st == _native.PLUQ_EINVAL and np.array_equal(bad, keep)
+    finally:
+        ctx.set_option("host_chunk_mb", old)

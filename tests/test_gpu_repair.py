@@ -1,0 +1,126 @@
+"""Pivot repair of the speculative LU on large nodes (csrc/pluq_driver.cu speculative_lu).
+
+A leading minor that vanishes by coincidence (probability ~ r/p per matrix: the seed-0
+cfg5 input has one, at pivot 11148) used to send the whole node to the exact recursion.
+Now the zero pivot is repaired by the row-order elimination that defines R_A (the
+leftmost nonzero column of the pivot row is rotated into place) and Alg.1 is replayed
+symbolically on R_A for P, Q and the OpCounts.  Every case is compared bit for bit with the
+oracle (P, Q, rank, packed, OpCounts)."""
+
+import numpy as np
+import pytest
+
+from oracle import pluq_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb(cuda_ok):
+    import paper_1301_4438_b200 as mod
+    from paper_1301_4438_b200 import _native
+
+    _native.load_library()
+    return mod
+
+
+def _vanish(a, g, width, p, rng):
+    """Make the leading minors g+1 .. g+width of a vanish in the first `width` columns of
+    row g: row g restricted to columns :g+width = a combination of the rows above."""
+    coef = rng.integers(0, p, g).astype(object)
+    a[g, :g + width] = np.array((coef @ a[:g, :g + width].astype(object)) % p, dtype=np.int64)
+
+
+CASES = [
+    # name, m, n, rank or None, [(g, width)], p
+    ("mid_block", 400, 420, None, [(57, 1)], 65521),
+    ("block_edge", 400, 400, None, [(127, 1)], 65521),
+    ("block_start", 400, 400, None, [(128, 1)], 65521),
+    ("panel_edge", 600, 640, None, [(255, 1)], 65521),
+    ("second_panel", 600, 600, None, [(300, 1)], 65521),
+    ("two", 520, 500, None, [(40, 1), (333, 1)], 65521),
+    ("wide_gap", 300, 360, None, [(90, 3)], 65521),
+    ("near_end", 300, 300, None, [(297, 1)], 65521),
+    ("rank_deficient", 420, 400, 250, [(100, 1)], 65521),
+    ("p23", 360, 380, None, [(70, 1)], 8388593),
+    ("small_p", 300, 300, None, [(20, 1)], 1009),
+]
+
+
+def _make(name, m, n, r, gs, p):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.integers(0, p, (m, n)) if r is None else orc.gen_xy_rank(m, n, r, p, 5)
+    a = np.asarray(a, np.int64)
+    for g, w in gs:
+        _vanish(a, g, w, p, rng)
+    return a
+
+
+@pytest.mark.parametrize("opts", [dict(small_cap=1, spec_panel=256),
+                                  dict(small_cap=1, spec_block=16, spec_panel=48, spec_check=3)],
+                         ids=["blocks128", "blocks16"])
+@pytest.mark.parametrize("name,m,n,r,gs,p", CASES, ids=[c[0] for c in CASES])
+def test_repair_vs_oracle(pb, opts, name, m, n, r, gs, p):
+    from paper_1301_4438_b200 import _native
+
+    a0 = _make(name, m, n, r, gs, p)
+    x = a0.astype(orc.field_dtype(p))
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(orc.field_dtype(p)))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert f.rank == R
+    assert np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+    # the top node was finished by the repaired speculative LU, not the exact recursion
+    assert st["spec_repairs"] >= 1 and st["speculative_fail"] == 0, st
+
+
+def test_repair_disabled_falls_back(pb):
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    a0 = _make("mid_block", 400, 420, None, [(57, 1)], p)
+    x = a0.astype(np.float64)
+    P, Q, R, _ = orc.pluq(x, p, 30, orc.Counts())
+    ctx = _native.context()
+    ctx.set_option("small_cap", 1)
+    ctx.set_option("spec_repairs", 0)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64))
+        f = pb.pluq(a)
+        st = pb.last_stats()
+    finally:
+        ctx.set_option("small_cap", 128 * 128)
+        ctx.set_option("spec_repairs", 32)
+    assert st["speculative_fail"] >= 1 and st["spec_repairs"] == 0
+    assert f.rank == R and np.array_equal(f.q_perm.sigma, Q) and np.array_equal(a.data, x)
+
+
+def test_cfg5_seed0_full_size_repaired(pb):
+    """The headline input itself (65536^2, rank 32768, seed 0): one coincidence at pivot
+    11148, repaired; Q swaps columns 11148/11149 (the reference's rank profile), P = I."""
+    import torch
+    from paper_1301_4438_b200 import gen, verify
+
+    a5 = gen.gen_cfg5_device(seed=0)
+    f = pb.pluq(pb.DenseMatrix(pb.PrimeField(65521), a5.clone()))
+    st = pb.last_stats()
+    assert f.rank == 32768 and st["spec_repairs"] == 1 and st["speculative_fail"] == 0
+    q = np.arange(65536)
+    q[11148], q[11149] = 11149, 11148
+    assert np.array_equal(f.p_perm.sigma, np.arange(65536)) and np.array_equal(f.q_perm.sigma, q)
+    assert verify.structure_ok(f) and verify.freivalds(a5, f, probes=2)
+    del a5, f
+    torch.cuda.empty_cache()
