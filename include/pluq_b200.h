@@ -44,6 +44,9 @@ typedef struct pluq_ctx pluq_ctx;
 int pluq_create(pluq_ctx** ctx, int device, void* stream);
 int pluq_destroy(pluq_ctx* ctx);
 int pluq_set_stream(pluq_ctx* ctx, void* stream);
+/* Frees the context's kept device workspace: the node backup of the speculative LU
+ * (m*n*2 bytes for p < 2^16, else m*n*4, kept between calls) and the pool's free blocks. */
+int pluq_release_workspace(pluq_ctx* ctx);
 /* Tuning knobs (0 = keep default): largest node m*n handled whole by one CTA in
  * shared memory, and whether the tensor-core GEMM may be used (1/0). */
 int pluq_set_option(pluq_ctx* ctx, const char* key, int64_t value);

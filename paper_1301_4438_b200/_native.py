@@ -25,6 +25,7 @@ SIGNATURES = {
     "pluq_create": (ctypes.c_int, [ctypes.POINTER(_p), ctypes.c_int, _p]),
     "pluq_destroy": (ctypes.c_int, [_p]),
     "pluq_set_stream": (ctypes.c_int, [_p, _p]),
+    "pluq_release_workspace": (ctypes.c_int, [_p]),
     "pluq_set_option": (ctypes.c_int, [_p, ctypes.c_char_p, _i64]),
     "pluq_get_option": (ctypes.c_int, [_p, ctypes.c_char_p, _pi64]),
     "pluq_check_residues": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64]),

@@ -203,6 +203,21 @@ struct pluq_ctx {
   int64_t host_threads = 0;        // host-buffer pipeline: conversion threads (0 = hardware threads, <= 32)
   int64_t host_chunk_mb = 64;      // host-buffer pipeline: uint32 bytes per pinned staging chunk
   std::unique_ptr<HostPool> hpool;
+  // backup of a large node for the speculative LU (restored on failure): kept across calls
+  // (one node-sized buffer; 2 bytes per entry when p < 2^16), freed by pluq_release_workspace
+  void* node_backup = nullptr;
+  size_t node_backup_bytes = 0;
+  void* backup_buffer(size_t bytes) {
+    if (bytes > node_backup_bytes) {
+      sync();
+      if (node_backup) CU(cudaFree(node_backup));
+      node_backup = nullptr;
+      node_backup_bytes = 0;
+      CU(cudaMalloc(&node_backup, bytes));
+      node_backup_bytes = bytes;
+    }
+    return node_backup;
+  }
   char* ring = nullptr;            // pinned staging ring of the host-buffer pipeline (kRing chunks)
   size_t ring_chunk = 0;
   static constexpr int kRing = 4;
@@ -530,6 +545,18 @@ struct Ops {
     c->check_launch();
   }
 
+  void copy_to16(uint16_t* dst, const View& src) {
+    if (src.m == 0 || src.n == 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ((int64_t)src.m * src.n / 4 + 255) / 256));
+    copy_to16_kernel<<<grid, 256, 0, c->stream>>>(dst, src);
+    c->check_launch();
+  }
+  void copy_from16(const View& dst, const uint16_t* src) {
+    if (dst.m == 0 || dst.n == 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ((int64_t)dst.m * dst.n / 4 + 255) / 256));
+    copy_from16_kernel<<<grid, 256, 0, c->stream>>>(dst, src);
+    c->check_launch();
+  }
   void copy(const View& dst, const View& src) {
     if (dst.m == 0 || dst.n == 0) return;
     dim3 grid((dst.n + 255) / 256, grid_rows(dst.m));
@@ -1154,9 +1181,12 @@ struct Driver {
   // for the identity — q and cnt set).
   int speculative_lu(const View& x, int& rank, Perm& p_out, Perm& q, Counts& cnt) {
     const int m = x.m, n = x.n, mn = std::min(m, n);
-    uint32_t* backup = c->dalloc<uint32_t>((size_t)m * n);
-    View bk{backup, n, m, n};
-    ops.copy(bk, x);
+    const bool b16 = mp.p <= 65536u;  // residues fit 16 bits: half the backup traffic
+    void* backup = c->backup_buffer((size_t)m * n * (b16 ? 2 : 4));
+    View bk{static_cast<uint32_t*>(backup), n, m, n};
+    auto save = [&]() { b16 ? ops.copy_to16(static_cast<uint16_t*>(backup), x) : ops.copy(bk, x); };
+    auto restore = [&]() { b16 ? ops.copy_from16(x, static_cast<const uint16_t*>(backup)) : ops.copy(x, bk); };
+    save();
     Perm sig = ident(n);
     int g0 = 0, repairs = 0, res = 0;
     for (;;) {
@@ -1189,7 +1219,7 @@ struct Driver {
         // one column inside a base case): R_A is still exact, so the packed output is the
         // unpivoted LU of A' = A[P^-1][:, Q], whose leading minors 1..r are nonzero (fact 2):
         // restore, permute, and factor A' without pivoting.
-        ops.copy(x, bk);
+        restore();
         ops.gather_rows(x, inverse(P));
         ops.gather_cols(x, Q);
         const int g2 = spec_core(x, (int64_t)m * n);
@@ -1203,10 +1233,9 @@ struct Driver {
       ++c->st_spec_ok;
       c->st_repairs += repairs;
     } else {
-      ops.copy(x, bk);
+      restore();
       ++c->st_spec_fail;
     }
-    c->dfree(backup);
     return res;
   }
 
@@ -1511,6 +1540,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->pin) cudaFreeHost(c->pin);
   if (c->h_bres) cudaFreeHost(c->h_bres);
   if (c->ring) cudaFreeHost(c->ring);
+  if (c->node_backup) cudaFree(c->node_backup);
   for (auto e : c->ring_ev) if (e) cudaEventDestroy(e);
   c->hpool.reset();
   for (auto e : c->evpool) cudaEventDestroy(e);
@@ -1535,6 +1565,16 @@ int pluq_destroy(pluq_ctx* c) {
   return kOk;
 }
 
+int pluq_release_workspace(pluq_ctx* c) {
+  return guarded(c, [&] {
+    c->sync();
+    if (c->node_backup) CU(cudaFree(c->node_backup));
+    c->node_backup = nullptr;
+    c->node_backup_bytes = 0;
+    if (c->pool) CU(cudaMemPoolTrimTo(c->pool, 0));
+  });
+}
+
 int pluq_set_stream(pluq_ctx* c, void* stream) {
   if (!c) return kInvalid;
   c->stream = (cudaStream_t)stream;
@@ -1547,7 +1587,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(use_tc, c->use_tc) X(tc_min_dim, c->tc_min_dim) X(tc_min_k, c->tc_min_k)                        \
   X(tc_k_pass, c->tc.k_pass_override) X(tc_cfg, c->tc.variant) X(tc_mnb, c->tc.mn_b)               \
   X(tc_group, c->tc.raster_group) X(tc_cpf, c->tc.c_prefetch) X(tc_grid, c->tc.grid_override)      \
-  X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma)                        \
+  X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma) X(tc_epi, c->tc.epi_warps)  \
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \

@@ -1130,13 +1130,65 @@ __global__ void first_nonzero_kernel(View x, int* out) {
 }
 
 // flag <- 1 if the block holds any nonzero (zero-block short-circuit).
+// 16-byte loads when rows allow it; blocks stop early once any block has set the flag (a
+// nonzero Schur complement is usually nonzero right at its first rows).
 __global__ void nonzero_kernel(View x, int* flag) {
   bool nz = false;
+  const bool vec = (x.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x.a) & 15) == 0;
+  const int n4 = vec ? x.n / 4 : 0;
   for (int i = blockIdx.y; i < x.m; i += gridDim.y) {
     const uint32_t* xr = x.row(i);
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) nz |= xr[j] != 0u;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += gridDim.x * blockDim.x) {
+      const uint4 q = reinterpret_cast<const uint4*>(xr)[j];
+      nz |= (q.x | q.y | q.z | q.w) != 0u;
+    }
+    for (int j = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) nz |= xr[j] != 0u;
+    if (((i - blockIdx.y) / gridDim.y & 7) == 7) {  // every 8 rows: stop if anyone found a nonzero
+      if (__syncthreads_or(nz) || *reinterpret_cast<volatile int*>(flag)) {
+        if (threadIdx.x == 0) atomicOr(flag, 1);
+        return;
+      }
+    }
   }
   if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// Compact node backup (p < 2^16): residues stored as uint16, rows packed (pitch = n).
+// 16-byte loads / 8-byte stores when the rows allow it (HBM-bound: 6 bytes per entry).
+__device__ __forceinline__ bool rows16_vec(const View& v) {
+  return (v.ld % 4) == 0 && (v.n % 4) == 0 && (reinterpret_cast<uintptr_t>(v.a) & 15) == 0;
+}
+__global__ void copy_to16_kernel(uint16_t* dst, View src) {
+  if (rows16_vec(src)) {
+    const int64_t nq = src.n / 4, total = (int64_t)src.m * nq;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = t / nq, q = t - i * nq;
+      const uint4 v = reinterpret_cast<const uint4*>(src.a + i * src.ld)[q];
+      reinterpret_cast<uint2*>(dst + i * src.n)[q] = make_uint2(v.x | (v.y << 16), v.z | (v.w << 16));
+    }
+    return;
+  }
+  const int64_t total = (int64_t)src.m * src.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / src.n, j = t - i * src.n;
+    dst[t] = (uint16_t)src.a[i * src.ld + j];
+  }
+}
+__global__ void copy_from16_kernel(View dst, const uint16_t* src) {
+  if (rows16_vec(dst)) {
+    const int64_t nq = dst.n / 4, total = (int64_t)dst.m * nq;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = t / nq, q = t - i * nq;
+      const uint2 v = reinterpret_cast<const uint2*>(src + i * dst.n)[q];
+      reinterpret_cast<uint4*>(dst.a + i * dst.ld)[q] = make_uint4(v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16);
+    }
+    return;
+  }
+  const int64_t total = (int64_t)dst.m * dst.n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / dst.n, j = t - i * dst.n;
+    dst.a[i * dst.ld + j] = src[t];
+  }
 }
 
 __global__ void copy_view_kernel(View dst, View src) {

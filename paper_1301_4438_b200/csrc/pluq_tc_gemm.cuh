@@ -140,27 +140,41 @@ template <> struct TcCfg<1, 1> { static constexpr int BN = 256, STAGES = 4, NBUF
 template <> struct TcCfg<2, 1> { static constexpr int BN = 128, STAGES = 3, NBUF = 1; };
 template <> struct TcCfg<3, 1> { static constexpr int BN = 96, STAGES = 2, NBUF = 1; };
 template <> struct TcCfg<4, 1> { static constexpr int BN = 64, STAGES = 2, NBUF = 1; };
+// V = 2 (two-limb primes, MN-major B): two passes per tile, see tc_modgemm2p_kernel.
+template <> struct TcCfg<2, 2> { static constexpr int BN = 128, STAGES = 4, NBUF = 1; };
 
 constexpr int TC_BM = 128, TC_BK = 128;
 
-constexpr int TC_EPI_WARPS = 8, TC_CW = 16;                          // epilogue chunk: 16 columns
-constexpr size_t TC_EPI_SMEM = (size_t)TC_EPI_WARPS * 32 * (TC_CW + 1) * 4;  // per-warp transpose tile
+// Epilogue: EPI warps (8 or 16; 4 per TMEM lane quarter), each draining BN / (EPI / 4)
+// columns of its 32 rows in chunks of CW columns (16 with 8 warps, 8 with 16 warps).
+template <int EPI>
+struct TcEpi {
+  static constexpr int CW = EPI == 16 ? 8 : 16;
+  static constexpr size_t SMEM = (size_t)EPI * 32 * (CW + 1) * 4;  // per-warp transpose tile
+  static constexpr int THREADS = (4 + EPI) * 32;                   // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle
+};
 
-template <int L, int V>
+template <int L, int V, int EPI = 8>
 constexpr size_t tc_smem_bytes() {
-  return 1024 + (size_t)TcCfg<L, V>::STAGES * L * (TC_BM * TC_BK + TcCfg<L, V>::BN * TC_BK) + 256 + TC_EPI_SMEM;
+  // V = 2 stages hold ONE A limb tile and both B limb tiles
+  return 1024 + (size_t)TcCfg<L, V>::STAGES * ((V == 2 ? 1 : L) * TC_BM * TC_BK + L * TcCfg<L, V>::BN * TC_BK) + 256 +
+         TcEpi<EPI>::SMEM;
+}
+
+template <int CW>
+__device__ __forceinline__ void tmem_ld_cw(uint32_t taddr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 16) tmem_ld16(taddr, v);
+  else tmem_ld8(taddr, v);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int TC_THREADS = 384;  // warp 0 TMA, warp 1 MMA, warp 2 TMEM alloc, warps 4..11 epilogue
-
 // MNB: B limb planes are row-major k x n (MN-major operand, written by the same
 // vectorised split as A, no transpose pass); requires BN == 128 (one swizzle atom).
-template <int L, int V, bool MNB>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int L, int V, bool MNB, int EPI>
+__global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
     tc_modgemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
                       int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg, int group,
                       int c_prefetch) {
@@ -204,7 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < NBUF; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    for (int b = 0; b < NBUF; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) tmem_alloc(tholder, TCOLS);
@@ -293,26 +307,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // acc_s < 2^31; L = 4 reduces after position 4) and reduced ONCE, then the 32 x 16
     // values are transposed through shared memory so that the read-modify-write of C is
     // coalesced (lanes along a row, 16 independent loads in flight per thread).
+    constexpr int TC_CW = TcEpi<EPI>::CW, RSTEP = 32 / TC_CW;
     const int q = warp & 3, h = (warp - 4) >> 2;
-    constexpr int HALF = BN / 2;
+    constexpr int HALF = BN / (EPI / 4);  // columns of this warp's share
     static_assert(HALF % TC_CW == 0, "epilogue chunking");
     uint32_t* tr = epi_smem + (warp - 4) * 32 * (TC_CW + 1);
-    const int tc_col = lane & (TC_CW - 1), tc_row0 = lane >> 4;  // transposed phase: 2 rows x 16 columns
+    const int tc_col = lane % TC_CW, tc_row0 = lane / TC_CW;  // transposed phase: RSTEP rows x CW columns
     // limb positions of one 16-column chunk -> 16 reduced values of this thread's row
     auto combine = [&](uint32_t lane_base, int cc, uint32_t (&v)[TC_CW]) {
       uint32_t acc[NPOS][TC_CW];
       if constexpr (CAT) {  // X0 | X1 | Y0 | Y1  ->  positions X0, X1 + Y0, Y1
         uint32_t y0[TC_CW];
-        tmem_ld16(lane_base + (uint32_t)cc, acc[0]);
-        tmem_ld16(lane_base + (uint32_t)(BN + cc), acc[1]);
-        tmem_ld16(lane_base + (uint32_t)(2 * BN + cc), y0);
-        tmem_ld16(lane_base + (uint32_t)(3 * BN + cc), acc[2]);
+        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)cc, acc[0]);
+        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(BN + cc), acc[1]);
+        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(2 * BN + cc), y0);
+        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(3 * BN + cc), acc[2]);
         tmem_ld_wait();
 #pragma unroll
         for (int t = 0; t < TC_CW; ++t) acc[1][t] += y0[t];
       } else {
 #pragma unroll
-        for (int s = 0; s < NPOS; ++s) tmem_ld16(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+        for (int s = 0; s < NPOS; ++s) tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(s * BN + cc), acc[s]);
         tmem_ld_wait();
       }
 #pragma unroll
@@ -339,16 +354,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int t = 0; t < TC_CW; ++t) tr[lane * (TC_CW + 1) + t] = v[t];
       __syncwarp();
       const int col = n0 + cc + tc_col;
-      uint32_t w[16], cur[16];
+      uint32_t w[TC_CW], cur[TC_CW];
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const int rr = tc_row0 + 2 * kk, row = m0 + q * 32 + rr;
+      for (int kk = 0; kk < TC_CW; ++kk) {
+        const int rr = tc_row0 + RSTEP * kk, row = m0 + q * 32 + rr;
         w[kk] = tr[rr * (TC_CW + 1) + tc_col];
         cur[kk] = (row < c.m && col < c.n) ? c.row(row)[col] : 0u;
       }
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const int row = m0 + q * 32 + tc_row0 + 2 * kk;
+      for (int kk = 0; kk < TC_CW; ++kk) {
+        const int row = m0 + q * 32 + tc_row0 + RSTEP * kk;
         if (row < c.m && col < c.n) c.row(row)[col] = submod(cur[kk], w[kk], mp);
       }
       __syncwarp();  // tr is reused by the next chunk
@@ -386,6 +401,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (dbg & 4) continue;  // diagnostics: no C read-modify-write
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) apply(m0, n0, h * HALF + ch * TC_CW, v[ch]);
       } else {
@@ -399,6 +415,182 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tbase, TCOLS);
+  }
+}
+
+// Two-pass variant for two-limb primes (p < 2^16) with MN-major B: each 128 x 128 tile is
+// computed as pass X = A_lo [B_lo | B_hi] (TMEM columns 0..255: X0 | X1) and then pass
+// Y = A_hi [B_lo | B_hi] (columns 256..511: Y0 | Y1), each over the whole K range, with its
+// own full/empty accumulator barriers.  The epilogue drains X0 + 2^8 X1 as soon as pass X
+// is done (while pass Y runs) and 2^8 Y0 + 2^16 Y1 after pass Y (while the next tile's
+// pass X runs), so the tensor pipe never waits for a TMEM drain: the one-set kernel
+// loses the whole drain (256 KB of TMEM at 64 B/cycle) plus the MMA-drain round trip per
+// tile, ~40 % at K = 2048 (tools/gemm_dbg.py).  Price: B is loaded once per pass (+50 %
+// operand bytes).  The pass-X partial stays in registers until pass Y is drained, so C is
+// read-modified-written once per tile.
+__global__ void __launch_bounds__(TcEpi<8>::THREADS, 1)
+    tc_modgemm2p_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, View c,
+                        int m_pad, int n_pad, int kblocks, ModP mp, const int* stop, int dbg, int group,
+                        int c_prefetch) {
+  constexpr int L = 2, BN = 128, STAGES = TcCfg<2, 2>::STAGES, EPI = 8;
+  const int kplane = kblocks * TC_BK;
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  constexpr uint32_t TCOLS = 512;
+  constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
+  constexpr uint32_t STAGE_BYTES = A_TILE + L * B_TILE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                                  // [STAGES][128x128]
+  uint8_t* sB = smem + (size_t)STAGES * A_TILE;        // [STAGES][L][BNx128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)STAGES * L * B_TILE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;   // [2]: pass X, pass Y accumulators ready
+  uint64_t* tempty = tfull + 2;       // [2]: pass X, pass Y columns drained
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* epi_smem = reinterpret_cast<uint32_t*>(sB + (size_t)STAGES * L * B_TILE + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = n_pad / BN, tiles_m = m_pad / TC_BM, tiles = tiles_m * tiles_n;
+  auto tile_coords = [&](int tile, int& m0, int& n0) {
+    const int g = group > 0 ? group : tiles_m;
+    const int span = g * tiles_n, gid = tile / span, fm = gid * g, gsz = min(tiles_m - fm, g);
+    const int rem = tile - gid * span;
+    m0 = (fm + rem % gsz) * TC_BM;
+    n0 = (rem / gsz) * BN;
+  };
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) tmem_alloc(tholder, TCOLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tholder;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer: per tile, pass X (A_lo) then pass Y (A_hi) ----------
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      int m0, n0;
+      tile_coords(tile, m0, n0);
+      for (int pass = 0; pass < 2; ++pass)
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          if ((dbg & 1) && g >= (uint32_t)STAGES) {
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(sA + (size_t)s * A_TILE, &ta, &full[s], kb * TC_BK, pass * m_pad + m0);
+#pragma unroll
+          for (int l = 0; l < L; ++l)
+            tma_load_2d(sB + ((size_t)s * L + l) * B_TILE, &tb, &full[s], n0, l * kplane + kb * TC_BK);
+        }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: N = 256 MMAs against [B_lo | B_hi] --------------------
+    constexpr uint32_t idesc_cat = idesc_i8(2 * BN, true);
+    uint32_t g = 0, local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      for (int pass = 0; pass < 2; ++pass) {
+        mbar_wait(&tempty[pass], (local & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tbase + (uint32_t)(pass * 2 * BN);
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + (size_t)s * A_TILE);
+          const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 32; ++kk)
+            mma_i8(dacc, desc_k_sw128(a0 + kk * 32), desc_mn_sw128(b0 + kk * 32 * 128, B_TILE), idesc_cat,
+                   (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[pass]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: per pass, TMEM -> partial value mod p -> C -= value -----
+    constexpr int TC_CW = TcEpi<EPI>::CW, RSTEP = 32 / TC_CW, HALF = BN / 2, NCH = HALF / TC_CW;
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    uint32_t* tr = epi_smem + (warp - 4) * 32 * (TC_CW + 1);
+    const int tc_col = lane % TC_CW, tc_row0 = lane / TC_CW;
+    auto apply = [&](int m0, int n0, int cc, const uint32_t (&v)[TC_CW]) {
+#pragma unroll
+      for (int t = 0; t < TC_CW; ++t) tr[lane * (TC_CW + 1) + t] = v[t];
+      __syncwarp();
+      const int col = n0 + cc + tc_col;
+      uint32_t w[TC_CW], cur[TC_CW];
+#pragma unroll
+      for (int kk = 0; kk < TC_CW; ++kk) {
+        const int rr = tc_row0 + RSTEP * kk, row = m0 + q * 32 + rr;
+        w[kk] = tr[rr * (TC_CW + 1) + tc_col];
+        cur[kk] = (row < c.m && col < c.n) ? c.row(row)[col] : 0u;
+      }
+#pragma unroll
+      for (int kk = 0; kk < TC_CW; ++kk) {
+        const int row = m0 + q * 32 + tc_row0 + RSTEP * kk;
+        if (row < c.m && col < c.n) c.row(row)[col] = submod(cur[kk], w[kk], mp);
+      }
+      __syncwarp();
+    };
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
+      int m0, n0;
+      tile_coords(tile, m0, n0);
+      if (c_prefetch) {
+        const int row = m0 + q * 32 + lane, col = n0 + h * HALF;
+        if (row < c.m && col < c.n) {
+          const char* p = reinterpret_cast<const char*>(c.row(row) + col);
+          const int bytes = min(HALF, c.n - col) * 4;
+          for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+        }
+      }
+      // pass X: v = X0 + 2^8 X1 (mod p) into registers, release the X columns; pass Y:
+      // v += 2^8 Y0 + 2^16 Y1 (mod p), release the Y columns; then ONE C read-modify-write
+      // (every accumulator < 2^31, so each partial fits 48 bits before its reduction)
+      uint32_t v[NCH][TC_CW];
+      for (int pass = 0; pass < 2; ++pass) {
+        mbar_wait(&tfull[pass], local & 1);
+        tc_fence_after();
+        if (dbg & 2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[pass]);
+          continue;
+        }
+        const uint32_t lane_base = tbase + (uint32_t)(pass * 2 * BN) + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          const int cc = h * HALF + ch * TC_CW;
+          uint32_t lo[TC_CW], hi[TC_CW];
+          tmem_ld_cw<TC_CW>(lane_base + (uint32_t)cc, lo);
+          tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(BN + cc), hi);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < TC_CW; ++t) {
+            const uint32_t part = reduce64(((uint64_t)lo[t] + ((uint64_t)hi[t] << 8)) << (8 * pass), mp);
+            v[ch][t] = pass ? addmod(v[ch][t], part, mp) : part;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[pass]);
+      }
+      if (dbg & 6) continue;  // diagnostics: 4 = no C read-modify-write
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) apply(m0, n0, h * HALF + ch * TC_CW, v[ch]);
     }
   }
   tc_fence_before();
@@ -557,7 +749,8 @@ struct TcGemm {
   PFN_encodeTiled encode = nullptr;
   std::string last_error;
   int64_t k_pass_override = 0;  // tests: force multi-pass K splitting
-  bool attrs_set[2][2][5] = {};
+  bool attrs_set[2][3][5][2] = {};
+  int epi_warps = 8;            // option tc_epi: epilogue warps of the 1-set (V = 1) kernels (8 or 16)
   int variant = 1;              // TcCfg variant (option tc_cfg)
   int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
   int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring, 2 = skip the epilogue
@@ -626,7 +819,7 @@ struct TcGemm {
     return true;
   }
 
-  template <int L, int V, bool MNB>
+  template <int L, int V, bool MNB, int EPI = 8>
   int launch(const View& c, const View& a, const View& b, const ModP mp, cudaStream_t st, const int* stop,
              int max_ctas) {
     constexpr int BN = TcCfg<L, V>::BN;
@@ -644,14 +837,21 @@ struct TcGemm {
       last_error = "workspace allocation failed";
       return kNoMemory;
     }
-    constexpr size_t smem = tc_smem_bytes<L, V>();
-    if (!attrs_set[MNB][V][L]) {
-      if (cudaFuncSetAttribute(tc_modgemm_kernel<L, V, MNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess) {
+    constexpr size_t smem = tc_smem_bytes<L, V, EPI>();
+    static_assert(smem <= 232448, "shared memory budget");
+    static_assert(V != 2 || (L == 2 && MNB && EPI == 8), "two-pass kernel: two limbs, MN-major B");
+    if (!attrs_set[MNB][V][L][EPI == 16]) {
+      cudaError_t ae;
+      if constexpr (V == 2)
+        ae = cudaFuncSetAttribute(tc_modgemm2p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      else
+        ae = cudaFuncSetAttribute(tc_modgemm_kernel<L, V, MNB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem);
+      if (ae != cudaSuccess) {
         last_error = "cannot set shared memory size";
         return kCuda;
       }
-      attrs_set[MNB][V][L] = true;
+      attrs_set[MNB][V][L][EPI == 16] = true;
     }
     for (int64_t k0 = 0; k0 < k; k0 += kp) {
       const int kc = (int)std::min<int64_t>(kp, k - k0);
@@ -692,8 +892,12 @@ struct TcGemm {
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
       }
-      tc_modgemm_kernel<L, V, MNB><<<grid, TC_THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp,
-                                                                   stop, dbg, raster_group, c_prefetch);
+      if constexpr (V == 2)
+        tc_modgemm2p_kernel<<<grid, TcEpi<8>::THREADS, smem, st>>>(ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop,
+                                                                   dbg, raster_group, c_prefetch);
+      else
+        tc_modgemm_kernel<L, V, MNB, EPI><<<grid, TcEpi<EPI>::THREADS, smem, st>>>(
+            ta, tb, c, m_pad, n_pad, k_pad / TC_BK, mp, stop, dbg, raster_group, c_prefetch);
       if (time_mma) {
         float ms = 0.f;
         cudaEventRecord(e1, st);
@@ -737,6 +941,8 @@ struct TcGemm {
       switch (L) {
         case 1: return launch<1, 1, false>(c, a, b, mp, st, stop, max_ctas);
         case 2:
+          if (mn_b && variant == 2) return launch<2, 2, true>(c, a, b, mp, st, stop, max_ctas);
+          if (mn_b && epi_warps == 16) return launch<2, 1, true, 16>(c, a, b, mp, st, stop, max_ctas);
           return mn_b ? launch<2, 1, true>(c, a, b, mp, st, stop, max_ctas)
                       : launch<2, 1, false>(c, a, b, mp, st, stop, max_ctas);
         case 3: return launch<3, 1, false>(c, a, b, mp, st, stop, max_ctas);

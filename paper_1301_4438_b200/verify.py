@@ -29,7 +29,8 @@ def _mm(a, b, p):
     ctx = _native.context(a.device.index)
     st = ctx.lib.pluq_modgemm_sub(ctx.handle, c.data_ptr(), n, a.data_ptr(), k, b.data_ptr(), n, m, n, k, p)
     _native.raise_for(st, ctx, "freivalds gemm")
-    return torch.remainder(p - c.to(torch.int64), p).to(torch.int32)
+    c.neg_().add_(p)  # c = -AB mod p  ->  AB mod p, in place
+    return c.masked_fill_(c == p, 0)
 
 
 def freivalds(original, factors: PluqFactors, probes: int = 4, seed: int = 0) -> bool:

@@ -168,3 +168,23 @@ def test_host_pipeline_chunks_vs_oracle(pb, p, dtype):
         assert st == _native.PLUQ_EINVAL and np.array_equal(bad, keep)
     finally:
         ctx.set_option("host_chunk_mb", old)
+
+
+def test_device_materialization_matches_host(pb):
+    """extract_lm / extract_uv / reconstruct / check_structure on a device-resident result
+    (matrix.py:308-349) equal the host versions and rebuild A."""
+    import torch
+
+    p = 65521
+    a0 = orc.gen_xy_rank(300, 260, 170, p, 12)
+    fh = pb.pluq(pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64)))
+    t = torch.from_numpy(a0).cuda().to(torch.int32)
+    fd = pb.pluq(pb.DenseMatrix(pb.PrimeField(p), t))
+    assert fd.rank == fh.rank == 170
+    lm, uv = fd.extract_lm(), fd.extract_uv()
+    assert lm.is_cuda and uv.is_cuda
+    assert np.array_equal(lm.cpu().numpy().astype(np.int64), fh.extract_lm().astype(np.int64))
+    assert np.array_equal(uv.cpu().numpy().astype(np.int64), fh.extract_uv().astype(np.int64))
+    rec = fd.reconstruct()
+    assert rec.on_device and np.array_equal(rec.data.cpu().numpy().astype(np.int64), a0)
+    assert fd.check_structure() == [] == fh.check_structure()

@@ -42,12 +42,13 @@ class _opts:
         self.ctx, self.kw = _native.context(), kw
 
     def __enter__(self):
+        self.old = {k: self.ctx.get_option(k) for k in self.kw}
         for k, v in self.kw.items():
             self.ctx.set_option(k, v)
 
     def __exit__(self, *exc):
-        for k in self.kw:
-            self.ctx.set_option(k, DEFAULTS[k])
+        for k, v in self.old.items():
+            self.ctx.set_option(k, v)
 
 
 def _nongeneric_batch(p, n_blocks, seed):
@@ -125,9 +126,11 @@ def test_speculative_variants(pb, opts, case):
     assert np.array_equal(np.asarray(a.data, dtype=np.int64), packed)
 
 
-@pytest.mark.parametrize("mnb", [0, 1])
-@pytest.mark.parametrize("shape", [(256, 384, 200), (130, 260, 1100), (512, 128, 64)])
-def test_tc_gemm_b_layouts(pb, mnb, shape):
+@pytest.mark.parametrize("mnb,epi,cfg", [(0, 8, 1), (1, 8, 1), (1, 16, 1), (1, 8, 2)],
+                         ids=["kmajorB", "mnB", "mnB_epi16", "mnB_twopass"])
+@pytest.mark.parametrize("shape", [(256, 384, 200), (130, 260, 1100), (512, 128, 64), (1000, 700, 2048),
+                                   (300, 1300, 2500)])
+def test_tc_gemm_b_layouts(pb, mnb, shape, epi, cfg):
     import torch
     from paper_1301_4438_b200 import _native
 
@@ -140,12 +143,12 @@ def test_tc_gemm_b_layouts(pb, mnb, shape):
     tc = torch.from_numpy(C).cuda().to(torch.int32)
     ta = torch.from_numpy(A).cuda().to(torch.int32)
     tb = torch.from_numpy(B).cuda().to(torch.int32)
-    with _opts(tc_mnb=mnb):
+    with _opts(tc_mnb=mnb, tc_epi=epi, tc_cfg=cfg):
         ctx = _native.context()
         st = ctx.lib.pluq_modgemm_sub_tc(ctx.handle, tc.data_ptr(), n, ta.data_ptr(), k, tb.data_ptr(), n, m, n, k, p)
         _native.raise_for(st, ctx, "tc gemm")
         torch.cuda.synchronize()
-    want = (C.astype(object) - A.astype(object).dot(B.astype(object))) % p
+    want = (C - orc._mulmod_exact(A, B, p)) % p
     assert np.array_equal(tc.cpu().numpy().astype(np.int64), want.astype(np.int64))
 
 
