@@ -367,6 +367,74 @@ def measure_peaks_live(dev):
     return max((ctx.measure_peaks() for _ in range(3)), key=lambda d: d["int8_tops"])
 
 
+def hbm_kernels(dev, a0, packed, rank):
+    """The memory-bound kernels of the path in achieved HBM GB/s (north_star), each timed
+    with CUDA events (best of 5 after a warm-up) on cfg5-sized data, against the measured
+    copy bandwidth in MEASURED_PEAKS.json.  Bytes are ALGORITHMIC (what the operation must
+    move at least once), not the kernels' own traffic."""
+    import ctypes
+
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    hbm, _, kind = peaks()
+    ctx = _native.context(dev.index)
+    lib = ctx.lib
+    out = {"peak_gbs": hbm, "peak_kind": kind}
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize(dev)
+        best = 1e30
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        return best
+
+    def line(name, nbytes, t, what):
+        out[name] = {"bytes": nbytes, "ms": t * 1e3, "gbs": nbytes / t / 1e9, "frac": nbytes / t / 1e9 / hbm,
+                     "what": what}
+
+    m, n = a0.shape
+    p = 65521
+    t = timed(lambda: lib.pluq_check_residues(ctx.handle, a0.data_ptr(), n, m, n, p))
+    line("range_check", m * n * 4, t, "canonical-residue check of the 65536^2 input (read once)")
+    flag = ctypes.c_int64()
+    zero = packed[rank:, rank:]
+    t = timed(lambda: lib.pluq_nonzero(ctx.handle, zero.data_ptr(), n, m - rank, n - rank, ctypes.byref(flag)))
+    line("zero_test", (m - rank) * (n - rank) * 4, t,
+         "zero test of the trailing (m-r)x(n-r) block of the result (read once, all zero)")
+    k = 16384
+    x = torch.randint(0, p, (k, k), dtype=torch.int32, device=dev)
+    g = np.random.default_rng(1).permutation(k).astype(np.int64)
+    gp = g.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    t = timed(lambda: lib.pluq_permute_rows(ctx.handle, x.data_ptr(), k, k, k, gp))
+    line("row_gather", 2 * k * k * 4, t, "apply_rows of a random permutation on 16384^2 (every row moves)")
+    t = timed(lambda: lib.pluq_permute_cols(ctx.handle, x.data_ptr(), k, k, k, gp))
+    line("col_gather", 2 * k * k * 4, t, "apply_cols of a random permutation on 16384^2 (every column moves)")
+    # limb split: whole tensor-core GEMM call minus its MMA kernel (option tc_time)
+    kk = 2048
+    A = torch.randint(0, p, (k, kk), dtype=torch.int32, device=dev)
+    B = torch.randint(0, p, (kk, k), dtype=torch.int32, device=dev)
+    args = (ctx.handle, x.data_ptr(), k, A.data_ptr(), kk, B.data_ptr(), k, k, k, kk, p)
+    t_all = timed(lambda: lib.pluq_modgemm_sub_tc(*args))
+    ctx.set_option("tc_time", 1)
+    lib.pluq_modgemm_sub_tc(*args)
+    torch.cuda.synchronize(dev)
+    t_mma = ctx.stats()["t_tc_mma_ns"] / 1e9
+    ctx.set_option("tc_time", 0)
+    split_bytes = 2 * (k * kk * 4 + 2 * k * kk)  # A and B: read int32, write 2 uint8 limb planes
+    line("limb_split", split_bytes, max(t_all - t_mma, 1e-9), "operand limb split of a 16384x16384x2048 GEMM "
+         "(both operands; call time minus the MMA kernel)")
+    del x, A, B
+    torch.cuda.empty_cache()
+    return out
+
+
 def launch_ranks(args):
     """--gpus N outside torchrun: one process per GPU via torch.distributed.run (127.0.0.1)."""
     import torch
@@ -485,6 +553,13 @@ def bench_single(pb, name, args, dev, world, rank):
         int8_peak = pk["int8_tops"]
         L = limbs(c["p"])
         roof = roofline_step(pb, name, a0, int8_peak) if world == 1 else None
+        mem = None
+        if world == 1 and name == "cfg5":
+            x = a0.clone()
+            f5 = pb.pluq(pb.DenseMatrix(pb.PrimeField(c["p"]), x), THRESHOLD)
+            mem = hbm_kernels(dev, a0, x, f5.rank)
+            del x, f5
+            torch.cuda.empty_cache()
         if roof is not None:
             roof["gemm_share_of_step"] = None  # from the ncu launch list (profiles/), not measurable here
         ms = 1e3 * t_dev / args.steps
@@ -504,6 +579,7 @@ def bench_single(pb, name, args, dev, world, rank):
                                     "note": f"a field MAC is L^2 = {L * L} int8 MACs on the limb path: "
                                             "field-op/s ceiling = int8 peak / L^2"},
             "measured_peaks": {"int8_tcgen05_tops": int8_peak, "fp64_dmma_tflops": pk["fp64_tflops"]},
+            "hbm_kernels": mem,
             "clocks": res["clocks"], "wall_s_timed_region": res["wall"],
             "driver_stats": {k: v for k, v in res["stats"].items() if not k.startswith("t_") and "timed" not in k},
         }

@@ -181,6 +181,7 @@ struct pluq_ctx {
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
   int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
+  int64_t la_pair = 1;             // ... and panel P's far update merges into P+1's (one K = 2W GEMM)
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 24;        // pipeline depth of the host-buffer batched path
   int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
@@ -1060,6 +1061,13 @@ struct Driver {
       CU(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     }
     bool side_pending = false;
+    // Paired far updates: when panel P defers, its far update (rows below panel P+1, columns
+    // beyond it) is merged into panel P+1's as ONE K = 2W tensor-core GEMM (per-tile fixed
+    // costs of the one-accumulator-set kernel — the TMEM drain and the MMA restart — halve
+    // relative to the MMA work); panel P+1's own rows still get P's update eagerly because
+    // its U12 needs them.  deferred[P] records it for the finishing step after a stop.
+    int defer_ps = -1;
+    std::vector<char> deferred((size_t)npanels + 1, 0);
     cudaStream_t side2 = c->side_streams()[4];
     cudaEvent_t ev_d = nullptr, ev_t = nullptr;
     CU(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
@@ -1112,9 +1120,10 @@ struct Driver {
         side_pending = false;
       }
       const int ne = std::min(pe + W, n);
+      const int gs = defer_ps >= 0 ? defer_ps : ps;  // K range [gs, pe): this panel, or the pair
       if (la && pe < mn && ne < n) {
         sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne - pe));
-        sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, ne - pe));
+        sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, gs, m - pe, pe - gs), x.sub(gs, pe, pe - gs, ne - pe));
         const int pidx = ps / W;
         CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
         CU(cudaEventRecord(ev_main, c->stream));
@@ -1124,12 +1133,21 @@ struct Driver {
         aops.stop = snap + pidx;
         aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
         aops.trsm_l(l11, x.sub(ps, ne, pe - ps, n - ne));
-        aops.gemm(x.sub(pe, ne, m - pe, n - ne), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
+        const bool defer = c->la_pair && defer_ps < 0 && ne < mn && ne + W < n;
+        if (defer) {  // only the next panel's rows now; the rest merges into its update
+          aops.gemm(x.sub(pe, ne, ne - pe, n - ne), x.sub(pe, ps, ne - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
+          deferred[pidx] = 1;
+          defer_ps = ps;
+        } else {
+          aops.gemm(x.sub(pe, ne, m - pe, n - ne), x.sub(pe, gs, m - pe, pe - gs), x.sub(gs, ne, pe - gs, n - ne));
+          defer_ps = -1;
+        }
         CU(cudaEventRecord(ev_side, side));
         side_pending = true;
       } else {
         sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
-        sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, n - pe));
+        sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, gs, m - pe, pe - gs), x.sub(gs, pe, pe - gs, n - pe));
+        defer_ps = -1;
       }
     }
     if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
@@ -1151,6 +1169,11 @@ struct Driver {
       const int k0 = c->h_stop[1], t = c->h_stop[2], g = k0 + t;
       const int ps = (k0 / W) * W, pe = std::min(ps + W, mn);
       const int bs = std::min(BS, pe - k0);
+      if (ps >= W && deferred[ps / W - 1]) {
+        // the previous panel deferred its far update into this panel's: apply it on the rows
+        // below this panel (its own rows already have it), columns right of this panel
+        ops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps - W, m - pe, W), x.sub(ps - W, pe, W, n - pe));
+      }
       if (t > 0) {
         const View b11 = x.sub(k0, k0, t, t);
         ops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, t), b11);
@@ -1591,6 +1614,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
+  X(la_pair, c->la_pair)                                                                            \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

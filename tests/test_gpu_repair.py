@@ -124,3 +124,45 @@ def test_cfg5_seed0_full_size_repaired(pb):
     assert verify.structure_ok(f) and verify.freivalds(a5, f, probes=2)
     del a5, f
     torch.cuda.empty_cache()
+
+
+PAIR_CASES = [
+    # name, m, n, rank or None, [(g, width)]: zero pivots in the first / second panel of a pair
+    ("generic", 1100, 1200, None, []),
+    ("stop_second_of_pair", 1100, 1100, 400, []),      # rank 400: zero Schur inside panel 1 (W=256)
+    ("stop_first_of_pair", 1100, 1100, 600, []),       # inside panel 2
+    ("repair_second_of_pair", 1100, 1150, None, [(300, 1)]),
+    ("repair_two_pairs", 1200, 1100, None, [(100, 1), (700, 1)]),
+]
+
+
+@pytest.mark.parametrize("la_pair", [0, 1])
+@pytest.mark.parametrize("name,m,n,r,gs", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
+def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
+    """Panel P's far update merged into panel P+1's (option la_pair, one K = 2W GEMM), with
+    zero pivots / repairs in either panel of a pair (the finishing step applies a pending
+    deferred update)."""
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    a0 = _make(name, m, n, r, gs, p)
+    x = a0.astype(np.float64)
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(small_cap=1, spec_panel=256, la_pair=la_pair)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert st["speculative_ok"] >= 1 and st["speculative_fail"] == 0
+    assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
