@@ -488,7 +488,7 @@ struct Ops {
     void* h = c->stage(both.data(), both.size() * 4);
     CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
     uint32_t* tmp = c->dalloc<uint32_t>((size_t)nmv * x.n);
-    dim3 grid((x.n + 255) / 256, grid_rows(nmv));
+    dim3 grid((unsigned)std::max(1, std::min(8, (x.n / 4 + 255) / 256)), grid_rows(nmv));
     rows_to_tmp_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx, nmv, tmp);
     c->check_launch();
     tmp_to_rows_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx + nmv, nmv, tmp);

@@ -1089,19 +1089,23 @@ __global__ void diag_zero_kernel(View u, int* flag) {
 // ---------------------------------------------------------------------------------
 // Permutations restricted to the moved set: tmp[q] <- X[src[q]], then X[dst[q]] <- tmp[q].
 // ---------------------------------------------------------------------------------
-__global__ void rows_to_tmp_kernel(View x, const int* src, int nmv, uint32_t* tmp) {
-  for (int q = blockIdx.y; q < nmv; q += gridDim.y) {
-    const uint32_t* sr = x.row(src[q]);
-    uint32_t* tr = tmp + (int64_t)q * x.n;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) tr[j] = sr[j];
+// Whole-row copies: 16-byte accesses when every row of the view and of the temporary is
+// 16-byte aligned (pitch and width multiples of 4), else scalar.
+__device__ __forceinline__ void copy_row(uint32_t* d, const uint32_t* s, int n, bool vec) {
+  if (vec) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n / 4; j += gridDim.x * blockDim.x)
+      reinterpret_cast<uint4*>(d)[j] = reinterpret_cast<const uint4*>(s)[j];
+  } else {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) d[j] = s[j];
   }
 }
+__global__ void rows_to_tmp_kernel(View x, const int* src, int nmv, uint32_t* tmp) {
+  const bool vec = (x.ld % 4) == 0 && (x.n % 4) == 0 && (reinterpret_cast<uintptr_t>(x.a) & 15) == 0;
+  for (int q = blockIdx.y; q < nmv; q += gridDim.y) copy_row(tmp + (int64_t)q * x.n, x.row(src[q]), x.n, vec);
+}
 __global__ void tmp_to_rows_kernel(View x, const int* dst, int nmv, const uint32_t* tmp) {
-  for (int q = blockIdx.y; q < nmv; q += gridDim.y) {
-    uint32_t* dr = x.row(dst[q]);
-    const uint32_t* tr = tmp + (int64_t)q * x.n;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) dr[j] = tr[j];
-  }
+  const bool vec = (x.ld % 4) == 0 && (x.n % 4) == 0 && (reinterpret_cast<uintptr_t>(x.a) & 15) == 0;
+  for (int q = blockIdx.y; q < nmv; q += gridDim.y) copy_row(x.row(dst[q]), tmp + (int64_t)q * x.n, x.n, vec);
 }
 __global__ void cols_to_tmp_kernel(View x, const int* src, int nmv, uint32_t* tmp) {
   for (int i = blockIdx.y; i < x.m; i += gridDim.y) {

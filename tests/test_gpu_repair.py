@@ -166,3 +166,35 @@ def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
     assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
     assert np.array_equal(a.data, x)
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+
+
+@pytest.mark.parametrize("la_pair", [0, 1])
+@pytest.mark.parametrize("W", [384, 640, 768])
+def test_panel_widths_generic_and_repaired(pb, la_pair, W):
+    """Panel widths that do not divide the size (partial last panels, pairs cut short), on a
+    rank-deficient X Y input with one coincidental zero minor: the speculative path must
+    succeed (no fallback) and match the oracle."""
+    from paper_1301_4438_b200 import _native
+
+    p, m, n = 65521, 2000, 2100
+    a0 = _make("w", m, n, 1300, [(500, 1)], p)
+    x = a0.astype(np.float64)
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(small_cap=1, spec_panel=W, la_pair=la_pair)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+    assert st["speculative_fail"] == 0 and st["spec_repairs"] == 1, st
