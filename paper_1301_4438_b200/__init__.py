@@ -10,6 +10,7 @@ from .field import ABSOLUTE_MODULUS_BOUND, DEFAULT_MODULUS_BOUND, PrimeField, in
 from .kernels import ClassicalKernels, CudaKernels, device_matmul_mod
 from .matrix import DenseMatrix, OpCounts, Permutation, PluqFactors, apply_cols, apply_rows, perm_block_diag
 from .distributed import pluq_distributed
+from .leu import LeuFactors, check_triangular_extension, to_leu
 from .rank_profile import col_rank_profile, leading_rank_profiles, row_rank_profile
 from .recursive import (
     DEFAULT_THRESHOLD,
@@ -36,6 +37,7 @@ __all__ = [
     "DEFAULT_MODULUS_BOUND",
     "DEFAULT_THRESHOLD",
     "DenseMatrix",
+    "LeuFactors",
     "OpCounts",
     "Permutation",
     "PluqFactors",
@@ -48,6 +50,7 @@ __all__ = [
     "base_case_row",
     "build_s_perm",
     "build_t_perm",
+    "check_triangular_extension",
     "col_rank_profile",
     "device_matmul_mod",
     "inverse_mod",
@@ -60,4 +63,5 @@ __all__ = [
     "pluq_distributed",
     "pluq_iterative",
     "row_rank_profile",
+    "to_leu",
 ]

@@ -15,6 +15,7 @@
 // for the kernel calls it issues and on the device for work done inside kernels.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -1896,7 +1897,55 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
 // Host dtype <-> uint32 residues on host threads (the reference's storage dtype: float64
 // when (p-1)^2 * 8192 <= 2^53, else int64; field.py:75-81).  to_u32 returns false if an entry
 // is not a canonical residue (field.py:140-147).
+// AVX2 float64 <-> uint32 for the large-matrix pipeline: non-temporal stores into the pinned
+// ring and into the caller's float64 buffer (no read-for-ownership of 32 GiB at cfg5).
+// Chosen at run time (__builtin_cpu_supports); the scalar loops below are the reference.
+__attribute__((target("avx2"))) static bool f64_to_u32_avx2(const double* s, uint32_t* d, int64_t count, uint32_t p) {
+  int64_t i = 0;
+  bool ok = true;
+  const __m256d zero = _mm256_setzero_pd(), pd = _mm256_set1_pd((double)p);
+  __m256d bad = _mm256_setzero_pd();
+  for (; i < count && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) {
+    const double v = s[i];
+    const bool good = v >= 0.0 && v < (double)p && v == std::floor(v);
+    d[i] = good ? (uint32_t)v : 0u;
+    ok &= good;
+  }
+  for (; i + 4 <= count; i += 4) {
+    const __m256d v = _mm256_loadu_pd(s + i);
+    const __m256d fl = _mm256_round_pd(v, _MM_FROUND_TO_NEG_INF | _MM_FROUND_NO_EXC);
+    // bad lanes: v < 0, v >= p, v != floor(v), NaN (unordered compares)
+    const __m256d b = _mm256_or_pd(_mm256_or_pd(_mm256_cmp_pd(v, zero, _CMP_NGE_UQ), _mm256_cmp_pd(v, pd, _CMP_NLT_UQ)),
+                                   _mm256_cmp_pd(v, fl, _CMP_NEQ_UQ));
+    bad = _mm256_or_pd(bad, b);
+    const __m128i q = _mm256_cvttpd_epi32(_mm256_andnot_pd(b, v));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), q);
+  }
+  ok &= _mm256_movemask_pd(bad) == 0;
+  for (; i < count; ++i) {
+    const double v = s[i];
+    const bool good = v >= 0.0 && v < (double)p && v == std::floor(v);
+    d[i] = good ? (uint32_t)v : 0u;
+    ok &= good;
+  }
+  _mm_sfence();
+  return ok;
+}
+__attribute__((target("avx2"))) static void u32_to_f64_avx2(const uint32_t* s, double* d, int64_t count) {
+  int64_t i = 0;
+  for (; i < count && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = (double)s[i];
+  for (; i + 4 <= count; i += 4)  // residues < 2^31: the signed conversion is exact
+    _mm256_stream_pd(d + i, _mm256_cvtepi32_pd(_mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i))));
+  for (; i < count; ++i) d[i] = (double)s[i];
+  _mm_sfence();
+}
+static bool have_avx2() {
+  static const bool v = __builtin_cpu_supports("avx2");
+  return v;
+}
+
 static bool host_to_u32(const void* src, bool is_f64, uint32_t* dst, int64_t count, uint32_t p) {
+  if (is_f64 && have_avx2()) return f64_to_u32_avx2(static_cast<const double*>(src), dst, count, p);
   bool ok = true;
   if (is_f64) {
     const double* s = static_cast<const double*>(src);
@@ -1918,6 +1967,7 @@ static bool host_to_u32(const void* src, bool is_f64, uint32_t* dst, int64_t cou
   return ok;
 }
 static void host_from_u32(const uint32_t* src, bool is_f64, void* dst, int64_t count) {
+  if (is_f64 && have_avx2()) return u32_to_f64_avx2(src, static_cast<double*>(dst), count);
   if (is_f64) {
     double* d = static_cast<double*>(dst);
     for (int64_t i = 0; i < count; ++i) d[i] = (double)src[i];
@@ -1991,9 +2041,10 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
       uint32_t* slot = reinterpret_cast<uint32_t*>(ring + (size_t)s * chunk);
       const char* src = static_cast<const char*>(hA) + (size_t)e0 * esz;
-      hp.run(parts, [&](int t) {
-        const int64_t a = ne * t / parts, b = ne * (t + 1) / parts;
-        if (!host_to_u32(src + (size_t)a * esz, is_f64, slot + a, b - a, (uint32_t)p)) ok.store(false);
+      hp.run(parts, [&](int t) {  // per-thread ranges start on 16-entry boundaries
+        const int64_t a = t ? (ne * t / parts) & ~int64_t(15) : 0;
+        const int64_t b = t + 1 < parts ? (ne * (t + 1) / parts) & ~int64_t(15) : ne;
+        if (b > a && !host_to_u32(src + (size_t)a * esz, is_f64, slot + a, b - a, (uint32_t)p)) ok.store(false);
       });
       CU(cudaMemcpyAsync(dA + e0, slot, (size_t)ne * 4, cudaMemcpyHostToDevice, sin));
       CU(cudaEventRecord(ev[s], sin));
@@ -2022,8 +2073,9 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       const uint32_t* slot = reinterpret_cast<const uint32_t*>(ring + (size_t)s * chunk);
       char* dst = static_cast<char*>(hA) + (size_t)e0 * esz;
       hp.run(parts, [&](int t) {
-        const int64_t a = ne * t / parts, b = ne * (t + 1) / parts;
-        host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
+        const int64_t a = t ? (ne * t / parts) & ~int64_t(15) : 0;
+        const int64_t b = t + 1 < parts ? (ne * (t + 1) / parts) & ~int64_t(15) : ne;
+        if (b > a) host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
       });
       if (k + pluq_ctx::kRing < nch) issue(k + pluq_ctx::kRing);
     }

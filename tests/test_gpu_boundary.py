@@ -188,3 +188,54 @@ def test_device_materialization_matches_host(pb):
     rec = fd.reconstruct()
     assert rec.on_device and np.array_equal(rec.data.cpu().numpy().astype(np.int64), a0)
     assert fd.check_structure() == [] == fh.check_structure()
+
+
+def test_cli_decompose_matches_reference_files(pb, tmp_path):
+    """`python -m paper_1301_4438_b200 decompose` writes the reference's own factor file
+    (tests/golden/text_fixtures.json), `verify` accepts it, `rank-profile` answers."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "tests", "golden", "text_fixtures.json")) as fh:
+        cases = json.load(fh)
+    for i, c in enumerate(cases):
+        mf = tmp_path / f"m{i}.txt"
+        mf.write_text(c["matrix_text"])
+        out = subprocess.run([sys.executable, "-m", "paper_1301_4438_b200", "decompose", str(mf)], cwd=root,
+                             capture_output=True, text=True)
+        assert out.returncode == 0, out.stderr
+        assert out.stdout == c["factors_text"], (i, out.stdout, c["factors_text"])
+        ff = tmp_path / f"f{i}.txt"
+        ff.write_text(out.stdout)
+        v = subprocess.run([sys.executable, "-m", "paper_1301_4438_b200", "verify", str(mf), str(ff)], cwd=root,
+                           capture_output=True, text=True)
+        assert v.returncode == 0 and v.stdout.strip() == "OK", v.stderr
+    rp = subprocess.run([sys.executable, "-m", "paper_1301_4438_b200", "rank-profile", str(tmp_path / "m0.txt")],
+                        cwd=root, capture_output=True, text=True)
+    assert rp.returncode == 0 and set(json.loads(rp.stdout)) == {"rows", "cols"}
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_to_leu_host_and_device(pb, on_device):
+    import torch
+
+    p = 101
+    for seed, (m, n, r) in enumerate([(40, 30, 12), (25, 50, 25), (33, 33, 0), (20, 20, 20)]):
+        a0 = orc.gen_xy_rank(m, n, r, p, seed) if r else np.zeros((m, n), np.int64)
+        orig = pb.DenseMatrix(pb.PrimeField(p), a0.copy())
+        data = torch.from_numpy(a0).cuda().to(torch.int32) if on_device else a0.astype(np.float64)
+        f = pb.pluq(pb.DenseMatrix(pb.PrimeField(p), data))
+        leu = pb.to_leu(f, orig)
+        lbar = leu.lbar.host_array()
+        e = leu.e.host_array()
+        ubar = leu.ubar.host_array()
+        assert np.array_equal(np.tril(lbar), lbar) and np.all(np.diagonal(lbar) == 1)
+        assert np.array_equal(np.triu(ubar), ubar) and int(e.sum()) == f.rank
+        prod = (lbar.astype(object).dot(e.astype(object)).dot(ubar.astype(object))) % p
+        assert np.array_equal(prod.astype(np.int64), a0)
+        y = np.eye(m - f.rank, dtype=np.int64)
+        z = np.zeros((n - f.rank, n - f.rank), np.int64)
+        assert pb.check_triangular_extension(f, y, z) == (True, True)
