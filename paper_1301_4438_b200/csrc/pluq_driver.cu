@@ -1069,12 +1069,23 @@ struct Driver {
     // its U12 needs them.  deferred[P] records it for the finishing step after a stop.
     int defer_ps = -1;
     std::vector<char> deferred((size_t)npanels + 1, 0);
+    // option trace_pipeline: timing events per panel on both streams, printed at the end
+    const bool trace = c->trace_pipeline != 0;
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    auto mark = [&](const std::string& label, cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      CU(cudaEventRecord(e, st));
+      tev.emplace_back(label, e);
+    };
     cudaStream_t side2 = c->side_streams()[4];
     cudaEvent_t ev_d = nullptr, ev_t = nullptr;
     CU(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
+      mark("P" + std::to_string(ps / W) + " inner", c->stream);
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
@@ -1122,6 +1133,7 @@ struct Driver {
       }
       const int ne = std::min(pe + W, n);
       const int gs = defer_ps >= 0 ? defer_ps : ps;  // K range [gs, pe): this panel, or the pair
+      mark("P" + std::to_string(ps / W) + " outer", c->stream);
       if (la && pe < mn && ne < n) {
         sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne - pe));
         sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, gs, m - pe, pe - gs), x.sub(gs, pe, pe - gs, ne - pe));
@@ -1129,6 +1141,7 @@ struct Driver {
         CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
         CU(cudaEventRecord(ev_main, c->stream));
         CU(cudaStreamWaitEvent(side, ev_main, 0));
+        mark("P" + std::to_string(ps / W) + " side", side);
         Ops aops = ops;
         aops.st = side;
         aops.stop = snap + pidx;
@@ -1144,6 +1157,7 @@ struct Driver {
           defer_ps = -1;
         }
         CU(cudaEventRecord(ev_side, side));
+        mark("P" + std::to_string(ps / W) + " side_end", side);
         side_pending = true;
       } else {
         sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
@@ -1152,6 +1166,19 @@ struct Driver {
       }
     }
     if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+    if (trace) {
+      mark("end", c->stream);
+      CU(cudaDeviceSynchronize());
+      for (auto& te : tev) {
+        float ms = -1.f;
+        if (cudaEventElapsedTime(&ms, tev[0].second, te.second) != cudaSuccess) {
+          cudaGetLastError();
+          ms = -1.f;
+        }
+        fprintf(stderr, "spec %dx%d W=%d: %-14s %9.3f ms\n", m, n, W, te.first.c_str(), ms);
+        cudaEventDestroy(te.second);
+      }
+    }
     cudaEventDestroy(ev_d);
     cudaEventDestroy(ev_t);
     if (la) {
