@@ -183,6 +183,7 @@ struct pluq_ctx {
   int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_pair = 1;             // ... and panel P's far update merges into P+1's (one K = 2W GEMM)
+  int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 24;        // pipeline depth of the host-buffer batched path
   int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
@@ -1069,6 +1070,10 @@ struct Driver {
     // its U12 needs them.  deferred[P] records it for the finishing step after a stop.
     int defer_ps = -1;
     std::vector<char> deferred((size_t)npanels + 1, 0);
+    // la_pair = 2 (group look-ahead, below): first panel of the open group, and which panels
+    // opened a group (for the finishing step after a stop in the group's second panel)
+    int gfirst = -1;
+    std::vector<char> grouped((size_t)npanels + 1, 0);
     // option trace_pipeline: timing events per panel on both streams, printed at the end
     const bool trace = c->trace_pipeline != 0;
     std::vector<std::pair<std::string, cudaEvent_t>> tev;
@@ -1086,6 +1091,12 @@ struct Driver {
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
       mark("P" + std::to_string(ps / W) + " inner", c->stream);
+      // While a side update runs on (SMs - la_reserve) persistent CTAs, a tensor-core GEMM of
+      // this stream launched with a full grid would get only la_reserve SMs for its first
+      // CTAs and the rest after the side update ends (persistent CTAs never yield): cap it.
+      // la_cap 1: cap it at la_reserve CTAs; 2: one CTA per tile, so it also takes the SMs
+      // the side update frees when it ends
+      sops.max_ctas = !(side_pending && c->la_cap) ? 0 : c->la_cap == 2 ? -1 : std::max(1, (int)c->la_reserve);
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
@@ -1127,13 +1138,78 @@ struct Driver {
       if (stopped_early) break;
       // outer step: U rows [ps, pe) right of the panel, then the K = W trailing update
       const View l11 = x.sub(ps, ps, pe - ps, pe - ps);
+      if (la && c->la_pair == 2) {
+        // Group look-ahead: panels P, P+1 form a group.  P's outer step touches only P+1's
+        // columns (it does NOT wait for the previous group's far update, which keeps running
+        // under P's and P+1's factorizations); P+1's outer step waits for it, finishes the
+        // group's U rows for every column right of the group, updates the NEXT group's 2W
+        // columns on this stream (K = 2W) and launches the K = 2W far update on the side.
+        const int pidx = ps / W;
+        const int ne1 = std::min(pe + W, n);
+        if (gfirst < 0 && pe < mn && ne1 <= mn && ne1 < n) {  // P: first panel of a group
+          mark("P" + std::to_string(pidx) + " outer", c->stream);
+          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne1 - pe));
+          sops.gemm(x.sub(pe, pe, m - pe, ne1 - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, ne1 - pe));
+          grouped[pidx] = 1;
+          gfirst = ps;
+          continue;
+        }
+        if (side_pending) {
+          CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+          side_pending = false;
+        }
+        sops.max_ctas = 0;
+        mark("P" + std::to_string(pidx) + " outer", c->stream);
+        const int gs2 = gfirst >= 0 ? gfirst : ps;  // group start (or this panel alone)
+        if (gfirst >= 0 && pe < n) {  // U rows of P for every column right of the group, P's
+          // contribution to P+1's rows there, then U rows of P+1
+          const View l0 = x.sub(gfirst, gfirst, ps - gfirst, ps - gfirst);
+          sops.trsm_l(l0, x.sub(gfirst, pe, ps - gfirst, n - pe));
+          sops.gemm(x.sub(ps, pe, pe - ps, n - pe), x.sub(ps, gfirst, pe - ps, ps - gfirst),
+                    x.sub(gfirst, pe, ps - gfirst, n - pe));
+        }
+        gfirst = -1;
+        const int nn = std::min(pe + (gs2 < ps ? 2 : 1) * W, n);  // columns updated on this stream
+        if (pe < mn && nn < n) {
+          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+          sops.gemm(x.sub(pe, pe, m - pe, nn - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, nn - pe));
+          CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+          CU(cudaEventRecord(ev_main, c->stream));
+          CU(cudaStreamWaitEvent(side, ev_main, 0));
+          mark("P" + std::to_string(pidx) + " side", side);
+          Ops aops = ops;
+          aops.st = side;
+          aops.stop = snap + pidx;
+          aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
+          aops.gemm(x.sub(pe, nn, m - pe, n - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n - nn));
+          CU(cudaEventRecord(ev_side, side));
+          mark("P" + std::to_string(pidx) + " side_end", side);
+          side_pending = true;
+        } else {
+          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+          sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, n - pe));
+        }
+        continue;
+      }
       if (side_pending) {  // rows [ps, pe) right of this panel came from the previous side update
         CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
         side_pending = false;
       }
+      sops.max_ctas = 0;
       const int ne = std::min(pe + W, n);
       const int gs = defer_ps >= 0 ? defer_ps : ps;  // K range [gs, pe): this panel, or the pair
       mark("P" + std::to_string(ps / W) + " outer", c->stream);
+      const bool defer_main = c->la_pair == 3 && defer_ps < 0 && ne < mn && ne + W < n;
+      if (la && pe < mn && ne < n && defer_main) {
+        // la_pair 3: the deferring panel's remaining work (U rows right of the next panel, the
+        // next panel's rows) on this stream, so the next panel factors on an idle GPU
+        sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+        sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, ne - pe));
+        sops.gemm(x.sub(pe, ne, ne - pe, n - ne), x.sub(pe, ps, ne - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
+        deferred[ps / W] = 1;
+        defer_ps = ps;
+        continue;
+      }
       if (la && pe < mn && ne < n) {
         sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne - pe));
         sops.gemm(x.sub(pe, pe, m - pe, ne - pe), x.sub(pe, gs, m - pe, pe - gs), x.sub(gs, pe, pe - gs, ne - pe));
@@ -1147,7 +1223,7 @@ struct Driver {
         aops.stop = snap + pidx;
         aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
         aops.trsm_l(l11, x.sub(ps, ne, pe - ps, n - ne));
-        const bool defer = c->la_pair && defer_ps < 0 && ne < mn && ne + W < n;
+        const bool defer = c->la_pair == 1 && defer_ps < 0 && ne < mn && ne + W < n;
         if (defer) {  // only the next panel's rows now; the rest merges into its update
           aops.gemm(x.sub(pe, ne, ne - pe, n - ne), x.sub(pe, ps, ne - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
           deferred[pidx] = 1;
@@ -1171,13 +1247,15 @@ struct Driver {
       CU(cudaDeviceSynchronize());
       for (auto& te : tev) {
         float ms = -1.f;
-        if (cudaEventElapsedTime(&ms, tev[0].second, te.second) != cudaSuccess) {
+        const cudaError_t er = cudaEventElapsedTime(&ms, tev[0].second, te.second);
+        if (er != cudaSuccess) {
           cudaGetLastError();
           ms = -1.f;
         }
-        fprintf(stderr, "spec %dx%d W=%d: %-14s %9.3f ms\n", m, n, W, te.first.c_str(), ms);
-        cudaEventDestroy(te.second);
+        fprintf(stderr, "spec %dx%d W=%d: %-14s %9.3f ms %s\n", m, n, W, te.first.c_str(), ms,
+                er == cudaSuccess ? "" : cudaGetErrorString(er));
       }
+      for (auto& te : tev) cudaEventDestroy(te.second);  // after the loop: tev[0] is the time origin
     }
     cudaEventDestroy(ev_d);
     cudaEventDestroy(ev_t);
@@ -1201,6 +1279,13 @@ struct Driver {
         // the previous panel deferred its far update into this panel's: apply it on the rows
         // below this panel (its own rows already have it), columns right of this panel
         ops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps - W, m - pe, W), x.sub(ps - W, pe, W, n - pe));
+      }
+      if (ps >= W && grouped[ps / W - 1] && pe < n) {
+        // group look-ahead, stop in the group's second panel: the first panel's U rows and
+        // its contribution to every row below it, right of this panel, are still pending
+        const View l0 = x.sub(ps - W, ps - W, W, W);
+        ops.trsm_l(l0, x.sub(ps - W, pe, W, n - pe));
+        ops.gemm(x.sub(ps, pe, m - ps, n - pe), x.sub(ps, ps - W, m - ps, W), x.sub(ps - W, pe, W, n - pe));
       }
       if (t > 0) {
         const View b11 = x.sub(k0, k0, t, t);
@@ -1642,7 +1727,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair)                                                                            \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap)                                                      \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

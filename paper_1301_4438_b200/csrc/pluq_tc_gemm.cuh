@@ -884,8 +884,11 @@ struct TcGemm {
         return kCuda;
       }
       const int tiles = (n_pad / BN) * (m_pad / TC_BM);
-      const int grid =
-          std::min(tiles, max_ctas > 0 ? max_ctas : grid_override > 0 ? grid_override : num_sms());
+      // max_ctas < 0: one CTA per tile (not persistent), so the grid fills whatever SMs free
+      // up while a persistent kernel on another stream holds the rest
+      const int grid = max_ctas < 0 ? tiles
+                                    : std::min(tiles, max_ctas > 0 ? max_ctas
+                                                                   : grid_override > 0 ? grid_override : num_sms());
       cudaEvent_t e0 = nullptr, e1 = nullptr;
       if (time_mma) {
         cudaEventCreate(&e0);

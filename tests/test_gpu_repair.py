@@ -136,7 +136,7 @@ PAIR_CASES = [
 ]
 
 
-@pytest.mark.parametrize("la_pair", [0, 1])
+@pytest.mark.parametrize("la_pair", [0, 1, 2, 3])
 @pytest.mark.parametrize("name,m,n,r,gs", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
 def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
     """Panel P's far update merged into panel P+1's (option la_pair, one K = 2W GEMM), with
@@ -168,7 +168,7 @@ def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
 
 
-@pytest.mark.parametrize("la_pair", [0, 1])
+@pytest.mark.parametrize("la_pair", [0, 1, 2, 3])
 @pytest.mark.parametrize("W", [384, 640, 768])
 def test_panel_widths_generic_and_repaired(pb, la_pair, W):
     """Panel widths that do not divide the size (partial last panels, pairs cut short), on a
