@@ -594,8 +594,12 @@ def bench_single(pb, name, args, dev, world, rank):
         ts, r2, nbytes = e2e_single(pb, name, host, max(1, args.e2e_steps), 1)
         del host
         e2e_value = work(c["m"], c["n"], r2) * len(ts) / sum(ts) / 1e9
-        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                       "path": "pluq(DenseMatrix(PrimeField(p), float64 numpy)) -> C ABI pluq_factor_host_f64",
+        wire = c["m"] * c["n"] * (2 if c["p"] <= 65536 else 4)  # uint16 / uint32 over PCIe
+        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": wire, "d2h_bytes_per_step": wire,
+                       "host_buffer_bytes": nbytes,
+                       "path": "pluq(DenseMatrix(PrimeField(p), float64 numpy)) -> C ABI pluq_factor_host_f64: host "
+                               "threads convert the float64 buffer to a uint16 wire (p <= 2^16) in pinned chunks, "
+                               "widened on the device; the reverse on the way back",
                        "steps": len(ts), "ms_per_step": 1e3 * sum(ts) / len(ts),
                        "step_ms": [round(1e3 * v, 2) for v in ts]}
         if not args.no_cpu:

@@ -204,7 +204,8 @@ struct pluq_ctx {
   int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
   cudaMemPool_t pool = nullptr;    // the context's own stream-ordered pool (not the device default pool)
   int64_t host_threads = 0;        // host-buffer pipeline: conversion threads (0 = hardware threads, <= 32)
-  int64_t host_chunk_mb = 64;      // host-buffer pipeline: uint32 bytes per pinned staging chunk
+  int64_t host_chunk_mb = 64;      // host-buffer pipeline: wire bytes per pinned staging chunk
+  int64_t host_wire16 = 1;         // host-buffer pipeline, p <= 2^16: 2-byte wire, widened on the device
   std::unique_ptr<HostPool> hpool;
   // backup of a large node for the speculative LU (restored on failure): kept across calls
   // (one node-sized buffer; 2 bytes per entry when p < 2^16), freed by pluq_release_workspace
@@ -1736,6 +1737,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(spec_panel_big, c->spec_panel_big) X(spec_big_elems, c->spec_big_elems)                         \
   X(spec_repairs, c->spec_repairs)                                                                  \
   X(check_inputs, c->check_inputs) X(pool_keep_mb, c->pool_keep_mb) X(host_chunk_mb, c->host_chunk_mb)     \
+  X(host_wire16, c->host_wire16)                                                                    \
   X(host_threads, c->host_threads)
 
 int pluq_set_option(pluq_ctx* c, const char* key, int64_t value) {
@@ -2051,6 +2053,49 @@ __attribute__((target("avx2"))) static void u32_to_f64_avx2(const uint32_t* s, d
   for (; i < count; ++i) d[i] = (double)s[i];
   _mm_sfence();
 }
+// uint16 wire (p <= 2^16): float64 -> uint16 with the same validation, and back.
+__attribute__((target("avx2"))) static bool f64_to_u16_avx2(const double* s, uint16_t* d, int64_t count, uint32_t p) {
+  int64_t i = 0;
+  const __m256d zero = _mm256_setzero_pd(), pd = _mm256_set1_pd((double)p);
+  __m256d bad = _mm256_setzero_pd();
+  bool ok = true;
+  for (; i < count && (reinterpret_cast<uintptr_t>(d + i) & 15); ++i) {
+    const double v = s[i];
+    const bool good = v >= 0.0 && v < (double)p && v == std::floor(v);
+    d[i] = good ? (uint16_t)v : 0;
+    ok &= good;
+  }
+  for (; i + 8 <= count; i += 8) {
+    __m128i q[2];
+    for (int h = 0; h < 2; ++h) {
+      const __m256d v = _mm256_loadu_pd(s + i + 4 * h);
+      const __m256d fl = _mm256_round_pd(v, _MM_FROUND_TO_NEG_INF | _MM_FROUND_NO_EXC);
+      const __m256d b = _mm256_or_pd(_mm256_or_pd(_mm256_cmp_pd(v, zero, _CMP_NGE_UQ), _mm256_cmp_pd(v, pd, _CMP_NLT_UQ)),
+                                     _mm256_cmp_pd(v, fl, _CMP_NEQ_UQ));
+      bad = _mm256_or_pd(bad, b);
+      q[h] = _mm256_cvttpd_epi32(_mm256_andnot_pd(b, v));
+    }
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), _mm_packus_epi32(q[0], q[1]));
+  }
+  ok &= _mm256_movemask_pd(bad) == 0;
+  for (; i < count; ++i) {
+    const double v = s[i];
+    const bool good = v >= 0.0 && v < (double)p && v == std::floor(v);
+    d[i] = good ? (uint16_t)v : 0;
+    ok &= good;
+  }
+  _mm_sfence();
+  return ok;
+}
+__attribute__((target("avx2"))) static void u16_to_f64_avx2(const uint16_t* s, double* d, int64_t count) {
+  int64_t i = 0;
+  for (; i < count && (reinterpret_cast<uintptr_t>(d + i) & 31); ++i) d[i] = (double)s[i];
+  for (; i + 4 <= count; i += 4)
+    _mm256_stream_pd(d + i, _mm256_cvtepi32_pd(_mm_cvtepu16_epi32(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(s + i)))));
+  for (; i < count; ++i) d[i] = (double)s[i];
+  _mm_sfence();
+}
+
 static bool have_avx2() {
   static const bool v = __builtin_cpu_supports("avx2");
   return v;
@@ -2078,6 +2123,34 @@ static bool host_to_u32(const void* src, bool is_f64, uint32_t* dst, int64_t cou
   }
   return ok;
 }
+static bool host_to_u16(const void* src, bool is_f64, uint16_t* dst, int64_t count, uint32_t p) {
+  if (is_f64 && have_avx2()) return f64_to_u16_avx2(static_cast<const double*>(src), dst, count, p);
+  bool ok = true;
+  for (int64_t i = 0; i < count; ++i) {
+    bool good;
+    uint32_t v;
+    if (is_f64) {
+      const double x = static_cast<const double*>(src)[i];
+      good = x >= 0.0 && x < (double)p && x == std::floor(x);
+      v = good ? (uint32_t)x : 0u;
+    } else {
+      const int64_t x = static_cast<const int64_t*>(src)[i];
+      good = x >= 0 && x < (int64_t)p;
+      v = good ? (uint32_t)x : 0u;
+    }
+    dst[i] = (uint16_t)v;
+    ok &= good;
+  }
+  return ok;
+}
+static void host_from_u16(const uint16_t* src, bool is_f64, void* dst, int64_t count) {
+  if (is_f64 && have_avx2()) return u16_to_f64_avx2(src, static_cast<double*>(dst), count);
+  for (int64_t i = 0; i < count; ++i) {
+    if (is_f64) static_cast<double*>(dst)[i] = (double)src[i];
+    else static_cast<int64_t*>(dst)[i] = (int64_t)src[i];
+  }
+}
+
 static void host_from_u32(const uint32_t* src, bool is_f64, void* dst, int64_t count) {
   if (is_f64 && have_avx2()) return u32_to_f64_avx2(src, static_cast<double*>(dst), count);
   if (is_f64) {
@@ -2133,12 +2206,17 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
     // chunks are in flight, so PCIe carries 4 bytes per entry instead of 8; on the way back
     // D2H of later chunks overlaps the widening of earlier ones.  The caller's buffer is
     // written only after the factorization, so invalid input leaves it untouched.
-    const size_t ce = chunk / 4;                                   // entries per chunk
+    // p <= 2^16: the wire carries uint16 (2 bytes per entry), widened on the device
+    const bool w16 = p <= 65536 && c->host_wire16;
+    const size_t wb = w16 ? 2 : 4;                                 // wire bytes per entry
+    const size_t ce = chunk / wb;                                  // entries per chunk
     const int64_t nch = (cnt + (int64_t)ce - 1) / (int64_t)ce;
     char* ring = c->staging_ring(chunk);
     HostPool& hp = c->host_pool();
     const int parts = hp.size() * 2;
     uint32_t* dA = c->dalloc<uint32_t>((size_t)cnt);
+    uint16_t* dstage = w16 ? c->dalloc<uint16_t>((size_t)pluq_ctx::kRing * ce) : nullptr;
+    auto wgrid = [](int64_t ne) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (ne / 8 + 255) / 256)); };
     cudaStream_t* ss = c->side_streams();
     cudaStream_t sin = ss[0], sout = ss[1];
     cudaEvent_t* ev = c->ring_ev;
@@ -2152,19 +2230,29 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       if (k >= pluq_ctx::kRing) CU(cudaEventSynchronize(ev[s]));  // the slot's previous copy is done
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
       uint32_t* slot = reinterpret_cast<uint32_t*>(ring + (size_t)s * chunk);
+      uint16_t* slot16 = reinterpret_cast<uint16_t*>(ring + (size_t)s * chunk);
       const char* src = static_cast<const char*>(hA) + (size_t)e0 * esz;
       hp.run(parts, [&](int t) {  // per-thread ranges start on 16-entry boundaries
         const int64_t a = t ? (ne * t / parts) & ~int64_t(15) : 0;
         const int64_t b = t + 1 < parts ? (ne * (t + 1) / parts) & ~int64_t(15) : ne;
-        if (b > a && !host_to_u32(src + (size_t)a * esz, is_f64, slot + a, b - a, (uint32_t)p)) ok.store(false);
+        if (b > a && !(w16 ? host_to_u16(src + (size_t)a * esz, is_f64, slot16 + a, b - a, (uint32_t)p)
+                           : host_to_u32(src + (size_t)a * esz, is_f64, slot + a, b - a, (uint32_t)p)))
+          ok.store(false);
       });
-      CU(cudaMemcpyAsync(dA + e0, slot, (size_t)ne * 4, cudaMemcpyHostToDevice, sin));
+      if (w16) {  // the slot's event then covers both the pinned and the device staging slot
+        CU(cudaMemcpyAsync(dstage + (size_t)s * ce, slot16, (size_t)ne * 2, cudaMemcpyHostToDevice, sin));
+        widen16_kernel<<<wgrid(ne), 256, 0, sin>>>(dstage + (size_t)s * ce, dA + e0, ne);
+        c->check_launch();
+      } else {
+        CU(cudaMemcpyAsync(dA + e0, slot, (size_t)ne * 4, cudaMemcpyHostToDevice, sin));
+      }
       CU(cudaEventRecord(ev[s], sin));
     }
     CU(cudaEventRecord(je[1], sin));
     CU(cudaStreamWaitEvent(c->stream, je[1], 0));
     if (!ok.load()) {
       c->dfree(dA);
+      if (dstage) c->dfree(dstage);
       c->sync();
       throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
     }
@@ -2174,7 +2262,13 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
     auto issue = [&](int64_t k) {
       const int s = (int)(k % pluq_ctx::kRing);
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
-      CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dA + e0, (size_t)ne * 4, cudaMemcpyDeviceToHost, sout));
+      if (w16) {
+        narrow16_kernel<<<wgrid(ne), 256, 0, sout>>>(dA + e0, dstage + (size_t)s * ce, ne);
+        c->check_launch();
+        CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dstage + (size_t)s * ce, (size_t)ne * 2, cudaMemcpyDeviceToHost, sout));
+      } else {
+        CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dA + e0, (size_t)ne * 4, cudaMemcpyDeviceToHost, sout));
+      }
       CU(cudaEventRecord(ev[s], sout));
     };
     for (int64_t k = 0; k < std::min<int64_t>(nch, pluq_ctx::kRing); ++k) issue(k);
@@ -2183,17 +2277,21 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       CU(cudaEventSynchronize(ev[s]));
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
       const uint32_t* slot = reinterpret_cast<const uint32_t*>(ring + (size_t)s * chunk);
+      const uint16_t* slot16 = reinterpret_cast<const uint16_t*>(ring + (size_t)s * chunk);
       char* dst = static_cast<char*>(hA) + (size_t)e0 * esz;
       hp.run(parts, [&](int t) {
         const int64_t a = t ? (ne * t / parts) & ~int64_t(15) : 0;
         const int64_t b = t + 1 < parts ? (ne * (t + 1) / parts) & ~int64_t(15) : ne;
-        if (b > a) host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
+        if (b <= a) return;
+        if (w16) host_from_u16(slot16 + a, is_f64, dst + (size_t)a * esz, b - a);
+        else host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
       });
       if (k + pluq_ctx::kRing < nch) issue(k + pluq_ctx::kRing);
     }
     CU(cudaEventRecord(je[1], sout));
     CU(cudaStreamWaitEvent(c->stream, je[1], 0));
     c->dfree(dA);
+    if (dstage) c->dfree(dstage);
     c->sync();
   });
 }

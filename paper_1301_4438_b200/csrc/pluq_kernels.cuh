@@ -1447,6 +1447,28 @@ inline size_t diag_fast_smem(int64_t bs, bool tab) {
   return (size_t)(((bs * (bs | 1)) + 3) & ~3ll) * 4 + (tab ? 65536 * 2 : 0);
 }
 
+// uint16 wire of the host pipeline (p <= 2^16): widen / narrow, 8 entries per iteration
+// with 16-byte accesses (chunks start at multiples of the chunk size: aligned).
+__global__ void widen16_kernel(const uint16_t* in, uint32_t* out, int64_t count) {
+  const int64_t n8 = count / 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(in)[t];
+    reinterpret_cast<uint4*>(out)[2 * t] = make_uint4(v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16);
+    reinterpret_cast<uint4*>(out)[2 * t + 1] = make_uint4(v.z & 0xffffu, v.z >> 16, v.w & 0xffffu, v.w >> 16);
+  }
+  for (int64_t t = 8 * n8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = in[t];
+}
+__global__ void narrow16_kernel(const uint32_t* in, uint16_t* out, int64_t count) {
+  const int64_t n8 = count / 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8; t += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = reinterpret_cast<const uint4*>(in)[2 * t], b = reinterpret_cast<const uint4*>(in)[2 * t + 1];
+    reinterpret_cast<uint4*>(out)[t] = make_uint4(a.x | (a.y << 16), a.z | (a.w << 16), b.x | (b.y << 16), b.z | (b.w << 16));
+  }
+  for (int64_t t = 8 * n8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (uint16_t)in[t];
+}
+
 // Host-format conversion: float64 / int64 residues <-> uint32 device storage.  The
 // reference validates canonical residues when a DenseMatrix is built (field.py:140-147,
 // ValueError); here the conversion flags any entry outside [0, p) (or a non-integral /
