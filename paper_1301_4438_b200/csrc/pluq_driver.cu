@@ -199,6 +199,7 @@ struct pluq_ctx {
   int64_t rpm_eager = 1;           // rank-profile kernel, p < 2^16: reduced 32-bit registers (else lazy 64-bit)
   int64_t fb_prefix = 1;           // 64x64 batches: the rank-profile kernel resumes after the generic kernel's pivots
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
+  int64_t tc_trsm_big = 1;         // triangles of 256 .. one GEMM pass: full inverse + one in-place GEMM
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   int64_t check_inputs = 1;        // device inputs: range-check residues first (field.py:140-147 -> EINVAL)
   int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
@@ -428,10 +429,77 @@ struct Ops {
     return true;
   }
 
+  // Full inverse X (r x r, pitch r) of the unit-lower (upper = false) or upper triangle t:
+  // 64-block inverses on the diagonal, then recursive doubling,
+  //   [A 0; B C]^-1 = [A^-1 0; -C^-1 B A^-1  C^-1],  [A B; 0 C]^-1 = [A^-1  -A^-1 B C^-1; 0 C^-1],
+  // the off-diagonal blocks as two modular GEMMs each.  ~r^3/3 MACs.
+  void tri_inverse(const View& t, bool upper, uint32_t* X) {
+    const int r = t.m, nb = (r + TR_BASE - 1) / TR_BASE;
+    uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
+    uint32_t* tmp = c->dalloc_on<uint32_t>((size_t)r * ((r + 1) / 2 + TR_BASE), s());
+    if (upper) trinv_upper_kernel<<<nb, 256, 0, s()>>>(t, inv, mp, c->invtab(mp.p), stop);
+    else trinv_lower_unit_kernel<<<nb, 256, 0, s()>>>(t, inv, mp, stop);
+    c->check_launch();
+    const View xv{X, r, r, r};
+    CU(cudaMemsetAsync(X, 0, (size_t)r * r * sizeof(uint32_t), s()));
+    place_blocks_kernel<<<nb, 256, 0, s()>>>(inv, xv, stop);
+    c->check_launch();
+    for (int b = TR_BASE; b < r; b *= 2)
+      for (int j0 = 0; j0 + b < r; j0 += 2 * b) {
+        const int b2 = std::min(b, r - j0 - b);
+        const View xtt = xv.sub(j0, j0, b, b), xbb = xv.sub(j0 + b, j0 + b, b2, b2);
+        if (!upper) {  // X_bt = -X_bb T_bt X_tt
+          const View tv{tmp, b, b2, b};
+          CU(cudaMemsetAsync(tmp, 0, (size_t)b2 * b * sizeof(uint32_t), s()));
+          gemm(tv, t.sub(j0 + b, j0, b2, b), xtt);  // -T_bt X_tt
+          negate(tv);
+          gemm(xv.sub(j0 + b, j0, b2, b), xbb, tv);
+        } else {       // X_tb = -X_tt U_tb X_bb
+          const View tv{tmp, b2, b, b2};
+          CU(cudaMemsetAsync(tmp, 0, (size_t)b * b2 * sizeof(uint32_t), s()));
+          gemm(tv, t.sub(j0, j0 + b, b, b2), xbb);  // -U_tb X_bb
+          negate(tv);
+          gemm(xv.sub(j0, j0 + b, b, b2), xtt, tv);
+        }
+      }
+    c->dfree_on(tmp, s());
+    c->dfree_on(inv, s());
+  }
+  void negate(const View& v) {
+    dim3 grid((v.n + 255) / 256, grid_rows(v.m));
+    negate_kernel<<<grid, 256, 0, s()>>>(v, mp, stop);
+    c->check_launch();
+  }
+
+  // Large triangles (r >= 256, one exact GEMM pass): B <- T^-1 B (or B U^-1) as ONE in-place
+  // tensor-core GEMM with I - X, X the full inverse (the operands are split into limb planes
+  // before the MMA kernel writes C, so C may alias an operand).  Replaces the recursion whose
+  // 64-row SIMT leaves dominated the 2048-wide panel solves of the speculative LU.
+  bool trsm_big_tc(const View& t, const View& b, bool upper) {
+    const int r = t.m;
+    const int L = TcGemm::limbs(mp.p);
+    if (!c->tc_trsm_big || !c->use_tc || r < 256 || (upper ? b.m : b.n) < c->tc_trsm_min ||
+        r > TcGemm::k_pass(L) || c->tc.k_pass_override > 0)
+      return false;
+    uint32_t* X = c->dalloc_on<uint32_t>((size_t)r * r, s());
+    tri_inverse(t, upper, X);
+    const View mv{X, r, r, r};
+    dim3 grid((r + 255) / 256, grid_rows(r));
+    i_minus_kernel<<<grid, 256, 0, s()>>>(mv, upper ? 1 : 0, mp, stop);  // X <- I - X
+    c->check_launch();
+    const int st = upper ? c->tc.run(b, b, mv, mp, s(), stop, max_ctas) : c->tc.run(b, mv, b, mp, s(), stop, max_ctas);
+    if (st != kOk) throw PluqError(st, "tensor-core TRSM failed: " + c->tc.last_error);
+    ++c->st_tc;
+    c->st_launch += 3;
+    c->dfree_on(X, s());
+    return true;
+  }
+
   void trsm_l(const View& l, const View& b) {
     const int r = l.m;
     if (r == 0 || b.n == 0) return;
     if (trsm128_tc(l, b, false)) return;
+    if (trsm_big_tc(l, b, false)) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
     trinv_lower_unit_kernel<<<nb, 256, 0, s()>>>(l, inv, mp, stop);
@@ -457,6 +525,7 @@ struct Ops {
     const int r = u.m;
     if (r == 0 || b.m == 0) return;
     if (trsm128_tc(u, b, true)) return;
+    if (trsm_big_tc(u, b, true)) return;
     const int nb = (r + TR_BASE - 1) / TR_BASE;
     uint32_t* inv = c->dalloc_on<uint32_t>((size_t)nb * TR_BASE * TR_BASE, s());
     trinv_upper_kernel<<<nb, 256, 0, s()>>>(u, inv, mp, c->invtab(mp.p), stop);
@@ -1078,12 +1147,15 @@ struct Driver {
     // option trace_pipeline: timing events per panel on both streams, printed at the end
     const bool trace = c->trace_pipeline != 0;
     std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    std::vector<double> thost;  // host time when each mark was enqueued
+    const auto th0 = std::chrono::steady_clock::now();
     auto mark = [&](const std::string& label, cudaStream_t st) {
       if (!trace) return;
       cudaEvent_t e;
       CU(cudaEventCreate(&e));
       CU(cudaEventRecord(e, st));
       tev.emplace_back(label, e);
+      thost.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
     };
     cudaStream_t side2 = c->side_streams()[4];
     cudaEvent_t ev_d = nullptr, ev_t = nullptr;
@@ -1253,8 +1325,8 @@ struct Driver {
           cudaGetLastError();
           ms = -1.f;
         }
-        fprintf(stderr, "spec %dx%d W=%d: %-14s %9.3f ms %s\n", m, n, W, te.first.c_str(), ms,
-                er == cudaSuccess ? "" : cudaGetErrorString(er));
+        fprintf(stderr, "spec %dx%d W=%d: %-14s %9.3f ms (host %9.3f ms) %s\n", m, n, W, te.first.c_str(), ms,
+                thost[&te - &tev[0]] - thost[0], er == cudaSuccess ? "" : cudaGetErrorString(er));
       }
       for (auto& te : tev) cudaEventDestroy(te.second);  // after the loop: tev[0] is the time origin
     }
@@ -1733,6 +1805,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
   X(rpm_eager, c->rpm_eager) X(tc_trsm_min, c->tc_trsm_min) X(trace_pipeline, c->trace_pipeline)    \
+  X(tc_trsm_big, c->tc_trsm_big)                                                                    \
   X(spec_block, c->spec_block) X(spec_check, c->spec_check) X(spec_panel, c->spec_panel)            \
   X(spec_panel_big, c->spec_panel_big) X(spec_big_elems, c->spec_big_elems)                         \
   X(spec_repairs, c->spec_repairs)                                                                  \

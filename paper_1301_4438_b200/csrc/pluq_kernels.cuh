@@ -1080,6 +1080,38 @@ __global__ void __launch_bounds__(128) trsm_apply_left_kernel(const uint32_t* li
     }
 }
 
+// Full-inverse assembly for the large-triangle TRSM (Ops::tri_inverse / trsm_big_tc).
+// place_blocks: the 64 x 64 diagonal-block inverses onto the diagonal of X (clipped at r).
+__global__ void place_blocks_kernel(const uint32_t* inv, View x, const int* stop) {
+  if (stopped(stop)) return;
+  const int b0 = blockIdx.x * TR_BASE, w = min(TR_BASE, x.m - b0);
+  const uint32_t* src = inv + (size_t)blockIdx.x * TR_BASE * TR_BASE;
+  for (int idx = threadIdx.x; idx < TR_BASE * TR_BASE; idx += blockDim.x) {
+    const int i = idx >> 6, j = idx & 63;
+    if (i < w && j < w) x.at(b0 + i, b0 + j) = src[idx];
+  }
+}
+__global__ void negate_kernel(View v, ModP mp, const int* stop) {
+  if (stopped(stop)) return;
+  for (int i = blockIdx.y; i < v.m; i += gridDim.y)
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < v.n; j += gridDim.x * blockDim.x) {
+      const uint32_t a = v.at(i, j);
+      v.at(i, j) = a ? mp.p - a : 0u;
+    }
+}
+// X <- I - X on the triangle of X (lower: strictly below the diagonal, whose diagonal is 1;
+// upper: the diagonal and above), zeros elsewhere are kept.
+__global__ void i_minus_kernel(View x, int upper, ModP mp, const int* stop) {
+  if (stopped(stop)) return;
+  for (int i = blockIdx.y; i < x.m; i += gridDim.y)
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < x.n; j += gridDim.x * blockDim.x) {
+      const uint32_t a = x.at(i, j);
+      const uint32_t neg = a ? mp.p - a : 0u;
+      if (i == j) x.at(i, j) = upper ? (neg + 1u == mp.p ? 0u : neg + 1u) : 0u;
+      else x.at(i, j) = neg;
+    }
+}
+
 // flag <- 1 if any diagonal entry of U is zero (kernels.py:93-95).
 __global__ void diag_zero_kernel(View u, int* flag) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < u.m; j += gridDim.x * blockDim.x)
