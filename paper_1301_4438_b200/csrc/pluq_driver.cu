@@ -183,6 +183,7 @@ struct pluq_ctx {
   int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_pair = 1;             // ... and panel P's far update merges into P+1's (one K = 2W GEMM)
+  int64_t inner_la = 1;            // speculative LU: look-ahead between the 128-wide blocks of a panel
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 24;        // pipeline depth of the host-buffer batched path
@@ -1161,6 +1162,19 @@ struct Driver {
     cudaEvent_t ev_d = nullptr, ev_t = nullptr;
     CU(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
+    // Inner look-ahead (option inner_la): block j's update of the panel columns beyond block
+    // j+1 runs on a third stream while block j+1's diagonal kernel and L21 solve run, predicated
+    // on a stop-flag snapshot taken before block j+1 (so a zero pivot there leaves exactly the
+    // sequential state); block j+1's U12 solve and update wait for it.
+    const bool ila = c->inner_la != 0;
+    cudaStream_t side3 = c->side_streams()[2];
+    int* isnap = ila ? c->dalloc<int>((size_t)(mn / BS) + npanels + 2) : nullptr;
+    cudaEvent_t ev_m3 = nullptr, ev_i3 = nullptr;
+    bool in_pending = false;
+    if (ila) {
+      CU(cudaEventCreateWithFlags(&ev_m3, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ev_i3, cudaEventDisableTiming));
+    }
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
       mark("P" + std::to_string(ps / W) + " inner", c->stream);
@@ -1186,10 +1200,13 @@ struct Driver {
                                                               c->d_stop + 1, k0);
         c->check_launch();
         const View b11 = x.sub(k0, k0, bs, bs);
+        if (ila && in_pending && !(c->par_trsm && pe - k0 - bs > 0))
+          CU(cudaStreamWaitEvent(c->stream, ev_i3, 0));  // U12 below runs on this stream
         if (c->par_trsm && pe - k0 - bs > 0) {
           // L21 and U12 are independent: U12 runs on a side stream next to L21
           CU(cudaEventRecord(ev_d, c->stream));
           CU(cudaStreamWaitEvent(side2, ev_d, 0));
+          if (ila && in_pending) CU(cudaStreamWaitEvent(side2, ev_i3, 0));  // rows k0.. right of block j+1
           Ops tops = sops;
           tops.st = side2;
           tops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                    // U12 (panel)
@@ -1200,13 +1217,35 @@ struct Driver {
           sops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, bs), b11);                     // L21
           sops.trsm_l(b11, x.sub(k0, k0 + bs, bs, pe - k0 - bs));                    // U12 (panel)
         }
-        sops.gemm(x.sub(k0 + bs, k0 + bs, m - k0 - bs, pe - k0 - bs), x.sub(k0 + bs, k0, m - k0 - bs, bs),
-                  x.sub(k0, k0 + bs, bs, pe - k0 - bs));
+        in_pending = false;
+        const int nxt = std::min(bs, pe - k0 - bs);  // columns of the next block
+        if (ila && pe - k0 - bs > nxt && nxt > 0) {
+          sops.gemm(x.sub(k0 + bs, k0 + bs, m - k0 - bs, nxt), x.sub(k0 + bs, k0, m - k0 - bs, bs),
+                    x.sub(k0, k0 + bs, bs, nxt));
+          CU(cudaMemcpyAsync(isnap + blk, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+          CU(cudaEventRecord(ev_m3, c->stream));
+          CU(cudaStreamWaitEvent(side3, ev_m3, 0));
+          Ops rops = sops;
+          rops.st = side3;
+          rops.stop = isnap + blk;
+          const int cr = k0 + bs + nxt;
+          rops.gemm(x.sub(k0 + bs, cr, m - k0 - bs, pe - cr), x.sub(k0 + bs, k0, m - k0 - bs, bs),
+                    x.sub(k0, cr, bs, pe - cr));
+          CU(cudaEventRecord(ev_i3, side3));
+          in_pending = true;
+        } else {
+          sops.gemm(x.sub(k0 + bs, k0 + bs, m - k0 - bs, pe - k0 - bs), x.sub(k0 + bs, k0, m - k0 - bs, bs),
+                    x.sub(k0, k0 + bs, bs, pe - k0 - bs));
+        }
         if (blk == 0 || (blk + 1) % c->spec_check == 0) {  // abort early on non-generic input
           CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
           c->sync();
           if (c->h_stop[0]) { stopped_early = true; break; }
         }
+      }
+      if (in_pending) {  // the panel's last look-ahead update
+        CU(cudaStreamWaitEvent(c->stream, ev_i3, 0));
+        in_pending = false;
       }
       if (stopped_early) break;
       // outer step: U rows [ps, pe) right of the panel, then the K = W trailing update
@@ -1315,6 +1354,12 @@ struct Driver {
       }
     }
     if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+    if (in_pending) CU(cudaStreamWaitEvent(c->stream, ev_i3, 0));
+    if (ila) {
+      c->dfree(isnap);
+      cudaEventDestroy(ev_m3);
+      cudaEventDestroy(ev_i3);
+    }
     if (trace) {
       mark("end", c->stream);
       CU(cudaDeviceSynchronize());
@@ -1800,7 +1845,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap)                                                      \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

@@ -136,9 +136,10 @@ PAIR_CASES = [
 ]
 
 
+@pytest.mark.parametrize("inner_la", [0, 1])
 @pytest.mark.parametrize("la_pair", [0, 1, 2, 3])
 @pytest.mark.parametrize("name,m,n,r,gs", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
-def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
+def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs, inner_la):
     """Panel P's far update merged into panel P+1's (option la_pair, one K = 2W GEMM), with
     zero pivots / repairs in either panel of a pair (the finishing step applies a pending
     deferred update)."""
@@ -150,7 +151,7 @@ def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs):
     cc = orc.Counts()
     P, Q, R, _ = orc.pluq(x, p, 30, cc)
     ctx = _native.context()
-    opts = dict(small_cap=1, spec_panel=256, la_pair=la_pair)
+    opts = dict(small_cap=1, spec_panel=256, la_pair=la_pair, inner_la=inner_la)
     old = {k: ctx.get_option(k) for k in opts}
     for k, v in opts.items():
         ctx.set_option(k, v)
