@@ -200,7 +200,7 @@ struct pluq_ctx {
   int64_t rpm_eager = 1;           // rank-profile kernel, p < 2^16: reduced 32-bit registers (else lazy 64-bit)
   int64_t fb_prefix = 1;           // 64x64 batches: the rank-profile kernel resumes after the generic kernel's pivots
   int64_t tc_trsm_min = 256;       // ... when the solved panel has at least this many rows / columns
-  int64_t tc_trsm_big = 1;         // triangles of 256 .. one GEMM pass: full inverse + one in-place GEMM
+  int64_t tc_trsm_big = 4;         // triangles of 256 .. one GEMM pass solved at least this many times as wide: full inverse + one in-place GEMM (0 = off)
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   int64_t check_inputs = 1;        // device inputs: range-check residues first (field.py:140-147 -> EINVAL)
   int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
@@ -479,7 +479,10 @@ struct Ops {
   bool trsm_big_tc(const View& t, const View& b, bool upper) {
     const int r = t.m;
     const int L = TcGemm::limbs(mp.p);
-    if (!c->tc_trsm_big || !c->use_tc || r < 256 || (upper ? b.m : b.n) < c->tc_trsm_min ||
+    const int wide = upper ? b.m : b.n;
+    // the inverse costs ~r^3/3 MACs and ~30 short launches: only worth it for solves much
+    // wider than the triangle (cfg5's U rows right of a 2048-wide panel: 61440 x 2048)
+    if (!c->tc_trsm_big || !c->use_tc || r < 256 || wide < c->tc_trsm_min || (int64_t)wide < c->tc_trsm_big * r ||
         r > TcGemm::k_pass(L) || c->tc.k_pass_override > 0)
       return false;
     uint32_t* X = c->dalloc_on<uint32_t>((size_t)r * r, s());

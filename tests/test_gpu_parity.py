@@ -202,7 +202,7 @@ def test_trsm_remultiplication(pb, p):  # test_kernels.py:114-134
     kern = pb.CudaKernels(field)
     # the last three take the large-triangle path (full inverse + one in-place GEMM) when
     # the solved side is >= 256 wide: r = 256 exactly, r not a multiple of 64, r = 2048
-    for r, n in [(1, 5), (7, 0), (33, 40), (64, 17), (65, 3), (200, 150), (256, 300), (700, 1030), (2048, 600)]:
+    for r, n in [(1, 5), (7, 0), (33, 40), (64, 17), (65, 3), (200, 150), (256, 1100), (700, 3000), (2048, 8200)]:
         l = np.tril(rng.integers(0, p, (r, r)), -1).astype(field.dtype)
         b = rng.integers(0, p, (r, n)).astype(field.dtype)
         orig = b.astype(np.int64).copy()
