@@ -36,6 +36,9 @@ from .matrix import DenseMatrix, OpCounts, Permutation, PluqFactors
 
 DEFAULT_PANEL = 1024
 
+# outcome of the last pluq_distributed on this rank 0: {"fallback": bool, "repaired_panels": int}
+last_info: dict = {}
+
 
 class CudaPanelBackend:
     """Panel operations on CUDA int32 tensors through the C ABI (this rank's device)."""
@@ -46,7 +49,8 @@ class CudaPanelBackend:
         self.lib = self.ctx.lib
 
     def factor_panel(self, x):
-        """In-place exact PLUQ of a contiguous panel; returns (rank, generic)."""
+        """In-place exact PLUQ of a contiguous panel; returns (rank, rows_in_order, Q.sigma):
+        rows_in_order means P = I, and then the panel holds the LU of panel[:, Q]."""
         m, n = x.shape
         P = np.empty(m, np.int64)
         Q = np.empty(n, np.int64)
@@ -55,8 +59,7 @@ class CudaPanelBackend:
         st = self.lib.pluq_factor(self.ctx.handle, x.data_ptr(), x.stride(0), m, n, self.p, self.threshold,
                                   _native.i64p(P), _native.i64p(Q), _native.i64p(r), _native.i64p(c))
         _native.raise_for(st, self.ctx, "pluq_factor (panel)")
-        generic = bool(np.array_equal(P, np.arange(m)) and np.array_equal(Q, np.arange(n)))
-        return int(r[0]), generic
+        return int(r[0]), bool(np.array_equal(P, np.arange(m))), Q
 
     def trsm_llu(self, l, b):
         """b <- l^-1 b, l unit lower (strided views)."""
@@ -76,6 +79,32 @@ class CudaPanelBackend:
                                    ctypes.byref(out))
         _native.raise_for(st, self.ctx, "pluq_nonzero")
         return out.value == 0
+
+
+def _panel_verdict(res, wk: int, colperm):
+    """(rank, usable, q) from a backend's factor_panel result.  A panel is usable when its
+    rows stay in order (P = I) and, unless column repairs are collected (colperm is a list),
+    its columns too.  q: the panel's Q.sigma when it is not the identity, else None."""
+    if len(res) == 2:  # legacy backends: (rank, generic)
+        return int(res[0]), bool(res[1]), None
+    rk, rows_ok, q = res
+    q = None if q is None or np.array_equal(np.asarray(q), np.arange(wk)) else np.asarray(q, dtype=np.int64)
+    usable = bool(rows_ok) and (q is None or colperm is not None)
+    return int(rk), usable, q
+
+
+def _share_q(q, wk: int, owner: int, flags, colperm, c0: int, world: int) -> None:
+    """Broadcast a repaired panel's column permutation and record it (global indices)."""
+    import torch
+    import torch.distributed as dist
+
+    buf = torch.zeros(wk, dtype=torch.int64, device=flags.device)
+    if q is not None:
+        buf.copy_(torch.from_numpy(q))
+    if world > 1:
+        dist.broadcast(buf, src=owner)
+    colperm.append((c0, buf.cpu().numpy().astype(np.int64)))
+    return buf
 
 
 def panel_bounds(n: int, width: int) -> list[tuple[int, int]]:
@@ -159,10 +188,15 @@ def gather_panels(slab: LocalSlab, a_full, m: int, n: int, width: int, make_empt
             dist.send(slab.panel(k).contiguous(), dst=0)
 
 
-def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags):
+def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags, colperm=None):
     """Factor the distributed panels in place.  Returns the rank r when the matrix has a
     generic rank profile (then P = Q = I), or None when it does not (panels are then
-    partially updated; the caller restarts from the original on one GPU)."""
+    partially updated; the caller restarts from the original on one GPU).
+
+    colperm (a list) also accepts panels whose factorization permuted only their own
+    columns (the pivot repair of a coincidental zero minor, csrc speculative_lu): the panel
+    then holds the LU of its columns in that order, later steps only use its L part, and
+    (c0, Q.sigma) is appended for the caller's check of the global rank profile matrix."""
     import torch.distributed as dist
 
     rank, world = _world()
@@ -174,16 +208,22 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
         wk = c1 - c0
         flag = flags()
         pan = flags.new_panel(m - c0, wk)  # contiguous broadcast buffer
+        q = None
         if rank == owner:
             pview = slab.panel(k)[c0:, :]
-            rk, generic = backend.factor_panel(pview)
+            rk, generic, q = _panel_verdict(backend.factor_panel(pview), wk, colperm)
             pan.copy_(pview)
-            flag[0], flag[1] = rk, int(generic)
+            flag[0], flag[1] = rk, int(generic) + 2 * int(q is not None)
         if world > 1:
             dist.broadcast(flag, src=owner)
-        rk, generic = int(flag[0]), bool(int(flag[1]))
+        rk, generic, repaired = int(flag[0]), bool(int(flag[1]) & 1), bool(int(flag[1]) & 2)
         if not generic:
             return None
+        if repaired:
+            qt = _share_q(q, wk, owner, flags, colperm, c0, world)
+            if rank == owner and c0 > 0:  # the U rows of earlier pivots in these columns move too
+                top = slab.panel(k)[:c0, :]
+                top.copy_(top[:, qt.to(top.device)])
         if world > 1:
             dist.broadcast(pan, src=owner)
         g = c0 + rk
@@ -332,8 +372,10 @@ def gather_2d(loc: LocalBlocks, a_full, m, n, width, grid: Grid2D, make_empty):
             dist.send(loc.t.contiguous(), dst=0)
 
 
-def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid: Grid2D, backend, flags):
-    """distributed_generic_lu on a pr x pc grid (same contract: the rank r, or None)."""
+def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid: Grid2D, backend, flags,
+                              colperm=None):
+    """distributed_generic_lu on a pr x pc grid (same contract: the rank r, or None; the
+    same column-repair collection through colperm)."""
     import torch
     import torch.distributed as dist
 
@@ -372,14 +414,22 @@ def distributed_generic_lu_2d(loc: LocalBlocks, m: int, n: int, width: int, grid
                 dist.send(mine.contiguous(), dst=root)
         # 2. factor on the root, broadcast the verdict and the factored panel
         flag = flags()
+        q = None
         if rank == root:
-            rk, generic = backend.factor_panel(pan)
-            flag[0], flag[1] = rk, int(generic)
+            rk, generic, q = _panel_verdict(backend.factor_panel(pan), wk, colperm)
+            flag[0], flag[1] = rk, int(generic) + 2 * int(q is not None)
         if world > 1:
             dist.broadcast(flag, src=root)
-        rk, generic = int(flag[0]), bool(int(flag[1]))
+        rk, generic, repaired = int(flag[0]), bool(int(flag[1]) & 1), bool(int(flag[1]) & 2)
         if not generic:
             return None
+        if repaired:
+            qt = _share_q(q, wk, root, flags, colperm, c0, world)
+            if grid.gc == gck:  # the U rows of earlier pivots in these columns move too
+                lr0 = loc.first_row_at_or_after(c0)
+                if lr0 > 0:
+                    top = loc.panel(k)[:lr0, :]
+                    top.copy_(top[:, qt.to(top.device)])
         if world > 1:
             dist.broadcast(pan, src=root)
         g = c0 + rk
@@ -457,6 +507,7 @@ def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: i
     if backend is None:
         backend = CudaPanelBackend(p, threshold, device.index if device.type == "cuda" else 0)
     flags = _Flags(device, torch.int32 if device.type == "cuda" else torch.int64)
+    colperm: list = []  # (c0, Q.sigma) of panels whose factorization repaired a zero minor
     if rank == 0:
         x = a.data
         if tuple(x.shape) != (m, n):
@@ -472,25 +523,43 @@ def pluq_distributed(a: DenseMatrix | None, m: int, n: int, p: int, threshold: i
         if world > 1:
             g2.make_groups()
         loc = scatter_2d(full, m, n, width, g2, flags.empty)
-        r = distributed_generic_lu_2d(loc, m, n, width, g2, backend, flags)
+        r = distributed_generic_lu_2d(loc, m, n, width, g2, backend, flags, colperm)
         if r is not None:
             gather_2d(loc, full if rank == 0 else None, m, n, width, g2, flags.empty)
     else:
         slab = scatter_panels(full, m, n, width, flags.empty)
-        r = distributed_generic_lu(slab, m, n, width, backend, flags)
+        r = distributed_generic_lu(slab, m, n, width, backend, flags, colperm)
         if r is not None:
             gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
     if rank != 0:
         return r
+    q_sig = np.arange(n, dtype=np.int64)
+    c = np.zeros(4, np.int64)
+    lib = _native.load_library()
+    if r is not None and colperm:
+        # the panels' column repairs compose into sigma; R_A = {(k, sigma(k))} (rows in
+        # order), and the result is the reference's exactly when Alg.1 replayed on R_A gives
+        # P = I and Q = sigma (csrc speculative_lu, fact (2)) -- else the exact fallback
+        for c0, q in colperm:
+            q_sig[c0:c0 + len(q)] = c0 + q
+        P = np.zeros(m, np.int64)
+        Q = np.zeros(n, np.int64)
+        prow = np.arange(r, dtype=np.int64)
+        pcol = np.ascontiguousarray(q_sig[:r])
+        st = lib.pluq_rank_profile_replay(m, n, threshold, r, _native.i64p(prow), _native.i64p(pcol),
+                                          _native.i64p(P), _native.i64p(Q), _native.i64p(c))
+        if st != 0 or not (np.array_equal(P, np.arange(m)) and np.array_equal(Q, q_sig)):
+            r = None
+    last_info.update(fallback=r is None, repaired_panels=len(colperm))
     if r is None:  # not generic: the exact recursion on one GPU, from the untouched original
         from .recursive import pluq
 
         return pluq(a, threshold=threshold, counts=counts)
     a.data.copy_(full)
     if counts is not None:
-        c = np.zeros(4, np.int64)
-        _native.raise_for(_native.load_library().pluq_generic_counts(m, n, r, threshold, _native.i64p(c)), None,
-                          "pluq_generic_counts")
+        if not colperm:
+            _native.raise_for(lib.pluq_generic_counts(m, n, r, threshold, _native.i64p(c)), None,
+                              "pluq_generic_counts")
         counts.field_mul += int(c[0]); counts.field_add += int(c[1])
         counts.field_inv += int(c[2]); counts.modular_reductions += int(c[3])
-    return PluqFactors(Permutation(np.arange(m, dtype=np.int64)), Permutation(np.arange(n, dtype=np.int64)), r, a)
+    return PluqFactors(Permutation(np.arange(m, dtype=np.int64)), Permutation(q_sig), r, a)

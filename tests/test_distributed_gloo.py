@@ -29,7 +29,7 @@ class NumpyPanelBackend:
         f = a.astype(orc.field_dtype(self.p))
         P, Q, r, _ = orc.pluq(f, self.p, self.threshold)
         a[...] = f.astype(np.int64)
-        return r, bool(np.array_equal(P, np.arange(a.shape[0])) and np.array_equal(Q, np.arange(a.shape[1])))
+        return r, bool(np.array_equal(P, np.arange(a.shape[0]))), np.asarray(Q, dtype=np.int64)
 
     def trsm_llu(self, l, b):
         bb = b.numpy().astype(orc.field_dtype(self.p))
@@ -204,6 +204,30 @@ def test_four_rank_2d_grid_vs_oracle():
 
 
 @pytest.mark.gpu
+def test_cuda_distributed_repaired_coincidence(cuda_ok):
+    """pluq_distributed on a matrix with a coincidental zero minor (the seed-0 cfg5
+    structure) stays on the distributed path: the panel repair, then the replay check."""
+    import torch
+
+    import paper_1301_4438_b200 as pb
+    from paper_1301_4438_b200 import distributed as D
+
+    p, m, n, g = 65521, 600, 640, 150
+    a0 = _coincidence(m, n, g, p, 5)
+    x = a0.astype(np.float64)
+    c0 = orc.Counts()
+    P, Q, rr, _ = orc.pluq(x, p, 30, c0)
+    for grid in (None, (1, 1)):
+        a = pb.DenseMatrix(pb.PrimeField(p), torch.from_numpy(a0).cuda().to(torch.int32))
+        c = pb.OpCounts()
+        f = D.pluq_distributed(a, m, n, p, 30, width=128, counts=c, grid=grid)
+        assert not D.last_info["fallback"] and D.last_info["repaired_panels"] == 1
+        assert f.rank == rr and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+        assert np.array_equal(a.data.cpu().numpy().astype(np.int64), x.astype(np.int64))
+        assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == c0.as_tuple()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,m,n,r,p,width", [
     ("full", 300, 300, None, 65521, 64), ("wide", 200, 420, None, 65521, 96),
     ("rank150", 320, 300, 150, 65521, 64), ("p23", 256, 256, None, 8388593, 64),
@@ -228,3 +252,87 @@ def test_cuda_panels_vs_oracle(cuda_ok, name, m, n, r, p, width, grid):
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == \
            (c0.field_mul, c0.field_add, c0.field_inv, c0.modular_reductions)
     assert f.packed is a
+
+
+# ---------------------------------------------------------------------------------------
+# a coincidental zero leading minor (the seed-0 cfg5 structure): the panel holding it
+# permutes only its own columns; the ranks collect that permutation and rank 0 checks the
+# global rank profile matrix with the replay of Alg. 1 (pluq_rank_profile_replay)
+# ---------------------------------------------------------------------------------------
+
+
+def _coincidence(m, n, g, p, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(0, p, (m, n))
+    coef = rng.integers(0, p, g).astype(object)
+    a[g, :g + 1] = np.array((coef @ a[:g, :g + 1].astype(object)) % p, dtype=np.int64)
+    return a
+
+
+COINC = [("inside_panel", 40, 44, 11), ("second_rank_panel", 40, 40, 19), ("last_row_panel", 32, 40, 29)]
+
+
+def _worker_coinc(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_4438_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for grid in (None, (2, 1), (1, 2)):
+            for name, m, n, g in COINC:
+                p, width = 65521, 8
+                a0 = _coincidence(m, n, g, p, g)
+                full = torch.from_numpy(a0.astype(np.int64)) if rank == 0 else None
+                flags = D._Flags(torch.device("cpu"), torch.int64)
+                colperm = []
+                if grid is None:
+                    slab = D.scatter_panels(full, m, n, width, flags.empty)
+                    rk = D.distributed_generic_lu(slab, m, n, width, NumpyPanelBackend(p, 30), flags, colperm)
+                    if rk is not None:
+                        D.gather_panels(slab, full if rank == 0 else None, m, n, width, flags.empty)
+                else:
+                    g2 = D.Grid2D(grid[0], grid[1], rank)
+                    g2.make_groups()
+                    loc = D.scatter_2d(full, m, n, width, g2, flags.empty)
+                    rk = D.distributed_generic_lu_2d(loc, m, n, width, g2, NumpyPanelBackend(p, 30), flags, colperm)
+                    if rk is not None:
+                        D.gather_2d(loc, full if rank == 0 else None, m, n, width, g2, flags.empty)
+                out.append((grid, name, rk, [(c0, qq.tolist()) for c0, qq in colperm],
+                            full.numpy().copy() if rank == 0 and rk is not None else None))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_column_repairs_vs_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_coinc, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    i = 0
+    for grid in (None, (2, 1), (1, 2)):
+        for name, m, n, g in COINC:
+            p = 65521
+            a0 = _coincidence(m, n, g, p, g)
+            x = a0.astype(np.float64)
+            P, Q, rr, _ = orc.pluq(x, p, 30)
+            assert np.array_equal(P, np.arange(m)) and not np.array_equal(Q, np.arange(n)), name
+            r0, r1 = res[0][i], res[1][i]
+            assert r0[2] == r1[2] == rr and r0[3] == r1[3], (grid, name)  # same decision and repairs
+            sig = np.arange(n)
+            for c0, qq in r0[3]:
+                sig[c0:c0 + len(qq)] = c0 + np.asarray(qq)
+            assert np.array_equal(sig, Q), (grid, name)
+            assert np.array_equal(r0[4], x.astype(np.int64)), (grid, name)
+            i += 1
