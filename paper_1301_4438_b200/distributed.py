@@ -188,7 +188,8 @@ def gather_panels(slab: LocalSlab, a_full, m: int, n: int, width: int, make_empt
             dist.send(slab.panel(k).contiguous(), dst=0)
 
 
-def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags, colperm=None):
+def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags, colperm=None,
+                           lookahead: bool = True):
     """Factor the distributed panels in place.  Returns the rank r when the matrix has a
     generic rank profile (then P = Q = I), or None when it does not (panels are then
     partially updated; the caller restarts from the original on one GPU).
@@ -196,23 +197,33 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
     colperm (a list) also accepts panels whose factorization permuted only their own
     columns (the pivot repair of a coincidental zero minor, csrc speculative_lu): the panel
     then holds the LU of its columns in that order, later steps only use its L part, and
-    (c0, Q.sigma) is appended for the caller's check of the global rank profile matrix."""
+    (c0, Q.sigma) is appended for the caller's check of the global rank profile matrix.
+
+    lookahead: the owner of panel k+1 updates that panel's columns with panel k FIRST, factors
+    it, and only then updates the rest of its later panels, so the factorization of k+1 hides
+    behind the other ranks' trailing updates (the HPL look-ahead); collectives keep the same
+    order on every rank."""
     import torch.distributed as dist
 
     rank, world = _world()
     mn = min(m, n)
-    for k, (c0, c1) in enumerate(panel_bounds(n, width)):
-        if c0 >= mn:
-            break
+    bounds = [b for b in panel_bounds(n, width) if b[0] < mn]
+
+    def factor(k):
+        c0, c1 = bounds[k]
+        return _panel_verdict(backend.factor_panel(slab.panel(k)[c0:, :]), c1 - c0, colperm)
+
+    ahead = factor(0) if bounds and rank == panel_owner(0, world) else None
+    for k, (c0, c1) in enumerate(bounds):
         owner = panel_owner(k, world)
         wk = c1 - c0
         flag = flags()
         pan = flags.new_panel(m - c0, wk)  # contiguous broadcast buffer
         q = None
         if rank == owner:
-            pview = slab.panel(k)[c0:, :]
-            rk, generic, q = _panel_verdict(backend.factor_panel(pview), wk, colperm)
-            pan.copy_(pview)
+            rk, generic, q = ahead if ahead is not None else factor(k)
+            ahead = None
+            pan.copy_(slab.panel(k)[c0:, :])
             flag[0], flag[1] = rk, int(generic) + 2 * int(q is not None)
         if world > 1:
             dist.broadcast(flag, src=owner)
@@ -229,10 +240,17 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
         g = c0 + rk
         rest = slab.after(k)
         if rest is not None and rk > 0:
-            top = rest[c0:g, :]
-            backend.trsm_llu(pan[:rk, :rk], top)                  # U12: pivot rows of the later panels
-            if g < m:
-                backend.gemm_sub(rest[g:, :], pan[rk:, :rk], top)  # A22 -= L21 U12
+            la = lookahead and rk == wk and k + 1 < len(bounds) and rank == panel_owner(k + 1, world)
+            w1 = slab.w[k + 1] if la else 0
+            parts = [(0, w1), (w1, rest.shape[1])] if la else [(0, rest.shape[1])]
+            for i, (a0, a1) in enumerate(parts):
+                if a1 > a0:
+                    top = rest[c0:g, a0:a1]
+                    backend.trsm_llu(pan[:rk, :rk], top)                          # U12 rows
+                    if g < m:
+                        backend.gemm_sub(rest[g:, a0:a1], pan[rk:, :rk], top)  # A22 -= L21 U12
+                if la and i == 0:
+                    ahead = factor(k + 1)  # panel k+1 is up to date: factor it now
         if rk < wk:
             # zero pivot at g: generic only if the whole Schur complement A[g:, g:] vanishes
             # (panel k's own part was checked by the exact panel factorization)
