@@ -203,6 +203,7 @@ struct pluq_ctx {
   int64_t tc_trsm_big = 4;         // triangles of 256 .. one GEMM pass solved at least this many times as wide: full inverse + one in-place GEMM (0 = off)
   int64_t rpm_threads = 512;       // CTA size of the rank-profile kernel (16 warps: 64 rows in registers)
   int64_t check_inputs = 1;        // device inputs: range-check residues first (field.py:140-147 -> EINVAL)
+  bool range_check_pending = false;  // the top node's speculative LU validates in its backup copy
   int64_t pool_keep_mb = 2048;     // the context's memory pool is trimmed to this after every call
   cudaMemPool_t pool = nullptr;    // the context's own stream-ordered pool (not the device default pool)
   int64_t host_threads = 0;        // host-buffer pipeline: conversion threads (0 = hardware threads, <= 32)
@@ -622,10 +623,16 @@ struct Ops {
     c->check_launch();
   }
 
-  void copy_to16(uint16_t* dst, const View& src) {
+  void copy_to16(uint16_t* dst, const View& src, int* bad = nullptr) {
     if (src.m == 0 || src.n == 0) return;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ((int64_t)src.m * src.n / 4 + 255) / 256));
-    copy_to16_kernel<<<grid, 256, 0, c->stream>>>(dst, src);
+    copy_to16_kernel<<<grid, 256, 0, c->stream>>>(dst, src, mp.p, bad);
+    c->check_launch();
+  }
+  void backup32(uint32_t* dst, const View& src, int* bad) {
+    if (src.m == 0 || src.n == 0) return;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ((int64_t)src.m * src.n + 255) / 256));
+    backup32_kernel<<<grid, 256, 0, c->stream>>>(dst, src, mp.p, bad);
     c->check_launch();
   }
   void copy_from16(const View& dst, const uint16_t* src) {
@@ -743,13 +750,23 @@ struct SymHost {
   const std::vector<int>& cp;  // original column -> original row (-1: none)
   int thr;
   Counts cnt{0, 0, 0, 0};
-  std::vector<int> rmark, cmark;  // stamp of the current node's row / column lists
+  std::vector<int> cmark;         // stamp of the current node's column list
   std::vector<int> rpos, cpos;    // local position of an original row / column in a base case
   int stamp = 0;
+  // bump stack for the index lists of the recursion (children are processed one after the
+  // other, so a node's lists are released when it returns): no allocation per node
+  std::vector<int> stack;
+  size_t top = 0;
+  int* take(size_t k) {
+    int* p = stack.data() + top;
+    top += k;
+    if (top > stack.size()) throw std::runtime_error("symbolic replay: stack overflow");
+    return p;
+  }
 
   SymHost(const std::vector<int>& rp_, const std::vector<int>& cp_, int thr_)
-      : rp(rp_), cp(cp_), thr(thr_), rmark(rp_.size(), 0), cmark(cp_.size(), 0), rpos(rp_.size(), -1),
-        cpos(cp_.size(), -1) {}
+      : rp(rp_), cp(cp_), thr(thr_), cmark(cp_.size(), 0), rpos(rp_.size(), -1), cpos(cp_.size(), -1),
+        stack(16 * (rp_.size() + cp_.size()) + 1024) {}
 
   bool has_pivot(const int* rows, const int* cols, int m, int n) {
     ++stamp;
@@ -764,10 +781,18 @@ struct SymHost {
   // Alg.2 frontier walk (the host twin of sym_base): P[local row] = position, Q[position]
   // = local column, pivots first, then the rest in local order.
   int base(const int* rows, const int* cols, int m, int n, int* P, int* Q) {
+    const size_t mark = top;
     for (int a = 0; a < m; ++a) rpos[rows[a]] = a;
     for (int b = 0; b < n; ++b) cpos[cols[b]] = b;
-    std::vector<int> lr(m, -1), lc(n, -1), ro, co;
+    const int mn = std::min(m, n);
+    int* lr = take(m);
+    int* lc = take(n);
+    int* ro = take(mn);
+    int* co = take(mn);
+    int* rowpos = take(m);
+    int* colpos = take(n);
     for (int a = 0; a < m; ++a) {
+      lr[a] = -1;
       const int x = rp[rows[a]];
       if (x >= 0) {
         const int q = cpos[x];
@@ -775,23 +800,24 @@ struct SymHost {
       }
     }
     for (int b = 0; b < n; ++b) {
+      lc[b] = -1;
       const int y = cp[cols[b]];
       if (y >= 0) {
         const int q = rpos[y];
         if (q >= 0 && q < m && rows[q] == y) lc[b] = q;
       }
     }
-    int i = 0, j = 0;
+    int i = 0, j = 0, r = 0;
     while (i < m || j < n) {
       int pr = -1, pc = -1;
       if (j < n && lc[j] >= 0 && lc[j] < i) { pr = lc[j]; pc = j; ++j; }
       else if (i < m && lr[i] >= 0 && lr[i] < j) { pr = i; pc = lr[i]; ++i; }
       else if (i < m && j < n && lr[i] == j) { pr = i; pc = j; ++i; ++j; }
       else { i = std::min(i + 1, m); j = std::min(j + 1, n); continue; }
-      ro.push_back(pr);
-      co.push_back(pc);
+      ro[r] = pr;
+      co[r] = pc;
+      ++r;
     }
-    const int r = (int)ro.size();
     for (int k = 0; k < r; ++k) {  // charges of iterative.py:59-75 per pivot
       long long below = m - 1 - ro[k], right = n - 1 - co[k];
       for (int t = 0; t < k; ++t) { below -= ro[t] > ro[k]; right -= co[t] > co[k]; }
@@ -799,13 +825,15 @@ struct SymHost {
         cnt.inv += 1; cnt.mul += below + below * right; cnt.add += below * right; cnt.red += below + below * right;
       }
     }
-    std::vector<int> rowpos(m, -1), colpos(n, -1);
+    for (int a = 0; a < m; ++a) rowpos[a] = -1;
+    for (int b = 0; b < n; ++b) colpos[b] = -1;
     for (int k = 0; k < r; ++k) { rowpos[ro[k]] = k; colpos[co[k]] = k; }
     for (int x = 0, nxt = r; x < m; ++x) P[x] = rowpos[x] >= 0 ? rowpos[x] : nxt++;
     for (int k = 0; k < r; ++k) Q[k] = co[k];
     for (int x = 0, nxt = r; x < n; ++x) if (colpos[x] < 0) Q[nxt++] = x;
     for (int a = 0; a < m; ++a) rpos[rows[a]] = -1;
     for (int b = 0; b < n; ++b) cpos[cols[b]] = -1;
+    top = mark;
     return r;
   }
 
@@ -816,10 +844,13 @@ struct SymHost {
       return 0;
     }
     if (m == 1 || n == 1 || std::min(m, n) <= thr) return base(rows, cols, m, n, P, Q);
+    const size_t mark = top;
     const int kr = m / 2, kc = n / 2;
-    std::vector<int> P1(kr), Q1(kc);
-    const int r1 = rec(rows, cols, kr, kc, P1.data(), Q1.data());
-    std::vector<int> rt(kr), cl(kc);
+    int* P1 = take(kr);
+    int* Q1 = take(kc);
+    const int r1 = rec(rows, cols, kr, kc, P1, Q1);
+    int* rt = take(kr);
+    int* cl = take(kc);
     for (int a = 0; a < kr; ++a) rt[P1[a]] = rows[a];
     for (int t = 0; t < kc; ++t) cl[t] = cols[Q1[t]];
     charge_trsm_l(cnt, r1, n - kc);
@@ -827,10 +858,14 @@ struct SymHost {
     charge_mm(cnt, kr - r1, n - kc, r1);
     charge_mm(cnt, m - kr, kc - r1, r1);
     charge_mm(cnt, m - kr, n - kc, r1);
-    std::vector<int> P2(kr - r1), Q2(n - kc), P3(m - kr), Q3(kc - r1);
-    const int r2 = rec(rt.data() + r1, cols + kc, kr - r1, n - kc, P2.data(), Q2.data());
-    const int r3 = rec(rows + kr, cl.data() + r1, m - kr, kc - r1, P3.data(), Q3.data());
-    std::vector<int> hr(m - kr), hc(n - kc);
+    int* P2 = take(kr - r1);
+    int* Q2 = take(n - kc);
+    int* P3 = take(m - kr);
+    int* Q3 = take(kc - r1);
+    const int r2 = rec(rt + r1, cols + kc, kr - r1, n - kc, P2, Q2);
+    const int r3 = rec(rows + kr, cl + r1, m - kr, kc - r1, P3, Q3);
+    int* hr = take(m - kr);
+    int* hc = take(n - kc);
     for (int a = 0; a < m - kr; ++a) hr[P3[a]] = rows[kr + a];
     for (int t = 0; t < n - kc; ++t) hc[t] = cols[kc + Q2[t]];
     const int m4 = m - kr - r3, n4 = n - kc - r2;
@@ -841,8 +876,9 @@ struct SymHost {
     charge_mm(cnt, r3, n4, r2);
     charge_mm(cnt, m4, n4, r2);
     charge_mm(cnt, m4, n4, r3);
-    std::vector<int> P4(m4), Q4(n4);
-    const int r4 = rec(hr.data() + r3, hc.data() + r2, m4, n4, P4.data(), Q4.data());
+    int* P4 = take(m4);
+    int* Q4 = take(n4);
+    const int r4 = rec(hr + r3, hc + r2, m4, n4, P4, Q4);
     for (int t = 0; t < m; ++t) {
       int y;
       if (t < kr) { const int z = P1[t]; y = z < r1 ? z : r1 + P2[z - r1]; }
@@ -856,6 +892,7 @@ struct SymHost {
       else { const int zz = z - kc; const int w = zz < r2 ? zz : r2 + Q4[zz - r2]; y = kc + Q2[w]; }
       Q[t] = y;
     }
+    top = mark;
     return r1 + r2 + r3 + r4;
   }
 };
@@ -1441,9 +1478,22 @@ struct Driver {
     const bool b16 = mp.p <= 65536u;  // residues fit 16 bits: half the backup traffic
     void* backup = c->backup_buffer((size_t)m * n * (b16 ? 2 : 4));
     View bk{static_cast<uint32_t*>(backup), n, m, n};
-    auto save = [&]() { b16 ? ops.copy_to16(static_cast<uint16_t*>(backup), x) : ops.copy(bk, x); };
+    // the backup copy doubles as the deferred input range check of the top node (pluq_factor)
+    const bool check = c->range_check_pending;
+    c->range_check_pending = false;
+    if (check) CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    auto save = [&]() {
+      if (b16) ops.copy_to16(static_cast<uint16_t*>(backup), x, check ? c->d_flag : nullptr);
+      else if (check) ops.backup32(static_cast<uint32_t*>(backup), x, c->d_flag);
+      else ops.copy(bk, x);
+    };
     auto restore = [&]() { b16 ? ops.copy_from16(x, static_cast<const uint16_t*>(backup)) : ops.copy(x, bk); };
     save();
+    if (check) {  // nothing was modified yet
+      CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+    }
     Perm sig = ident(n);
     int g0 = 0, repairs = 0, res = 0;
     for (;;) {
@@ -2008,8 +2058,20 @@ int pluq_factor(pluq_ctx* c, uint32_t* dA, int64_t ld, int64_t m, int64_t n, int
   if (int v = validate(m, n, p)) return v;
   if (ld < n || !rank || (m && !psig) || (n && !qsig)) return kInvalid;
   return guarded(c, [&] {
-    check_residues(c, View{dA, ld, (int)m, (int)n}, (uint32_t)p);
-    factor_device(c, dA, ld, m, n, p, threshold, psig, qsig, rank, counts, false);
+    // a node that goes straight to the speculative LU validates its entries in the backup
+    // copy (one read of the matrix instead of two); every other input is checked here
+    const int thr = (int)std::min<int64_t>(threshold, INT32_MAX);
+    const bool spec_top = c->try_generic && c->check_inputs && m > 1 && n > 1 && std::min(m, n) > thr &&
+                          !(m * n <= c->small_cap && block_smem_bytes(m, n, thr) <= kMaxDynSmem);
+    c->range_check_pending = spec_top;
+    if (!spec_top) check_residues(c, View{dA, ld, (int)m, (int)n}, (uint32_t)p);
+    try {
+      factor_device(c, dA, ld, m, n, p, threshold, psig, qsig, rank, counts, false);
+    } catch (...) {
+      c->range_check_pending = false;
+      throw;
+    }
+    c->range_check_pending = false;
   });
 }
 

@@ -1194,21 +1194,39 @@ __global__ void nonzero_kernel(View x, int* flag) {
 __device__ __forceinline__ bool rows16_vec(const View& v) {
   return (v.ld % 4) == 0 && (v.n % 4) == 0 && (reinterpret_cast<uintptr_t>(v.a) & 15) == 0;
 }
-__global__ void copy_to16_kernel(uint16_t* dst, View src) {
+// With `bad`, the copy doubles as the input range check (entries >= p set *bad), so a large
+// node's validation costs no extra read of the matrix.
+__global__ void copy_to16_kernel(uint16_t* dst, View src, uint32_t p, int* bad) {
+  bool b = false;
   if (rows16_vec(src)) {
     const int64_t nq = src.n / 4, total = (int64_t)src.m * nq;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
       const int64_t i = t / nq, q = t - i * nq;
       const uint4 v = reinterpret_cast<const uint4*>(src.a + i * src.ld)[q];
+      b |= (v.x >= p) | (v.y >= p) | (v.z >= p) | (v.w >= p);
       reinterpret_cast<uint2*>(dst + i * src.n)[q] = make_uint2(v.x | (v.y << 16), v.z | (v.w << 16));
     }
-    return;
+  } else {
+    const int64_t total = (int64_t)src.m * src.n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = t / src.n, j = t - i * src.n;
+      const uint32_t v = src.a[i * src.ld + j];
+      b |= v >= p;
+      dst[t] = (uint16_t)v;
+    }
   }
+  if (bad && __syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+__global__ void backup32_kernel(uint32_t* dst, View src, uint32_t p, int* bad) {
+  bool b = false;
   const int64_t total = (int64_t)src.m * src.n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / src.n, j = t - i * src.n;
-    dst[t] = (uint16_t)src.a[i * src.ld + j];
+    const uint32_t v = src.a[i * src.ld + j];
+    b |= v >= p;
+    dst[t] = v;
   }
+  if (bad && __syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 __global__ void copy_from16_kernel(View dst, const uint16_t* src) {
   if (rows16_vec(dst)) {

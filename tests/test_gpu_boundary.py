@@ -35,22 +35,29 @@ def test_device_densematrix_rejects_noncanonical(pb, bad):
         pb.DenseMatrix(pb.PrimeField(65521), t)
 
 
-def test_c_abi_factor_rejects_and_leaves_input(pb):
+@pytest.mark.parametrize("m,n,p,where", [(256, 256, 65521, (200, 3)), (1000, 1200, 65521, (999, 1199)),
+                                         (700, 500, 8388593, (0, 0)), (100, 40, 65521, (50, 39))])
+def test_c_abi_factor_rejects_and_leaves_input(pb, m, n, p, where):
+    """Non-canonical entries: PLUQ_EINVAL with the input untouched, whether the check runs
+    before the factorization or inside the top node's backup copy (large nodes)."""
     import torch
     from paper_1301_4438_b200 import _native
 
-    p = 65521
-    t = torch.randint(0, p, (256, 256), dtype=torch.int32, device="cuda")
-    t[200, 3] = p + 5
+    t = torch.randint(0, p, (m, n), dtype=torch.int32, device="cuda")
+    t[where] = p + 5
     before = t.clone()
     ctx = _native.context()
-    psig = np.zeros(256, np.int64)
-    qsig = np.zeros(256, np.int64)
+    psig = np.zeros(m, np.int64)
+    qsig = np.zeros(n, np.int64)
     rank = np.zeros(1, np.int64)
-    st = ctx.lib.pluq_factor(ctx.handle, t.data_ptr(), 256, 256, 256, p, 30, _native.i64p(psig),
+    st = ctx.lib.pluq_factor(ctx.handle, t.data_ptr(), n, m, n, p, 30, _native.i64p(psig),
                              _native.i64p(qsig), _native.i64p(rank), None)
     assert st == _native.PLUQ_EINVAL
     assert torch.equal(t, before)
+    t[where] = 1  # and the same matrix with a valid entry factors fine
+    st = ctx.lib.pluq_factor(ctx.handle, t.data_ptr(), n, m, n, p, 30, _native.i64p(psig),
+                             _native.i64p(qsig), _native.i64p(rank), None)
+    assert st == _native.PLUQ_OK
 
 
 @pytest.mark.parametrize("dtype,bad", [(np.float64, 0.5), (np.float64, float("nan")), (np.float64, -3.0),
