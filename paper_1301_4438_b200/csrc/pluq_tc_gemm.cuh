@@ -184,10 +184,15 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
   static_assert(!MNB || BN == 128, "MN-major B needs one 128-byte swizzle atom per tile");
   constexpr int NPOS = 2 * L - 1;
   // MNB (L = 2): the two B limb tiles sit side by side along N in shared memory, so each
-  // A limb multiplies [B_lo | B_hi] in ONE N = 256 MMA: X = A_lo [B_lo|B_hi], Y = A_hi
-  // [B_lo|B_hi], and the limb positions are X0, X1 + Y0, Y1 (2 MMAs per K step, not 4).
+  // A limb multiplies [B_lo | B_hi] in ONE N = 256 MMA (2 MMAs per K step, not 4).  The
+  // A_hi MMA is aimed one position to the right of the A_lo one, so the two middle products
+  // A_lo B_hi and A_hi B_lo accumulate into the SAME TMEM columns: the set is
+  // [P0 | P1 | P2] = [A_lo B_lo | A_lo B_hi + A_hi B_lo | A_hi B_hi], 3 x 128 columns (P1 <
+  // K * 2 * 255^2 < 2^31 is the one-pass bound k_pass already enforces).  Only the tile's
+  // first K step differs (P2 must start from zero while P1 accumulates): A_hi [B_lo|B_hi]
+  // initialises [P1 | P2], then A_lo B_lo initialises P0 and A_lo B_hi adds into P1.
   constexpr bool CAT = MNB && L == 2;
-  constexpr int ACC_COLS = CAT ? 4 * BN : NPOS * BN;  // one accumulator set
+  constexpr int ACC_COLS = NPOS * BN;  // one accumulator set
   constexpr uint32_t TCOLS = 512;
   static_assert(NBUF * ACC_COLS <= 512, "the accumulator sets must fit in TMEM");
   constexpr uint32_t A_TILE = TC_BM * TC_BK, B_TILE = BN * TC_BK;
@@ -268,14 +273,25 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
         const uint32_t a0 = smem_u32(sA + (size_t)s * L * A_TILE);
         const uint32_t b0 = smem_u32(sB + (size_t)s * L * B_TILE);
         if constexpr (CAT) {
+          // the A_lo MMAs of the stage first, then the A_hi ones: an MMA whose columns only
+          // partly overlap the previous one's (offset by one position) waits for it, so the
+          // stage has two such switches instead of eight (tools/gemm_dbg.py)
 #pragma unroll
           for (int kk = 0; kk < TC_BK / 32; ++kk) {
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
             const uint64_t bd = desc_mn_sw128(b0 + kk * 32 * 128, B_TILE);
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-              mma_i8(dacc + (uint32_t)(i * 2 * BN), desc_k_sw128(a0 + i * A_TILE + kk * 32), bd, idesc_cat, acc);
+            const uint64_t alo = desc_k_sw128(a0 + kk * 32);
+            if (kb == 0 && kk == 0) {
+              mma_i8(dacc + (uint32_t)BN, desc_k_sw128(a0 + A_TILE), bd, idesc_cat, 0u);  // [P1|P2] = A_hi [B_lo|B_hi]
+              mma_i8(dacc, alo, bd, idesc, 0u);                                          //  P0     = A_lo B_lo
+              mma_i8(dacc + (uint32_t)BN, alo, desc_mn_sw128(b0 + B_TILE, B_TILE), idesc, 1u);  // P1 += A_lo B_hi
+            } else {
+              mma_i8(dacc, alo, bd, idesc_cat, 1u);  // [P0 | P1] += A_lo [B_lo | B_hi]
+            }
           }
+#pragma unroll
+          for (int kk = (kb == 0 ? 1 : 0); kk < TC_BK / 32; ++kk)  // [P1 | P2] += A_hi [B_lo | B_hi]
+            mma_i8(dacc + (uint32_t)BN, desc_k_sw128(a0 + A_TILE + kk * 32),
+                   desc_mn_sw128(b0 + kk * 32 * 128, B_TILE), idesc_cat, 1u);
           mma_commit(&empty[s]);
           continue;
         }
@@ -316,20 +332,9 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
     // limb positions of one 16-column chunk -> 16 reduced values of this thread's row
     auto combine = [&](uint32_t lane_base, int cc, uint32_t (&v)[TC_CW]) {
       uint32_t acc[NPOS][TC_CW];
-      if constexpr (CAT) {  // X0 | X1 | Y0 | Y1  ->  positions X0, X1 + Y0, Y1
-        uint32_t y0[TC_CW];
-        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)cc, acc[0]);
-        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(BN + cc), acc[1]);
-        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(2 * BN + cc), y0);
-        tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(3 * BN + cc), acc[2]);
-        tmem_ld_wait();
 #pragma unroll
-        for (int t = 0; t < TC_CW; ++t) acc[1][t] += y0[t];
-      } else {
-#pragma unroll
-        for (int s = 0; s < NPOS; ++s) tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(s * BN + cc), acc[s]);
-        tmem_ld_wait();
-      }
+      for (int s = 0; s < NPOS; ++s) tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(s * BN + cc), acc[s]);
+      tmem_ld_wait();
 #pragma unroll
       for (int t = 0; t < TC_CW; ++t) {
         if (NPOS <= 5) {
@@ -392,7 +397,36 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
         continue;
       }
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
-      if constexpr (NBUF == 1 && NCH <= 4) {
+      if constexpr (CAT && NBUF == 1 && NCH <= 4) {
+        // two limbs, single accumulator set: the critical section (TMEM busy, tensor pipe
+        // idle) holds only the drain and the exact 48-bit recombination, two IMAD.WIDE per
+        // value: x = P0 + 2^8 P1 + 2^16 P2 < 2^31 (1 + 2^8 + 2^16).  TMEM is released
+        // before the Barrett reductions and the C read-modify-write.
+        uint64_t xv[NCH][TC_CW];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t p0[TC_CW], p1[TC_CW], p2[TC_CW];
+          const uint32_t cc = (uint32_t)(h * HALF + ch * TC_CW);
+          tmem_ld_cw<TC_CW>(lane_base + cc, p0);
+          tmem_ld_cw<TC_CW>(lane_base + (uint32_t)BN + cc, p1);
+          tmem_ld_cw<TC_CW>(lane_base + (uint32_t)(2 * BN) + cc, p2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < TC_CW; ++t)
+            xv[ch][t] = (uint64_t)p0[t] + (uint64_t)p1[t] * 256u + (uint64_t)p2[t] * 65536u;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (dbg & 4) continue;  // diagnostics: no C read-modify-write
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+          uint32_t v[TC_CW];
+#pragma unroll
+          for (int t = 0; t < TC_CW; ++t) v[t] = reduce64(xv[ch][t], mp);
+          apply(m0, n0, h * HALF + ch * TC_CW, v);
+        }
+      } else if constexpr (NBUF == 1 && NCH <= 4) {
         // single accumulator set: drain TMEM into registers first and release it, so the
         // next tile's MMAs overlap this tile's C read-modify-write
         uint32_t v[NCH][TC_CW];
