@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpluq_b200.so")
 SOURCES = ["pluq_driver.cu"]
 HEADERS = ["pluq_common.cuh", "pluq_basecase.cuh", "pluq_small.cuh", "pluq_rpm.cuh", "pluq_kernels.cuh",
-           "pluq_tc_gemm.cuh", "pluq_diag.cuh"]
+           "pluq_tc_gemm.cuh", "pluq_diag.cuh", "pluq_diag2.cuh"]
 
 
 def nvcc_path() -> str:

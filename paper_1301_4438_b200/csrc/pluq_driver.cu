@@ -180,11 +180,15 @@ struct pluq_ctx {
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
-  int64_t diag_lazy = 3;           // speculative LU diagonal block: 3 = register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
+  int64_t diag_lazy = 4;           // speculative LU diagonal block: 4 = run-ahead register kernel (pluq_diag2.cuh; full 128-blocks, 512 <= p < 2^16, else 3), 3 = lock-step register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
   int64_t la_pair = 1;             // ... and panel P's far update merges into P+1's (one K = 2W GEMM)
   int64_t inner_la = 1;            // speculative LU: look-ahead between the 128-wide blocks of a panel
+  int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
+  int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t la_pair_big = 2;        // la_pair for nodes factored with >= 2048-wide panels
+  int64_t la_reserve_big = 40;    // la_reserve for those nodes
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
   int64_t host_chunks = 24;        // pipeline depth of the host-buffer batched path
   int64_t chunk_shape = 1;         // host-buffer chunks: 0 = equal, 1 = tent (small first and last)
@@ -585,6 +589,26 @@ struct Ops {
     both.insert(both.end(), dst.begin(), dst.end());
     void* h = c->stage(both.data(), both.size() * 4);
     CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    // single in-place pass when a row's moved span fits shared memory and is dense enough
+    // that staging the whole span costs no more HBM sectors than the scattered reads
+    const int lo = dst.front(), span = dst.back() + 1 - lo;
+    const size_t pitch = ((size_t)span + 3) / 4 * 4 + 8;
+    if (c->gather_inplace && (int64_t)nmv * 8 >= span && pitch * 4 <= (size_t)220 * 1024) {
+      const int nbuf = 2 * pitch * 4 <= (size_t)220 * 1024 ? 2 : 1;
+      const size_t sm = nbuf * pitch * 4;
+      static size_t sm_set = 0;
+      if (sm > sm_set) {
+        CU(cudaFuncSetAttribute(cols_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        sm_set = (size_t)220 * 1024;
+      }
+      const int threads = span >= 8192 ? 1024 : span >= 2048 ? 512 : 256;
+      const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2048 / threads, (size_t)220 * 1024 / (sm + 1024)));
+      const int grid1 = std::min(x.m, c->tc.num_sms() * per_sm);
+      cols_inplace_kernel<<<grid1, threads, sm, c->stream>>>(x, d_idx, d_idx + nmv, nmv, lo, span, nbuf);
+      c->check_launch();
+      c->dfree(d_idx);
+      return;
+    }
     uint32_t* tmp = c->dalloc<uint32_t>((size_t)nmv * x.m);
     dim3 grid((nmv + 255) / 256, grid_rows(x.m));
     cols_to_tmp_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx, nmv, tmp);
@@ -1138,18 +1162,26 @@ struct Driver {
     const int64_t panel = (c->spec_panel_big > 0 && panel_elems >= c->spec_big_elems) ? c->spec_panel_big
                                                                                        : c->spec_panel;
     const int W = std::max(BS, (int)(panel / BS) * BS);
+    // wide-panel nodes (cfg5): group look-ahead with more SMs left to the two hidden panels
+    const bool bigw = W >= 2048;
+    const int la_pair = (int)(bigw ? c->la_pair_big : c->la_pair);
+    const int la_reserve = (int)(bigw ? c->la_reserve_big : c->la_reserve);
     CU(cudaMemsetAsync(c->d_stop, 0, 4 * sizeof(int), c->stream));
     Ops sops = ops;
     sops.stop = c->d_stop;
     const uint16_t* itab = c->invtab(mp.p);
-    const bool reg = c->diag_lazy == 3 && BS <= 128 && (itab != nullptr || mp.kchunk >= 130);
+    const bool reg = c->diag_lazy >= 3 && BS <= 128 && (itab != nullptr || mp.kchunk >= 130);
+    // run-ahead producer/consumer version (pluq_diag2.cuh): full aligned 128-blocks, 512 <= p < 2^16
+    const bool run = reg && c->diag_lazy == 4 && itab != nullptr && mp.p >= 512 && BS == 128 && (x.ld & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(x.a) & 15) == 0;
     const bool lazy = !reg && c->diag_lazy && BS <= 128;
-    const size_t dsm = reg    ? diag_reg_smem(itab != nullptr)
+    const size_t dsm = reg    ? std::max(diag_reg_smem(itab != nullptr), diag_run_smem(itab != nullptr))
                        : lazy ? diag_lazy_smem(itab != nullptr)
                               : diag_fast_smem(BS, itab != nullptr);
     if (reg) {
       CU(cudaFuncSetAttribute(diag_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
       CU(cudaFuncSetAttribute(diag_reg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      CU(cudaFuncSetAttribute(diag_run_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
     }
     const int lazy_rw = c->diag_lazy == 2 ? 4 : 8;  // rows per warp of diag_lazy_kernel
     if (lazy) {
@@ -1215,6 +1247,59 @@ struct Driver {
       CU(cudaEventCreateWithFlags(&ev_m3, cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&ev_i3, cudaEventDisableTiming));
     }
+    auto launch_diag = [&](int k0, int bs) {
+      if (run && bs == 128)
+        diag_run_kernel<true, true, true><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+      else if (reg && itab)
+        diag_reg_kernel<true><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+      else if (reg)
+        diag_reg_kernel<false><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+      else if (lazy && lazy_rw == 8)
+        diag_lazy_kernel<8><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+      else if (lazy)
+        diag_lazy_kernel<4><<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
+      else
+        diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
+                                                c->d_stop + 1, k0);
+      c->check_launch();
+    };
+    // Recursive panel factorization (option panel_rec): the tall panel [c0, c0 + w) is split
+    // in halves on the 128-grid — left half, U12 = L11^-1 A12, A22 -= L21 U12 with K = w1,
+    // right half — so the panel's updates are a few GEMMs with K up to W/2 instead of one
+    // K = 128 update of the rest of the panel per block (4x less traffic over the panel at
+    // W = 2048; it matters when the panel runs on the few SMs the side update leaves free).
+    // U12 of a node runs on a side stream next to the L21 solve of the left half's last block.
+    std::function<bool(int, int)> prec = [&](int c0, int w) -> bool {
+      if (w <= BS) {
+        launch_diag(c0, w);
+        CU(cudaEventRecord(ev_d, c->stream));
+        sops.trsm_u(x.sub(c0 + w, c0, m - c0 - w, w), x.sub(c0, c0, w, w));  // L21, every row below
+        const bool check = blk == 0 || (blk + 1) % c->spec_check == 0;
+        ++blk;
+        if (check) {  // abort early on non-generic input
+          CU(cudaMemcpyAsync(c->h_stop, c->d_stop, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+          c->sync();
+          if (c->h_stop[0]) { stopped_early = true; return false; }
+        }
+        return true;
+      }
+      const int nbk = (w + BS - 1) / BS, w1 = ((nbk + 1) / 2) * BS, w2 = w - w1;
+      if (!prec(c0, w1)) return false;
+      const View l11 = x.sub(c0, c0, w1, w1), a12 = x.sub(c0, c0 + w1, w1, w2);
+      if (c->par_trsm) {  // after the last diagonal block of the left half (ev_d), not its L21
+        CU(cudaStreamWaitEvent(side2, ev_d, 0));
+        Ops tops = sops;
+        tops.st = side2;
+        tops.trsm_l(l11, a12);
+        CU(cudaEventRecord(ev_t, side2));
+        CU(cudaStreamWaitEvent(c->stream, ev_t, 0));
+      } else {
+        sops.trsm_l(l11, a12);
+      }
+      sops.gemm(x.sub(c0 + w1, c0 + w1, m - c0 - w1, w2), x.sub(c0 + w1, c0, m - c0 - w1, w1), a12);
+      return prec(c0 + w1, w2);
+    };
+    const bool prec_on = c->panel_rec == 2 || (c->panel_rec == 1 && W >= 2048);
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
       const int pe = std::min(ps + W, mn);
       mark("P" + std::to_string(ps / W) + " inner", c->stream);
@@ -1223,22 +1308,12 @@ struct Driver {
       // CTAs and the rest after the side update ends (persistent CTAs never yield): cap it.
       // la_cap 1: cap it at la_reserve CTAs; 2: one CTA per tile, so it also takes the SMs
       // the side update frees when it ends
-      sops.max_ctas = !(side_pending && c->la_cap) ? 0 : c->la_cap == 2 ? -1 : std::max(1, (int)c->la_reserve);
+      sops.max_ctas = !(side_pending && c->la_cap) ? 0 : c->la_cap == 2 ? -1 : std::max(1, la_reserve);
+      if (prec_on) prec(ps, pe - ps);
       // inner right-looking LU of the panel columns [ps, pe)
-      for (int k0 = ps; k0 < pe; k0 += BS, ++blk) {
+      for (int k0 = ps; k0 < pe && !prec_on; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
-        if (reg && itab)
-          diag_reg_kernel<true><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
-        else if (reg)
-          diag_reg_kernel<false><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
-        else if (lazy && lazy_rw == 8)
-          diag_lazy_kernel<8><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
-        else if (lazy)
-          diag_lazy_kernel<4><<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
-        else
-          diag_crout_fast_kernel<<<1, 1024, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop,
-                                                              c->d_stop + 1, k0);
-        c->check_launch();
+        launch_diag(k0, bs);
         const View b11 = x.sub(k0, k0, bs, bs);
         if (ila && in_pending && !(c->par_trsm && pe - k0 - bs > 0))
           CU(cudaStreamWaitEvent(c->stream, ev_i3, 0));  // U12 below runs on this stream
@@ -1290,7 +1365,7 @@ struct Driver {
       if (stopped_early) break;
       // outer step: U rows [ps, pe) right of the panel, then the K = W trailing update
       const View l11 = x.sub(ps, ps, pe - ps, pe - ps);
-      if (la && c->la_pair == 2) {
+      if (la && la_pair == 2) {
         // Group look-ahead: panels P, P+1 form a group.  P's outer step touches only P+1's
         // columns (it does NOT wait for the previous group's far update, which keeps running
         // under P's and P+1's factorizations); P+1's outer step waits for it, finishes the
@@ -1332,7 +1407,7 @@ struct Driver {
           Ops aops = ops;
           aops.st = side;
           aops.stop = snap + pidx;
-          aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
+          aops.max_ctas = std::max(1, c->tc.num_sms() - la_reserve);
           aops.gemm(x.sub(pe, nn, m - pe, n - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n - nn));
           CU(cudaEventRecord(ev_side, side));
           mark("P" + std::to_string(pidx) + " side_end", side);
@@ -1351,7 +1426,7 @@ struct Driver {
       const int ne = std::min(pe + W, n);
       const int gs = defer_ps >= 0 ? defer_ps : ps;  // K range [gs, pe): this panel, or the pair
       mark("P" + std::to_string(ps / W) + " outer", c->stream);
-      const bool defer_main = c->la_pair == 3 && defer_ps < 0 && ne < mn && ne + W < n;
+      const bool defer_main = la_pair == 3 && defer_ps < 0 && ne < mn && ne + W < n;
       if (la && pe < mn && ne < n && defer_main) {
         // la_pair 3: the deferring panel's remaining work (U rows right of the next panel, the
         // next panel's rows) on this stream, so the next panel factors on an idle GPU
@@ -1373,9 +1448,9 @@ struct Driver {
         Ops aops = ops;
         aops.st = side;
         aops.stop = snap + pidx;
-        aops.max_ctas = std::max(1, c->tc.num_sms() - (int)c->la_reserve);
+        aops.max_ctas = std::max(1, c->tc.num_sms() - la_reserve);
         aops.trsm_l(l11, x.sub(ps, ne, pe - ps, n - ne));
-        const bool defer = c->la_pair == 1 && defer_ps < 0 && ne < mn && ne + W < n;
+        const bool defer = la_pair == 1 && defer_ps < 0 && ne < mn && ne + W < n;
         if (defer) {  // only the next panel's rows now; the rest merges into its update
           aops.gemm(x.sub(pe, ne, ne - pe, n - ne), x.sub(pe, ps, ne - pe, pe - ps), x.sub(ps, ne, pe - ps, n - ne));
           deferred[pidx] = 1;
@@ -1445,11 +1520,35 @@ struct Driver {
         ops.trsm_l(l0, x.sub(ps - W, pe, W, n - pe));
         ops.gemm(x.sub(ps, pe, m - ps, n - pe), x.sub(ps, ps - W, m - ps, W), x.sub(ps - W, pe, W, n - pe));
       }
-      if (t > 0) {
+      if (t > 0 && prec_on) {
+        // recursive panel: the block's own columns only; the panel columns right of it follow
+        const View b11 = x.sub(k0, k0, t, t);
+        ops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, t), b11);
+        ops.gemm(x.sub(g, g, m - g, k0 + bs - g), x.sub(g, k0, m - g, t), x.sub(k0, g, t, k0 + bs - g));
+      } else if (t > 0) {
         const View b11 = x.sub(k0, k0, t, t);
         ops.trsm_u(x.sub(k0 + bs, k0, m - k0 - bs, t), b11);
         ops.trsm_l(b11, x.sub(k0, k0 + bs, t, pe - k0 - bs));
         ops.gemm(x.sub(g, g, m - g, pe - g), x.sub(g, k0, m - g, t), x.sub(k0, g, t, pe - g));
+      }
+      if (prec_on) {
+        // every node of the panel recursion whose LEFT half holds block k0 was skipped under the
+        // stop flag: its right half [c0 + w1, c0 + w) has the pivots < c0 only; apply [c0, g)
+        int c0 = ps, w = pe - ps;
+        while (w > BS) {
+          const int nbk = (w + BS - 1) / BS, w1 = ((nbk + 1) / 2) * BS, w2 = w - w1;
+          if (k0 < c0 + w1) {
+            if (g > c0) {
+              const View u12 = x.sub(c0, c0 + w1, g - c0, w2);
+              ops.trsm_l(x.sub(c0, c0, g - c0, g - c0), u12);
+              ops.gemm(x.sub(g, c0 + w1, m - g, w2), x.sub(g, c0, m - g, g - c0), u12);
+            }
+            w = w1;
+          } else {
+            c0 += w1;
+            w = w2;
+          }
+        }
       }
       if (g > ps) {
         ops.trsm_l(x.sub(ps, ps, g - ps, g - ps), x.sub(ps, pe, g - ps, n - pe));
@@ -1898,7 +1997,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

@@ -3,6 +3,7 @@
 #include "pluq_small.cuh"
 #include "pluq_rpm.cuh"
 #include "pluq_diag.cuh"
+#include "pluq_diag2.cuh"
 
 namespace pluq {
 
@@ -1151,6 +1152,57 @@ __global__ void tmp_to_cols_kernel(View x, const int* dst, int nmv, const uint32
     uint32_t* xr = x.row(i);
     const uint32_t* tr = tmp + (int64_t)i * nmv;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nmv; q += gridDim.x * blockDim.x) xr[dst[q]] = tr[q];
+  }
+}
+
+// Column gather in ONE pass, in place: the moved set of a column permutation is closed, so a
+// row's moved entries all lie in the column span [lo, lo + span).  Each CTA stages that span
+// of a row in shared memory (cp.async, 16-byte chunks where the row is aligned; the next row
+// is prefetched into the other buffer when two fit) and writes X[i, dst[q]] <- row[src[q]]
+// back over it: HBM traffic is one read and one write of the span instead of the two
+// scattered passes through a temporary (cols_to_tmp / tmp_to_cols).
+__global__ void __launch_bounds__(1024, 1) cols_inplace_kernel(View x, const int* __restrict__ src,
+                                                               const int* __restrict__ dst, int nmv, int lo,
+                                                               int span, int nbuf) {
+  extern __shared__ __align__(16) uint32_t s_rows[];
+  // buffers are padded so that a row's 16-byte-aligned global chunks land 16-byte aligned
+  const int pitch = (span + 3) / 4 * 4 + 8;
+  auto stage = [&](int i, int b) {
+    const uint32_t* g = x.row(i) + lo;
+    const int mis = (int)((reinterpret_cast<uintptr_t>(g) >> 2) & 3);  // words past a 16-byte boundary
+    uint32_t* s = s_rows + (size_t)b * pitch + mis;                    // same misalignment in shared memory
+    const int head = min(span, (4 - mis) & 3);
+    const int body = (span - head) / 4;
+    for (int j = threadIdx.x; j < body; j += blockDim.x) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(s + head + 4 * j);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g + head + 4 * j));
+    }
+    const int tail0 = head + 4 * body;
+    for (int j = threadIdx.x; j < head + (span - tail0); j += blockDim.x) {
+      const int e = j < head ? j : tail0 + (j - head);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(s + e);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g + e));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int i = blockIdx.x, b = 0;
+  if (i < x.m) stage(i, 0);
+  for (; i < x.m; i += gridDim.x) {
+    const int nx = i + gridDim.x;
+    if (nbuf == 2 && nx < x.m) {
+      stage(nx, b ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    uint32_t* g = x.row(i);
+    const int mis = (int)((reinterpret_cast<uintptr_t>(g + lo) >> 2) & 3);
+    const uint32_t* s = s_rows + (size_t)b * pitch + mis - lo;
+    for (int q = threadIdx.x; q < nmv; q += blockDim.x) g[dst[q]] = s[src[q]];
+    __syncthreads();  // the buffer is free again
+    if (nbuf == 2) b ^= 1;
+    else if (nx < x.m) stage(nx, 0);
   }
 }
 

@@ -249,3 +249,52 @@ def test_to_leu_host_and_device(pb, on_device):
         y = np.eye(m - f.rank, dtype=np.int64)
         z = np.zeros((n - f.rank, n - f.rank), np.int64)
         assert pb.check_triangular_extension(f, y, z) == (True, True)
+
+
+@pytest.mark.parametrize("inplace", [0, 1])
+@pytest.mark.parametrize("rows,cols,ld,off,kind", [
+    (300, 1000, 1000, 0, "full"),        # every column moves: one staged span per row
+    (257, 777, 1031, 3, "full"),         # odd pitch and a misaligned view: scalar head/tail chunks
+    (5000, 777, 1031, 1, "full"),        # several rows per CTA: both buffers, odd span
+    (3000, 30001, 30001, 0, "full"),     # several rows per CTA, single buffer
+    (64, 30000, 30000, 0, "full"),       # span > 100 KB: single buffer
+    (40, 60000, 60001, 1, "full"),       # span too wide for shared memory: two-pass path
+    (500, 4096, 4100, 2, "window"),      # only columns 1000..3000 move
+    (128, 5000, 5000, 0, "sparse"),      # few moved columns over a wide span: two-pass path
+    (1, 33, 33, 0, "full"), (700, 2, 2, 0, "full"),
+])
+def test_permute_cols_paths(pb, rows, cols, ld, off, kind, inplace):
+    """apply_cols through the C ABI (matrix.py:267-283 of the reference: X[:, j] <- X[:, g[j]]),
+    one-pass in-place gather vs the two-pass path through a temporary, on views with odd
+    pitches / offsets."""
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    rng = np.random.default_rng(rows * 31 + cols)
+    g = np.arange(cols)
+    if kind == "full":
+        g = rng.permutation(cols)
+    elif kind == "window":
+        g[1000:3000] = 1000 + rng.permutation(2000)
+    else:
+        idx = rng.choice(cols, 40, replace=False)
+        g[np.sort(idx)] = idx
+    buf = torch.randint(0, 65521, (rows * ld + off + 8,), dtype=torch.int32, device="cuda")
+    before = buf.clone()
+    view = buf[off:off + rows * ld].view(rows, ld)
+    want = view[:, :cols].cpu().numpy()[:, g]
+    ctx = _native.context()
+    old = ctx.get_option("gather_inplace")
+    ctx.set_option("gather_inplace", inplace)
+    try:
+        gp = (ctypes.c_int64 * cols)(*g.tolist())
+        st = ctx.lib.pluq_permute_cols(ctx.handle, buf.data_ptr() + 4 * off, ld, rows, cols, gp)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_option("gather_inplace", old)
+    assert st == 0
+    assert np.array_equal(view[:, :cols].cpu().numpy(), want)
+    # nothing outside the view's columns was touched
+    mask = torch.ones_like(buf, dtype=torch.bool)
+    mask[off:off + rows * ld].view(rows, ld)[:, :cols] = False
+    assert torch.equal(buf[mask], before[mask])

@@ -31,7 +31,7 @@ def _oracle(a0, p, thr=30):
     return P, Q, r, x.astype(np.int64), c.as_tuple()
 
 
-DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 3, "tc_mnb": 1, "par_trsm": 1, "tc_trsm": 1,
+DEFAULTS = {"sym_par": 1, "rpm_lazy": 1, "diag_lazy": 4, "tc_mnb": 1, "par_trsm": 1, "tc_trsm": 1,
             "pair_leaves": 1, "stream_fb": 4, "fb_prefix": 1, "rpm_eager": 1, "small_cap": 128 * 128}
 
 
@@ -107,7 +107,7 @@ def test_cfg4_shaped_leaves(pb, opts, thr):
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cnt
 
 
-@pytest.mark.parametrize("opts", [dict(diag_lazy=1), dict(par_trsm=0), dict(diag_lazy=1, par_trsm=0), dict(tc_trsm=0), {}])
+@pytest.mark.parametrize("opts", [dict(diag_lazy=1), dict(diag_lazy=3), dict(par_trsm=0), dict(diag_lazy=1, par_trsm=0), dict(tc_trsm=0), {}])
 @pytest.mark.parametrize("case", [("full", 400, 400, None), ("rank200", 400, 380, 200), ("rank128", 384, 384, 128),
                                   ("rank77", 300, 330, 77), ("rank129", 260, 300, 129)])
 def test_speculative_variants(pb, opts, case):

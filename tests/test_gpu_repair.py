@@ -136,10 +136,10 @@ PAIR_CASES = [
 ]
 
 
-@pytest.mark.parametrize("inner_la", [0, 1])
+@pytest.mark.parametrize("inner_la,panel_rec", [(0, 0), (1, 0), (0, 2)], ids=["rl", "rl_la", "rec"])
 @pytest.mark.parametrize("la_pair", [0, 1, 2, 3])
 @pytest.mark.parametrize("name,m,n,r,gs", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
-def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs, inner_la):
+def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs, inner_la, panel_rec):
     """Panel P's far update merged into panel P+1's (option la_pair, one K = 2W GEMM), with
     zero pivots / repairs in either panel of a pair (the finishing step applies a pending
     deferred update)."""
@@ -151,7 +151,7 @@ def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs, inner_la):
     cc = orc.Counts()
     P, Q, R, _ = orc.pluq(x, p, 30, cc)
     ctx = _native.context()
-    opts = dict(small_cap=1, spec_panel=256, la_pair=la_pair, inner_la=inner_la)
+    opts = dict(small_cap=1, spec_panel=256, la_pair=la_pair, inner_la=inner_la, panel_rec=panel_rec)
     old = {k: ctx.get_option(k) for k in opts}
     for k, v in opts.items():
         ctx.set_option(k, v)
@@ -169,9 +169,10 @@ def test_paired_far_updates_vs_oracle(pb, la_pair, name, m, n, r, gs, inner_la):
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
 
 
+@pytest.mark.parametrize("panel_rec", [0, 2])
 @pytest.mark.parametrize("la_pair", [0, 1, 2, 3])
 @pytest.mark.parametrize("W", [384, 640, 768])
-def test_panel_widths_generic_and_repaired(pb, la_pair, W):
+def test_panel_widths_generic_and_repaired(pb, la_pair, W, panel_rec):
     """Panel widths that do not divide the size (partial last panels, pairs cut short), on a
     rank-deficient X Y input with one coincidental zero minor: the speculative path must
     succeed (no fallback) and match the oracle."""
@@ -183,7 +184,7 @@ def test_panel_widths_generic_and_repaired(pb, la_pair, W):
     cc = orc.Counts()
     P, Q, R, _ = orc.pluq(x, p, 30, cc)
     ctx = _native.context()
-    opts = dict(small_cap=1, spec_panel=W, la_pair=la_pair)
+    opts = dict(small_cap=1, spec_panel=W, la_pair=la_pair, panel_rec=panel_rec)
     old = {k: ctx.get_option(k) for k in opts}
     for k, v in opts.items():
         ctx.set_option(k, v)
@@ -199,3 +200,37 @@ def test_panel_widths_generic_and_repaired(pb, la_pair, W):
     assert np.array_equal(a.data, x)
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
     assert st["speculative_fail"] == 0 and st["spec_repairs"] == 1, st
+
+
+@pytest.mark.parametrize("par_trsm", [0, 1])
+@pytest.mark.parametrize("r,gs", [(130, []), (300, []), (520, []), (777, []), (1000, []), (1024, []), (None, [(5, 1)]),
+                                  (None, [(200, 1), (640, 2)]), (None, [(895, 1)]), (None, [(1023, 1)]),
+                                  (1100, [(384, 1)])])
+def test_recursive_panel_stops(pb, r, gs, par_trsm):
+    """Recursive panel factorization (option panel_rec) on 1024-wide panels (3 levels of
+    halving): zero pivots / zero Schur complements at every depth of the recursion — the
+    finishing step applies the updates of the nodes skipped under the stop flag."""
+    from paper_1301_4438_b200 import _native
+
+    p, m, n = 65521, 1400, 1300
+    a0 = _make("rp", m, n, r, gs, p)
+    x = a0.astype(np.float64)
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(small_cap=1, spec_panel=1024, panel_rec=2, par_trsm=par_trsm, spec_check=3)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert st["speculative_ok"] >= 1 and st["speculative_fail"] == 0, st
+    assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
