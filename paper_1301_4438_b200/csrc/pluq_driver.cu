@@ -187,6 +187,7 @@ struct pluq_ctx {
   int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
   int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t la_preinv = 1;          // group look-ahead: I - L11^-1 of a panel formed right after its factorization
   int64_t la_pair_big = 2;        // la_pair for nodes factored with >= 2048-wide panels
   int64_t la_reserve_big = 40;    // la_reserve for those nodes
   int64_t la_reserve = 16;         // SMs left to the critical path while the side GEMM runs
@@ -502,6 +503,30 @@ struct Ops {
     c->st_launch += 3;
     c->dfree_on(X, s());
     return true;
+  }
+
+  // I - T^-1 of a large triangle computed ahead of its solves (group look-ahead of the
+  // speculative LU: the inverse is formed under the running side update, the solves on the
+  // critical path are then single GEMMs); nullptr when the one-pass GEMM form does not apply.
+  uint32_t* tri_im_inverse(const View& t, bool upper) {
+    const int r = t.m;
+    const int L = TcGemm::limbs(mp.p);
+    if (!c->tc_trsm_big || !c->use_tc || r < 256 || r > TcGemm::k_pass(L) || c->tc.k_pass_override > 0) return nullptr;
+    uint32_t* X = c->dalloc_on<uint32_t>((size_t)r * r, s());
+    tri_inverse(t, upper, X);
+    const View mv{X, r, r, r};
+    dim3 grid((r + 255) / 256, grid_rows(r));
+    i_minus_kernel<<<grid, 256, 0, s()>>>(mv, upper ? 1 : 0, mp, stop);  // X <- I - X
+    c->check_launch();
+    return X;
+  }
+  void trsm_l_pre(uint32_t* X, int r, const View& b) {  // B <- L^-1 B = B - (I - L^-1) B, in place
+    if (b.n == 0) return;
+    const View mv{X, r, r, r};
+    const int st = c->tc.run(b, mv, b, mp, s(), stop, max_ctas);
+    if (st != kOk) throw PluqError(st, "tensor-core TRSM failed: " + c->tc.last_error);
+    ++c->st_tc;
+    c->st_launch += 3;
   }
 
   void trsm_l(const View& l, const View& b) {
@@ -1205,7 +1230,10 @@ struct Driver {
       CU(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     }
-    bool side_pending = false;
+    bool side_pending = false, side1_pending = false;
+    cudaEvent_t ev_side1 = nullptr;
+    CU(cudaEventCreateWithFlags(&ev_side1, cudaEventDisableTiming));
+    uint32_t* xg0 = nullptr;  // I - L11^-1 of the open group's first panel
     // Paired far updates: when panel P defers, its far update (rows below panel P+1, columns
     // beyond it) is merged into panel P+1's as ONE K = 2W tensor-core GEMM (per-tile fixed
     // costs of the one-accumulator-set kernel — the TMEM drain and the MMA restart — halve
@@ -1368,22 +1396,36 @@ struct Driver {
       if (la && la_pair == 2) {
         // Group look-ahead: panels P, P+1 form a group.  P's outer step touches only P+1's
         // columns (it does NOT wait for the previous group's far update, which keeps running
-        // under P's and P+1's factorizations); P+1's outer step waits for it, finishes the
-        // group's U rows for every column right of the group, updates the NEXT group's 2W
-        // columns on this stream (K = 2W) and launches the K = 2W far update on the side.
+        // under P's and P+1's factorizations — only for its first part, P+1's columns);
+        // P+1's outer step waits for it, finishes the group's U rows for every column right of
+        // the group, updates the NEXT panel's columns on this stream (K = 2W) and launches the
+        // K = 2W far update on the side: first the columns of the panel after next, then the rest.
+        // I - L11^-1 of each panel is formed right after its factorization (under the side
+        // update), so the U-row solves on the critical path are single GEMMs.
         const int pidx = ps / W;
         const int ne1 = std::min(pe + W, n);
+        uint32_t* xcur = (c->la_preinv && pe - ps == W && pe < n) ? sops.tri_im_inverse(l11, false) : nullptr;
+        auto solve = [&](uint32_t* X, const View& l, const View& b) {
+          if (X && b.n >= c->tc_trsm_min) sops.trsm_l_pre(X, l.m, b);
+          else sops.trsm_l(l, b);
+        };
         if (gfirst < 0 && pe < mn && ne1 <= mn && ne1 < n) {  // P: first panel of a group
           mark("P" + std::to_string(pidx) + " outer", c->stream);
-          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, ne1 - pe));
+          if (side1_pending) {  // P+1's columns came from the first part of the previous far update
+            CU(cudaStreamWaitEvent(c->stream, ev_side1, 0));
+            side1_pending = false;
+          }
+          solve(xcur, l11, x.sub(ps, pe, pe - ps, ne1 - pe));
           sops.gemm(x.sub(pe, pe, m - pe, ne1 - pe), x.sub(pe, ps, m - pe, pe - ps), x.sub(ps, pe, pe - ps, ne1 - pe));
           grouped[pidx] = 1;
           gfirst = ps;
+          xg0 = xcur;
           continue;
         }
         if (side_pending) {
           CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
           side_pending = false;
+          side1_pending = false;
         }
         sops.max_ctas = 0;
         mark("P" + std::to_string(pidx) + " outer", c->stream);
@@ -1391,14 +1433,16 @@ struct Driver {
         if (gfirst >= 0 && pe < n) {  // U rows of P for every column right of the group, P's
           // contribution to P+1's rows there, then U rows of P+1
           const View l0 = x.sub(gfirst, gfirst, ps - gfirst, ps - gfirst);
-          sops.trsm_l(l0, x.sub(gfirst, pe, ps - gfirst, n - pe));
+          solve(xg0, l0, x.sub(gfirst, pe, ps - gfirst, n - pe));
           sops.gemm(x.sub(ps, pe, pe - ps, n - pe), x.sub(ps, gfirst, pe - ps, ps - gfirst),
                     x.sub(gfirst, pe, ps - gfirst, n - pe));
         }
+        if (xg0) c->dfree(xg0);
+        xg0 = nullptr;
         gfirst = -1;
-        const int nn = std::min(pe + (gs2 < ps ? 2 : 1) * W, n);  // columns updated on this stream
+        const int nn = std::min(pe + W, n);  // the next panel's columns are updated on this stream
         if (pe < mn && nn < n) {
-          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+          solve(xcur, l11, x.sub(ps, pe, pe - ps, n - pe));
           sops.gemm(x.sub(pe, pe, m - pe, nn - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, nn - pe));
           CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
           CU(cudaEventRecord(ev_main, c->stream));
@@ -1408,14 +1452,20 @@ struct Driver {
           aops.st = side;
           aops.stop = snap + pidx;
           aops.max_ctas = std::max(1, c->tc.num_sms() - la_reserve);
-          aops.gemm(x.sub(pe, nn, m - pe, n - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n - nn));
+          const int n2 = std::min(nn + W, n);  // first the columns of the panel after next
+          aops.gemm(x.sub(pe, nn, m - pe, n2 - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n2 - nn));
+          CU(cudaEventRecord(ev_side1, side));
+          side1_pending = true;
+          if (n2 < n)
+            aops.gemm(x.sub(pe, n2, m - pe, n - n2), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, n2, pe - gs2, n - n2));
           CU(cudaEventRecord(ev_side, side));
           mark("P" + std::to_string(pidx) + " side_end", side);
           side_pending = true;
         } else {
-          sops.trsm_l(l11, x.sub(ps, pe, pe - ps, n - pe));
+          solve(xcur, l11, x.sub(ps, pe, pe - ps, n - pe));
           sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, n - pe));
         }
+        if (xcur) c->dfree(xcur);
         continue;
       }
       if (side_pending) {  // rows [ps, pe) right of this panel came from the previous side update
@@ -1469,6 +1519,8 @@ struct Driver {
       }
     }
     if (side_pending) CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
+    if (xg0) c->dfree(xg0);
+    cudaEventDestroy(ev_side1);
     if (in_pending) CU(cudaStreamWaitEvent(c->stream, ev_i3, 0));
     if (ila) {
       c->dfree(isnap);
@@ -1997,7 +2049,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

@@ -189,7 +189,7 @@ def gather_panels(slab: LocalSlab, a_full, m: int, n: int, width: int, make_empt
 
 
 def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend, flags, colperm=None,
-                           lookahead: bool = True):
+                           lookahead: bool = True, prefetch: bool = True):
     """Factor the distributed panels in place.  Returns the rank r when the matrix has a
     generic rank profile (then P = Q = I), or None when it does not (panels are then
     partially updated; the caller restarts from the original on one GPU).
@@ -202,7 +202,12 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
     lookahead: the owner of panel k+1 updates that panel's columns with panel k FIRST, factors
     it, and only then updates the rest of its later panels, so the factorization of k+1 hides
     behind the other ranks' trailing updates (the HPL look-ahead); collectives keep the same
-    order on every rank."""
+    order on every rank.
+
+    prefetch (with lookahead): the broadcast of panel k+1 is started asynchronously during step
+    k — by its owner right after the look-ahead factorization, by the other ranks before their
+    own trailing update — and waited for at the start of step k+1, so the panel transfer
+    overlaps the tensor-core update instead of preceding it (NCCL runs it on its own stream)."""
     import torch.distributed as dist
 
     rank, world = _world()
@@ -213,20 +218,38 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
         c0, c1 = bounds[k]
         return _panel_verdict(backend.factor_panel(slab.panel(k)[c0:, :]), c1 - c0, colperm)
 
+    def post(k1, res):
+        """Start the broadcast of panel k1 (verdict flag + factored panel) without waiting for
+        it: the owner passes its verdict, the other ranks post the matching receives.  The
+        collectives are issued in the same order on every rank."""
+        c0n, c1n = bounds[k1]
+        own = panel_owner(k1, world)
+        flag = flags()
+        pan = flags.new_panel(m - c0n, c1n - c0n)  # contiguous broadcast buffer
+        q = None
+        if rank == own:
+            rk, generic, q = res
+            pan.copy_(slab.panel(k1)[c0n:, :])
+            flag[0], flag[1] = rk, int(generic) + 2 * int(q is not None)
+        works = []
+        if world > 1:
+            works.append(dist.broadcast(flag, src=own, async_op=True))
+            works.append(dist.broadcast(pan, src=own, async_op=True))
+        return flag, pan, q, works
+
     ahead = factor(0) if bounds and rank == panel_owner(0, world) else None
+    pending = None  # panel k's broadcast, started during step k - 1 (prefetch)
     for k, (c0, c1) in enumerate(bounds):
         owner = panel_owner(k, world)
         wk = c1 - c0
-        flag = flags()
-        pan = flags.new_panel(m - c0, wk)  # contiguous broadcast buffer
-        q = None
-        if rank == owner:
-            rk, generic, q = ahead if ahead is not None else factor(k)
+        if pending is None:
+            res = (ahead if ahead is not None else factor(k)) if rank == owner else None
             ahead = None
-            pan.copy_(slab.panel(k)[c0:, :])
-            flag[0], flag[1] = rk, int(generic) + 2 * int(q is not None)
-        if world > 1:
-            dist.broadcast(flag, src=owner)
+            pending = post(k, res)
+        flag, pan, q, works = pending
+        pending = None
+        for w in works:
+            w.wait()
         rk, generic, repaired = int(flag[0]), bool(int(flag[1]) & 1), bool(int(flag[1]) & 2)
         if not generic:
             return None
@@ -235,12 +258,17 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
             if rank == owner and c0 > 0:  # the U rows of earlier pivots in these columns move too
                 top = slab.panel(k)[:c0, :]
                 top.copy_(top[:, qt.to(top.device)])
-        if world > 1:
-            dist.broadcast(pan, src=owner)
         g = c0 + rk
         rest = slab.after(k)
+        # look-ahead + prefetch: the owner of panel k+1 brings that panel up to date first,
+        # factors it and starts its broadcast; the other ranks post the receive BEFORE their own
+        # trailing update, so the transfer of panel k+1 runs under the update with panel k
+        la_step = lookahead and rk == wk and k + 1 < len(bounds)
+        nxt = panel_owner(k + 1, world) if la_step else -1
+        if la_step and prefetch and rank != nxt:
+            pending = post(k + 1, None)
         if rest is not None and rk > 0:
-            la = lookahead and rk == wk and k + 1 < len(bounds) and rank == panel_owner(k + 1, world)
+            la = la_step and rank == nxt
             w1 = slab.w[k + 1] if la else 0
             parts = [(0, w1), (w1, rest.shape[1])] if la else [(0, rest.shape[1])]
             for i, (a0, a1) in enumerate(parts):
@@ -251,6 +279,9 @@ def distributed_generic_lu(slab: LocalSlab, m: int, n: int, width: int, backend,
                         backend.gemm_sub(rest[g:, a0:a1], pan[rk:, :rk], top)  # A22 -= L21 U12
                 if la and i == 0:
                     ahead = factor(k + 1)  # panel k+1 is up to date: factor it now
+                    if prefetch:
+                        pending = post(k + 1, ahead)
+                        ahead = None
         if rk < wk:
             # zero pivot at g: generic only if the whole Schur complement A[g:, g:] vanishes
             # (panel k's own part was checked by the exact panel factorization)
