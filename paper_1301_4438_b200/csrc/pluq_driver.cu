@@ -187,6 +187,8 @@ struct pluq_ctx {
   int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
   int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t panel_inv = 1;          // recursive panel: accumulate I - L^-1 of the panel (U12 solves as single GEMMs)
+  int64_t la_first_single = 1;    // group look-ahead: the first panel of a node is not grouped
   int64_t la_preinv = 1;          // group look-ahead: I - L11^-1 of a panel formed right after its factorization
   int64_t la_pair_big = 2;        // la_pair for nodes factored with >= 2048-wide panels
   int64_t la_reserve_big = 40;    // la_reserve for those nodes
@@ -520,13 +522,29 @@ struct Ops {
     c->check_launch();
     return X;
   }
-  void trsm_l_pre(uint32_t* X, int r, const View& b) {  // B <- L^-1 B = B - (I - L^-1) B, in place
+  void trsm_l_pre(uint32_t* X, int r, const View& b) { trsm_l_pre(View{X, r, r, r}, b); }
+  void trsm_l_pre(const View& mv, const View& b) {  // B <- L^-1 B = B - (I - L^-1) B, in place
     if (b.n == 0) return;
-    const View mv{X, r, r, r};
     const int st = c->tc.run(b, mv, b, mp, s(), stop, max_ctas);
     if (st != kOk) throw PluqError(st, "tensor-core TRSM failed: " + c->tc.last_error);
     ++c->st_tc;
     c->st_launch += 3;
+  }
+
+  // I - T^-1 of a 128 x 128 unit-lower block written into a view (pitch ld)
+  void tri128_im_lower(const View& t, const View& out) {
+    uint32_t* inv = c->dalloc_on<uint32_t>(2 * TR_BASE * TR_BASE, s());
+    trinv_lower_unit_kernel<<<2, 256, 0, s()>>>(t, inv, mp, stop);
+    c->check_launch();
+    trinv128_combine_kernel<false><<<4, 256, 0, s()>>>(t, inv, out.a, mp, stop, (int)out.ld);
+    c->check_launch();
+    c->dfree_on(inv, s());
+  }
+  void copy_on(const View& dst, const View& src) {
+    if (dst.m == 0 || dst.n == 0) return;
+    dim3 grid((dst.n + 255) / 256, grid_rows(dst.m));
+    copy_view_kernel<<<grid, 256, 0, s()>>>(dst, src);
+    c->check_launch();
   }
 
   void trsm_l(const View& l, const View& b) {
@@ -1275,6 +1293,15 @@ struct Driver {
       CU(cudaEventCreateWithFlags(&ev_m3, cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&ev_i3, cudaEventDisableTiming));
     }
+    // Panel inverse accumulated by the recursive panel factorization (option panel_inv): M = I - L^-1
+    // of the panel's unit-lower triangle, pitch W; leaves write their 128-blocks, nodes the block
+    // below them; U12 solves inside the panel and the outer U-row solves are then single GEMMs.
+    uint32_t* minv = nullptr;
+    int minv_ps = 0;
+    bool minv_side = false;
+    auto mview = [&](int r0, int c0, int mm, int nn) {
+      return View{minv + (size_t)(r0 - minv_ps) * W + (c0 - minv_ps), W, mm, nn};
+    };
     auto launch_diag = [&](int k0, int bs) {
       if (run && bs == 128)
         diag_run_kernel<true, true, true><<<1, 512, dsm, c->stream>>>(x.sub(k0, k0, bs, bs), mp, itab, c->d_stop, c->d_stop + 1, k0);
@@ -1301,6 +1328,14 @@ struct Driver {
       if (w <= BS) {
         launch_diag(c0, w);
         CU(cudaEventRecord(ev_d, c->stream));
+        if (minv) {  // I - L^-1 of the block, on the side stream next to the L21 solve
+          CU(cudaStreamWaitEvent(side2, ev_d, 0));
+          Ops tops = sops;
+          tops.st = side2;
+          tops.tri128_im_lower(x.sub(c0, c0, w, w), mview(c0, c0, w, w));
+          CU(cudaEventRecord(ev_t, side2));
+          minv_side = true;
+        }
         sops.trsm_u(x.sub(c0 + w, c0, m - c0 - w, w), x.sub(c0, c0, w, w));  // L21, every row below
         const bool check = blk == 0 || (blk + 1) % c->spec_check == 0;
         ++blk;
@@ -1314,7 +1349,15 @@ struct Driver {
       const int nbk = (w + BS - 1) / BS, w1 = ((nbk + 1) / 2) * BS, w2 = w - w1;
       if (!prec(c0, w1)) return false;
       const View l11 = x.sub(c0, c0, w1, w1), a12 = x.sub(c0, c0 + w1, w1, w2);
-      if (c->par_trsm) {  // after the last diagonal block of the left half (ev_d), not its L21
+      if (minv) {
+        // the inverse work of the side stream is ordered there (leaf inverses, node combines);
+        // U12 = A12 - (I - L11^-1) A12 as one GEMM with the left half's accumulated inverse
+        Ops tops = sops;
+        tops.st = side2;
+        tops.trsm_l_pre(mview(c0, c0, w1, w1), a12);
+        CU(cudaEventRecord(ev_t, side2));
+        CU(cudaStreamWaitEvent(c->stream, ev_t, 0));
+      } else if (c->par_trsm) {  // after the last diagonal block of the left half (ev_d), not its L21
         CU(cudaStreamWaitEvent(side2, ev_d, 0));
         Ops tops = sops;
         tops.st = side2;
@@ -1325,7 +1368,24 @@ struct Driver {
         sops.trsm_l(l11, a12);
       }
       sops.gemm(x.sub(c0 + w1, c0 + w1, m - c0 - w1, w2), x.sub(c0 + w1, c0, m - c0 - w1, w1), a12);
-      return prec(c0 + w1, w2);
+      if (!prec(c0 + w1, w2)) return false;
+      if (minv) {
+        // M = I - L^-1 of the node from its halves: M21 = Y2 B Y1 = (B - B M1) - M2 (B - B M1),
+        // B the block of L below the left half's triangle (final since the left half returned)
+        Ops tops = sops;
+        tops.st = side2;
+        const View bv = x.sub(c0 + w1, c0, w2, w1);
+        const View m21 = mview(c0 + w1, c0, w2, w1);
+        uint32_t* tmp = c->dalloc_on<uint32_t>((size_t)w2 * w1, side2);
+        const View tv{tmp, w1, w2, w1};
+        tops.copy_on(tv, bv);
+        tops.gemm(tv, bv, mview(c0, c0, w1, w1));              // T = B - B M1
+        tops.copy_on(m21, tv);
+        tops.gemm(m21, mview(c0 + w1, c0 + w1, w2, w2), tv);   // M21 = T - M2 T
+        c->dfree_on(tmp, side2);
+        CU(cudaEventRecord(ev_t, side2));
+      }
+      return true;
     };
     const bool prec_on = c->panel_rec == 2 || (c->panel_rec == 1 && W >= 2048);
     for (int ps = 0; ps < mn && !stopped_early; ps += W) {
@@ -1337,7 +1397,25 @@ struct Driver {
       // la_cap 1: cap it at la_reserve CTAs; 2: one CTA per tile, so it also takes the SMs
       // the side update frees when it ends
       sops.max_ctas = !(side_pending && c->la_cap) ? 0 : c->la_cap == 2 ? -1 : std::max(1, la_reserve);
-      if (prec_on) prec(ps, pe - ps);
+      uint32_t* panel_m = nullptr;  // I - L11^-1 of this panel when the recursion accumulated it
+      if (prec_on) {
+        minv = nullptr;
+        minv_side = false;
+        if (c->panel_inv && c->use_tc && c->tc_trsm && BS == 128 && pe - ps == W && W % 128 == 0 && W >= 256 &&
+            W <= TcGemm::k_pass(TcGemm::limbs(mp.p)) && c->tc.k_pass_override <= 0) {
+          minv = c->dalloc<uint32_t>((size_t)W * W);
+          minv_ps = ps;
+          CU(cudaMemsetAsync(minv, 0, (size_t)W * W * sizeof(uint32_t), c->stream));
+        }
+        prec(ps, pe - ps);
+        if (minv && minv_side) CU(cudaStreamWaitEvent(c->stream, ev_t, 0));
+        panel_m = minv;
+        minv = nullptr;
+        if (panel_m && (stopped_early || !(la && la_pair == 2))) {
+          c->dfree(panel_m);
+          panel_m = nullptr;
+        }
+      }
       // inner right-looking LU of the panel columns [ps, pe)
       for (int k0 = ps; k0 < pe && !prec_on; k0 += BS, ++blk) {
         const int bs = std::min(BS, pe - k0);
@@ -1404,12 +1482,14 @@ struct Driver {
         // update), so the U-row solves on the critical path are single GEMMs.
         const int pidx = ps / W;
         const int ne1 = std::min(pe + W, n);
-        uint32_t* xcur = (c->la_preinv && pe - ps == W && pe < n) ? sops.tri_im_inverse(l11, false) : nullptr;
+        uint32_t* xcur = panel_m ? panel_m : (c->la_preinv && pe - ps == W && pe < n) ? sops.tri_im_inverse(l11, false) : nullptr;
         auto solve = [&](uint32_t* X, const View& l, const View& b) {
           if (X && b.n >= c->tc_trsm_min) sops.trsm_l_pre(X, l.m, b);
           else sops.trsm_l(l, b);
         };
-        if (gfirst < 0 && pe < mn && ne1 <= mn && ne1 < n) {  // P: first panel of a group
+        // (the very first panel stays alone, option la_first_single: its K = W far update starts
+        // after ONE exposed panel factorization instead of two)
+        if (gfirst < 0 && pe < mn && ne1 <= mn && ne1 < n && !(ps == 0 && c->la_first_single)) {  // P: first panel of a group
           mark("P" + std::to_string(pidx) + " outer", c->stream);
           if (side1_pending) {  // P+1's columns came from the first part of the previous far update
             CU(cudaStreamWaitEvent(c->stream, ev_side1, 0));
@@ -2049,7 +2129,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

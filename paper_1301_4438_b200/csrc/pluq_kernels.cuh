@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(256) trinv_lower_unit_kernel(View l, uint32_t*
 // compute their 32 columns of it (2 x 64 x 32 x 64 MACs).
 template <bool kUpper>
 __global__ void __launch_bounds__(256) trinv128_combine_kernel(View t, const uint32_t* inv64, uint32_t* bp,
-                                                               ModP mp, const int* stop) {
+                                                               ModP mp, const int* stop, int ldb = 128) {
   if (stopped(stop)) return;
   __shared__ uint32_t MA[64][65], M3[64][33], T[64][33];  // MA holds B in pass 0, A in pass 1
   const int tid = threadIdx.x, c0 = 32 * blockIdx.x;  // output columns [c0, c0 + 32)
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(256) trinv128_combine_kernel(View t, const uin
         const uint32_t d = (i - r0 == cb + j) ? 1u : 0u;
         v = d >= x ? d - x : d + (mp.p - x);
       }
-      bp[i * 128 + c0 + j] = v;
+      bp[i * ldb + c0 + j] = v;
     }
     return;
   }
@@ -957,8 +957,8 @@ __global__ void __launch_bounds__(256) trinv128_combine_kernel(View t, const uin
       const int rb = kUpper ? 0 : 64;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        bp[(rb + i0) * 128 + c0 + j0 + q] = reduce64(acc[0][q], mp);
-        bp[(rb + i0 + 32) * 128 + c0 + j0 + q] = reduce64(acc[1][q], mp);
+        bp[(rb + i0) * ldb + c0 + j0 + q] = reduce64(acc[0][q], mp);
+        bp[(rb + i0 + 32) * ldb + c0 + j0 + q] = reduce64(acc[1][q], mp);
       }
     }
   }
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(256) trinv128_combine_kernel(View t, const uin
       const int i = idx >> 5, j = idx & 31;
       const uint32_t x = X[i * 64 + cc + j];
       const uint32_t d = (i == cc + j) ? 1u : 0u;
-      bp[(rb + i) * 128 + c0 + j] = d >= x ? d - x : d + (mp.p - x);
+      bp[(rb + i) * ldb + c0 + j] = d >= x ? d - x : d + (mp.p - x);
     }
   }
 }

@@ -234,3 +234,38 @@ def test_recursive_panel_stops(pb, r, gs, par_trsm):
     assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
     assert np.array_equal(a.data, x)
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+
+
+@pytest.mark.parametrize("first_single", [0, 1])
+@pytest.mark.parametrize("preinv", [0, 1])
+@pytest.mark.parametrize("name,m,n,r,gs", PAIR_CASES + [("repair_first_panel", 1300, 1300, None, [(77, 1)]),
+                                                         ("rank_in_third", 1300, 1250, 700, [])],
+                         ids=[c[0] for c in PAIR_CASES] + ["repair_first_panel", "rank_in_third"])
+def test_group_lookahead_variants(pb, name, m, n, r, gs, first_single, preinv):
+    """Group look-ahead (la_pair = 2) with the first panel grouped or alone (la_first_single) and
+    with / without the panel inverses formed ahead (la_preinv; 256-wide panels take the
+    precomputed-inverse GEMM form), far update split in two parts."""
+    from paper_1301_4438_b200 import _native
+
+    p = 65521
+    a0 = _make(name, m, n, r, gs, p)
+    x = a0.astype(np.float64)
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(small_cap=1, spec_panel=256, la_pair=2, panel_rec=2, la_first_single=first_single, la_preinv=preinv)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(np.float64))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert st["speculative_ok"] >= 1 and st["speculative_fail"] == 0
+    assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
