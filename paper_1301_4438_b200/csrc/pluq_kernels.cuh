@@ -383,7 +383,8 @@ __global__ void crout_fast_kernel(SmallArgs args) {
 // inverse before the barrier.  Static shared arrays give immediate-offset LDS.
 // kSmall (p < 2^16, with the inverse table): dot-product accumulators stay below 2^38 and
 // are reduced with two 32-bit Barrett steps; products of residues fit 32 bits.
-template <int M, int N, int NT, bool kFast, bool kSmall = false>
+// k40 (with kSmall, 512 <= p): the 5-instruction reductions of pluq_diag2.cuh (red40 / mul16).
+template <int M, int N, int NT, bool kFast, bool kSmall = false, bool k40 = false>
 __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   static_assert(M + N - 1 <= NT, "one item per thread per step");
   static_assert(!kSmall || kFast, "the small-prime path is a fast path");
@@ -399,9 +400,14 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   const uint16_t* tab = args.invtab;
   uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
   const uint32_t e32 = kSmall ? (uint32_t)((1ull << 32) % mp.p) : 0u;
-  auto mulm = [&](uint32_t a, uint32_t b) -> uint32_t { return kSmall ? reduce32(a * b, mp) : mulmod(a, b, mp); };
+  const uint32_t P40 = mp.p, NP40 = 0u - mp.p, mu40 = k40 ? (uint32_t)((1ull << 40) / mp.p) : 0u, mu32 = mp.mu32;
+  auto mulm = [&](uint32_t a, uint32_t b) -> uint32_t {
+    return k40 ? mul16(a, b, P40, NP40, mu32) : kSmall ? reduce32(a * b, mp) : mulmod(a, b, mp);
+  };
   auto red = [&](uint64_t x) -> uint32_t {
-    return kSmall ? reduce32(reduce32((uint32_t)x, mp) + (uint32_t)(x >> 32) * e32, mp) : reduce64(x, mp);
+    return k40      ? red40(x, P40, NP40, mu40)
+           : kSmall ? reduce32(reduce32((uint32_t)x, mp) + (uint32_t)(x >> 32) * e32, mp)
+                    : reduce64(x, mp);
   };
   {
     // stage the block with cp.async (4-byte copies: the odd row pitch keeps column walks
@@ -544,7 +550,8 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
 // applies, otherwise the runtime-shape kernel.
 inline bool launch_crout_fixed(const SmallArgs& a, int64_t batch, cudaStream_t st) {
   if (a.m == 64 && a.n == 64) {
-    if (a.mp.mu32 != 0 && a.invtab) crout_fixed_kernel<64, 64, 128, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    if (a.mp.mu32 != 0 && a.invtab && a.mp.p >= 512) crout_fixed_kernel<64, 64, 128, true, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    else if (a.mp.mu32 != 0 && a.invtab) crout_fixed_kernel<64, 64, 128, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else if (a.mp.kchunk >= 66) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else crout_fixed_kernel<64, 64, 128, false><<<(unsigned)batch, 128, 0, st>>>(a);
     return true;
