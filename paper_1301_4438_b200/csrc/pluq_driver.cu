@@ -179,6 +179,7 @@ struct pluq_ctx {
   int64_t tc_min_k = 32;
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
+  int64_t batch_dp = 1;            // 64x64 batch kernel: dp2a version (pluq_kernels.cuh crout_dp_kernel)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
   int64_t diag_lazy = 4;           // speculative LU diagonal block: 4 = run-ahead register kernel (pluq_diag2.cuh; full 128-blocks, 512 <= p < 2^16, else 3), 3 = lock-step register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
   int64_t lookahead = 1;           // speculative LU: trailing update of panel P overlaps panel P+1
@@ -2126,7 +2127,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(tc_k_pass, c->tc.k_pass_override) X(tc_cfg, c->tc.variant) X(tc_mnb, c->tc.mn_b)               \
   X(tc_group, c->tc.raster_group) X(tc_cpf, c->tc.c_prefetch) X(tc_grid, c->tc.grid_override)      \
   X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma) X(tc_epi, c->tc.epi_warps)  \
-  X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) \
+  X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
   X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_reserve_big, c->la_reserve_big)                             \
@@ -2332,6 +2333,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     c->reset_stats();
     if (m > 0 && n > 0) check_residues(c, View{dA, stride, (int)batch, (int)(m * n)}, (uint32_t)p);
     SmallArgs a;
+    a.batch_dp = (int)c->batch_dp;
     a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
     a.mp = ModP::make((uint32_t)p);
@@ -2788,6 +2790,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     const auto h0 = std::chrono::steady_clock::now();
     const ModP mp = ModP::make((uint32_t)p);
     SmallArgs a;
+    a.batch_dp = (int)c->batch_dp;
     a.lda = n; a.bstride = mn; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
     a.mp = mp; a.invtab = c->invtab((uint32_t)p);

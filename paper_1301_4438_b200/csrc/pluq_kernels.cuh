@@ -44,6 +44,7 @@ struct SmallArgs {
   long long spin_limit = 0;     // consumer: give up waiting after this many cycles (no hang)
   uint32_t* prefix = nullptr;   // per failure slot: [t | 64 x 65 Crout image] of the generic kernel
   int prefix_slots = 0;         // slots available in `prefix`
+  int batch_dp = 1;             // 64 x 64 generic kernel: dp2a version (512 <= p < 2^16)
   int eager = 0;                // rank-profile kernel, p < 2^16: eager (reduced) registers
   int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
   int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
@@ -546,11 +547,173 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
   }
 }
 
+// 64 x 64 generic-profile batch kernel for 512 <= p < 2^16, dp2a version of crout_fixed_kernel
+// (same schedule: one barrier per pivot, one item per thread per step, L column published
+// unscaled and scaled by its owner one step later).  Storage: the block as uint16 (row pitch
+// 66: rows are the A operand of the dot products, two consecutive k per 32-bit load) and the
+// finished U rows a second time as byte-packed pairs Up[k / 2][j] = [lo(U[2k'][j]),
+// lo(U[2k'+1][j]), hi(U[2k'][j]), hi(U[2k'+1][j])], the B operand of IDP.2A: per TWO terms one
+// LDS of each operand and two IDP.2A (low and high byte planes, 32-bit accumulators:
+// 64 terms x 65535 x 255 < 2^31) instead of four LDS and two IMAD.WIDE (IDP 2.0 vs IMAD.WIDE
+// 5.1 cycles per warp instruction, tools/micro/imad_bench.cu).
+template <int NT>
+__global__ void __launch_bounds__(NT) crout_dp_kernel(SmallArgs args) {
+  constexpr int M = 64, N = 64, MN = 64, LD = 66, LDI = 65;
+  static_assert(M + N - 1 <= NT, "one item per thread per step");
+  __shared__ __align__(16) uint16_t A[M * LD];
+  __shared__ uint32_t Up[(MN / 2) * N];
+  __shared__ uint32_t Ncol[2][M];
+  __shared__ uint32_t invs[2];
+  __shared__ int zero_at;
+  const int tid = threadIdx.x;
+  const ModP mp = args.mp;
+  const uint16_t* tab = args.invtab;
+  uint32_t* ga = args.a + (int64_t)blockIdx.x * args.bstride;
+  const uint32_t P = mp.p, NP = 0u - mp.p, mu40 = (uint32_t)((1ull << 40) / mp.p), mu32 = mp.mu32;
+  {
+    const int w = tid >> 5, ln = tid & 31;
+#pragma unroll 4
+    for (int i = w; i < M; i += NT / 32) {
+      const uint32_t v0 = ga[(int64_t)i * args.lda + ln], v1 = ga[(int64_t)i * args.lda + 32 + ln];
+      A[i * LD + ln] = (uint16_t)v0;
+      A[i * LD + 32 + ln] = (uint16_t)v1;
+    }
+  }
+  if (tid == 0) zero_at = -1;
+  __syncthreads();
+  int own_i = -1;          // L item row owned at the previous step
+  uint32_t own_num = 0;    // its unscaled numerator
+  uint32_t inv_prev = 0;
+  int t = 0;
+  for (; t < MN; ++t) {
+    const int nu = N - t;
+    const bool is_u = tid < nu;
+    const bool is_l = !is_u && tid - nu < M - t - 1;
+    const int row = is_u ? t : t + 1 + (tid - nu);
+    const int col = is_u ? t + tid : t;
+    // scale the L entry of the previous step (nobody reads A[.][t-1] during this step)
+    if (own_i >= 0) A[own_i * LD + t - 1] = (uint16_t)mul16(own_num, inv_prev, P, NP, mu32);
+    own_i = -1;
+    if (is_u || is_l) {
+      uint32_t alo = 0, ahi = 0, alo2 = 0, ahi2 = 0;
+      const uint32_t* ri = reinterpret_cast<const uint32_t*>(A + row * LD);  // pairs L[row][2k'], L[row][2k'+1]
+      const uint32_t* cj = Up + col;
+      const int kend = t - 1;        // terms k < t-1 read final values; k = t-1 is the deferred one
+      const int pend = kend >> 1;    // whole pairs
+      int kp = 0;
+#pragma unroll 4
+      for (; kp + 1 < pend; kp += 2) {
+        const uint32_t a0 = ri[kp], b0 = cj[kp * N], a1 = ri[kp + 1], b1 = cj[(kp + 1) * N];
+        alo = __dp2a_lo(a0, b0, alo);
+        ahi = __dp2a_hi(a0, b0, ahi);
+        alo2 = __dp2a_lo(a1, b1, alo2);
+        ahi2 = __dp2a_hi(a1, b1, ahi2);
+      }
+      if (kp < pend) {
+        const uint32_t a0 = ri[kp], b0 = cj[kp * N];
+        alo = __dp2a_lo(a0, b0, alo);
+        ahi = __dp2a_hi(a0, b0, ahi);
+      }
+      unsigned long long acc = (unsigned long long)(alo + alo2) + ((unsigned long long)(ahi + ahi2) << 8);
+      if (kend > 0 && (kend & 1)) acc += (uint32_t)A[row * LD + kend - 1] * (uint32_t)A[(kend - 1) * LD + col];  // odd term
+      if (t > 0) {
+        const uint32_t lt = mul16(Ncol[(t - 1) & 1][row], inv_prev, P, NP, mu32);  // L[row][t-1]
+        acc += (unsigned long long)(lt * (uint32_t)A[(t - 1) * LD + col]);
+      }
+      const uint32_t v = submod((uint32_t)A[row * LD + col], red40(acc, P, NP, mu40), mp);
+      if (is_u) {
+        A[row * LD + col] = (uint16_t)v;
+        uint8_t* ub = reinterpret_cast<uint8_t*>(Up + (t >> 1) * N + col);
+        ub[t & 1] = (uint8_t)(v & 255u);
+        ub[2 + (t & 1)] = (uint8_t)(v >> 8);
+        if (col == t) {
+          if (v == 0u) zero_at = t;
+          else invs[t & 1] = (uint32_t)tab[v];
+        }
+      } else {
+        Ncol[t & 1][row] = v;
+        own_i = row;
+        own_num = v;
+      }
+    }
+    __syncthreads();
+    if (zero_at >= 0) break;
+    inv_prev = invs[t & 1];
+  }
+  int r = MN;
+  if (zero_at >= 0) {
+    // zero pivot at t: column t's Schur values are the unscaled numerators; the
+    // previous column's owners already wrote their scaled entries in this step
+    for (int i = t + 1 + tid; i < M; i += NT) A[i * LD + t] = (uint16_t)Ncol[t & 1][i];
+    __syncthreads();
+    bool nz = false;
+    for (int j = t + tid; j < N; j += NT) nz |= A[t * LD + j] != 0;
+    const int rows = M - t - 1, cols = N - t;
+    for (int q = tid; q < rows * cols; q += NT) {
+      const int i = t + 1 + q / cols, j = t + q % cols;
+      if (j == t) { nz |= A[i * LD + j] != 0; continue; }
+      unsigned long long acc = 0;
+      for (int kk = 0; kk < t; ++kk) acc += (uint32_t)A[i * LD + kk] * (uint32_t)A[kk * LD + j];
+      nz |= submod((uint32_t)A[i * LD + j], reduce64(acc, mp), mp) != 0u;
+    }
+    if (__syncthreads_or(nz)) {
+      // not generic: the first t pivots are (k, k) and their factors are final in A; hand
+      // them to the rank-profile kernel (R_A = diag(I_t, R_S), S the Schur complement)
+      __shared__ int s_slot;
+      if (tid == 0) s_slot = args.fail_list ? atomicAdd(args.fail_count, 1) : -1;
+      __syncthreads();
+      const int slot = s_slot;
+      if (args.prefix && slot >= 0 && slot < args.prefix_slots) {
+        uint32_t* dst = args.prefix + (size_t)slot * kPrefixWords;
+        for (int idx = tid; idx < M * N; idx += NT) dst[4 + (idx >> 6) * LDI + (idx & 63)] = A[(idx >> 6) * LD + (idx & 63)];
+        if (tid == 0) dst[0] = (uint32_t)t;
+        __threadfence();
+      }
+      __syncthreads();
+      if (tid == 0) {
+        args.generic_flag[blockIdx.x] = 0;
+        if (slot >= 0) atomicExch(args.fail_list + slot, args.fail_base + blockIdx.x);  // a consumer may be waiting
+        if (args.done_count) { __threadfence(); atomicAdd(args.done_count, 1); }
+      }
+      return;
+    }
+    for (int q = tid; q < (M - t) * (N - t); q += NT) A[(t + q / (N - t)) * LD + t + q % (N - t)] = 0;
+    r = t;
+  } else if (own_i >= 0) {
+    A[own_i * LD + MN - 1] = (uint16_t)mul16(own_num, inv_prev, P, NP, mu32);  // last L column
+  }
+  __syncthreads();
+  {
+    const int w = tid >> 5, ln = tid & 31;
+    for (int i = w; i < M; i += NT / 32)
+      for (int j = ln; j < N; j += 32) ga[(int64_t)i * args.lda + j] = A[i * LD + j];
+  }
+  int* po = args.p_out + (int64_t)blockIdx.x * M;
+  int* qo = args.q_out + (int64_t)blockIdx.x * N;
+  for (int q = tid; q < M; q += NT) po[q] = q;
+  for (int q = tid; q < N; q += NT) qo[q] = q;
+  if (tid == 0) {
+    args.generic_flag[blockIdx.x] = 1;
+    args.r_out[blockIdx.x] = r;
+    if (args.done_count) atomicAdd(args.done_count, 1);
+    if (args.generic_counts) {
+      const unsigned long long* g = args.generic_counts + 4 * r;
+      unsigned long long* co = args.cnt_out + (args.cnt_accumulate ? 0 : 4 * (int64_t)blockIdx.x);
+      if (args.cnt_accumulate) {
+        atomicAdd(co + 0, g[0]); atomicAdd(co + 1, g[1]); atomicAdd(co + 2, g[2]); atomicAdd(co + 3, g[3]);
+      } else {
+        co[0] = g[0]; co[1] = g[1]; co[2] = g[2]; co[3] = g[3];
+      }
+    }
+  }
+}
+
 // Launch the generic-profile kernel for a batch: the specialised 64x64 instance when it
 // applies, otherwise the runtime-shape kernel.
 inline bool launch_crout_fixed(const SmallArgs& a, int64_t batch, cudaStream_t st) {
   if (a.m == 64 && a.n == 64) {
-    if (a.mp.mu32 != 0 && a.invtab && a.mp.p >= 512) crout_fixed_kernel<64, 64, 128, true, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
+    if (a.mp.mu32 != 0 && a.invtab && a.mp.p >= 512 && a.batch_dp) crout_dp_kernel<128><<<(unsigned)batch, 128, 0, st>>>(a);
+    else if (a.mp.mu32 != 0 && a.invtab && a.mp.p >= 512) crout_fixed_kernel<64, 64, 128, true, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else if (a.mp.mu32 != 0 && a.invtab) crout_fixed_kernel<64, 64, 128, true, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else if (a.mp.kchunk >= 66) crout_fixed_kernel<64, 64, 128, true><<<(unsigned)batch, 128, 0, st>>>(a);
     else crout_fixed_kernel<64, 64, 128, false><<<(unsigned)batch, 128, 0, st>>>(a);

@@ -10,3 +10,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:tc_m
 # 3. full capture of the diagonal-block kernel inside cfg3 (critical path of the speculative LU)
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:diag_reg -s 20 -c 1 -o gpurun_out/prof_diag_$V \
   python tools/run_one.py cfg3 4096 1 > /dev/null 2>&1
+# --- session 5 (V=v4): run-ahead diagonal kernel, in-place column gather, final GEMM ---
+# 4. diag_run_kernel inside cfg3
+#   timeout 900 ncu --set full --import-source on --clock-control none -k regex:diag_run -s 20 -c 1 -o gpurun_out/prof_diagrun_v4 python tools/run_one.py cfg3 4096 1
+# 5. GEMM at the merged far-update shape and at the K = 2048 shape (as 2.), -o prof_gemm4096_v4 / prof_gemm2048_v4
