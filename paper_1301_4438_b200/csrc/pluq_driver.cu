@@ -158,6 +158,7 @@ struct pluq_ctx {
   unsigned long long* d_counts = nullptr;  // 4 device tallies
   unsigned long long* h_counts = nullptr;
   int* d_flag = nullptr;
+  int* d_abort = nullptr;  // residue check of a batch, read back at the end of the call
   int* h_flag = nullptr;
   int* d_stop = nullptr;     // [stop, k0, t] of the speculative no-pivot path
   int* h_stop = nullptr;
@@ -2038,6 +2039,7 @@ int pluq_create(pluq_ctx** out, int device, void* stream) {
     CU(cudaMalloc((void**)&c->d_counts, 4 * sizeof(unsigned long long)));
     CU(cudaHostAlloc((void**)&c->h_counts, 4 * sizeof(unsigned long long), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_flag, sizeof(int)));
+    CU(cudaMalloc((void**)&c->d_abort, sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_flag, sizeof(int), cudaHostAllocDefault));
     CU(cudaMalloc((void**)&c->d_stop, 4 * sizeof(int)));
     CU(cudaHostAlloc((void**)&c->h_stop, 4 * sizeof(int), cudaHostAllocDefault));
@@ -2090,6 +2092,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->d_counts) cudaFree(c->d_counts);
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
+  if (c->d_abort) cudaFree(c->d_abort);
   if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->d_zflags) cudaFree(c->d_zflags);
   if (c->d_stop) cudaFree(c->d_stop);
@@ -2331,9 +2334,21 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
   if (stride < m * n) return kInvalid;
   return guarded(c, [&] {
     c->reset_stats();
-    if (m > 0 && n > 0) check_residues(c, View{dA, stride, (int)batch, (int)(m * n)}, (uint32_t)p);
+    // canonical-residue check WITHOUT a host round trip before the factorization: the check
+    // kernel sets a device flag, every kernel of the batch returns at once when it is set (the
+    // input stays untouched), and the host reads the flag once at the end of the call
+    const bool check_async = c->check_inputs && m > 0 && n > 0;
+    if (check_async) {
+      const View xv{dA, stride, (int)batch, (int)(m * n)};
+      CU(cudaMemsetAsync(c->d_abort, 0, sizeof(int), c->stream));
+      const int n4 = std::max(1, xv.n / 4);
+      dim3 rgrid((unsigned)std::min(4, (n4 + 255) / 256), (unsigned)std::min(xv.m, 4096));
+      range_check_kernel<<<rgrid, 256, 0, c->stream>>>(xv, (uint32_t)p, c->d_abort);
+      c->check_launch();
+    }
     SmallArgs a;
     a.batch_dp = (int)c->batch_dp;
+    a.abort_flag = check_async ? c->d_abort : nullptr;
     a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
     a.mp = ModP::make((uint32_t)p);
@@ -2421,6 +2436,11 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     }
     if (!d_counts) c->dfree(cnt);
     if (flags) c->dfree(flags);
+    if (check_async) {
+      CU(cudaMemcpyAsync(c->h_flag, c->d_abort, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+    }
   });
 }
 

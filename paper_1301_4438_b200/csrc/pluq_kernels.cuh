@@ -45,6 +45,7 @@ struct SmallArgs {
   uint32_t* prefix = nullptr;   // per failure slot: [t | 64 x 65 Crout image] of the generic kernel
   int prefix_slots = 0;         // slots available in `prefix`
   int batch_dp = 1;             // 64 x 64 generic kernel: dp2a version (512 <= p < 2^16)
+  const int* abort_flag = nullptr;  // batches: set by the asynchronous residue check; every kernel returns at once if set
   int eager = 0;                // rank-profile kernel, p < 2^16: eager (reduced) registers
   int sym_par = 0;              // rank-profile kernel: parallel symbolic replay (scratch in dynamic smem)
   int sym_par_off = 0;          // byte offset of that scratch behind rpm_smem_words (after the table)
@@ -55,6 +56,7 @@ __device__ void small_pluq_block(const SmallArgs& args, int blk);
 // One CTA per block (grid = batch), or - when fail_list is given - a persistent grid
 // walking the compacted list of blocks the generic kernel could not finish.
 __global__ void small_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+  if (args.abort_flag && *reinterpret_cast<const volatile int*>(args.abort_flag)) return;
   if (fail_list) {
     const int cnt = *fail_count;
     for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
@@ -295,6 +297,7 @@ __device__ __forceinline__ int rpm_next_slot(const SmallArgs& args, const int* f
 
 template <int SHAPE>
 __global__ void __launch_bounds__(512, 1) rpm_pluq_kernel(SmallArgs args, const int* fail_list, const int* fail_count) {
+  if (args.abort_flag && *reinterpret_cast<const volatile int*>(args.abort_flag)) return;
   if (args.claim) {
     for (int q = rpm_next_slot(args, fail_list, fail_count); q >= 0; q = rpm_next_slot(args, fail_list, fail_count)) {
       rpm_pluq_block<SHAPE>(args, *reinterpret_cast<const volatile int*>(fail_list + q), q);
@@ -329,6 +332,7 @@ inline size_t rpm_smem_bytes(int64_t m, int64_t n, bool table = false) {
 // written back with P = Q = I; failed blocks are left untouched in global memory and
 // flagged for small_pluq_kernel, which then runs the exact recursion on them only.
 __global__ void crout_fast_kernel(SmallArgs args) {
+  if (args.abort_flag && *reinterpret_cast<const volatile int*>(args.abort_flag)) return;
   extern __shared__ __align__(16) uint32_t smem_dyn[];
   __shared__ BcShared sh;
   const int m = args.m, n = args.n;
@@ -387,6 +391,7 @@ __global__ void crout_fast_kernel(SmallArgs args) {
 // k40 (with kSmall, 512 <= p): the 5-instruction reductions of pluq_diag2.cuh (red40 / mul16).
 template <int M, int N, int NT, bool kFast, bool kSmall = false, bool k40 = false>
 __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
+  if (args.abort_flag && *reinterpret_cast<const volatile int*>(args.abort_flag)) return;
   static_assert(M + N - 1 <= NT, "one item per thread per step");
   static_assert(!kSmall || kFast, "the small-prime path is a fast path");
   constexpr int MN = M < N ? M : N;
@@ -558,6 +563,7 @@ __global__ void __launch_bounds__(NT) crout_fixed_kernel(SmallArgs args) {
 // 5.1 cycles per warp instruction, tools/micro/imad_bench.cu).
 template <int NT>
 __global__ void __launch_bounds__(NT) crout_dp_kernel(SmallArgs args) {
+  if (args.abort_flag && *reinterpret_cast<const volatile int*>(args.abort_flag)) return;
   constexpr int M = 64, N = 64, MN = 64, LD = 66, LDI = 65;
   static_assert(M + N - 1 <= NT, "one item per thread per step");
   __shared__ __align__(16) uint16_t A[M * LD];

@@ -92,6 +92,21 @@ def test_batched_rejects_noncanonical(pb):
     h[31, 63, 63] = 1e9
     with pytest.raises(ValueError):
         pb.pluq_batched(h, 65521, 30)
+    # streaming-size batch (concurrent fallback consumers): the asynchronous check aborts every
+    # kernel of the call, the input stays untouched, and the next call is unaffected
+    big = torch.randint(0, 65521, (2048, 64, 64), dtype=torch.int32, device="cuda")
+    good = big.clone()
+    big[2047, 63, 0] = 65521
+    before = big.clone()
+    t0 = time.perf_counter()
+    with pytest.raises(ValueError):
+        pb.pluq_batched(big, 65521, 30)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 1.0
+    assert torch.equal(big, before)
+    res = pb.pluq_batched(good, 65521, 30)
+    torch.cuda.synchronize()
+    assert int(res.ranks.min()) >= 60
 
 
 def test_current_device_and_options_roundtrip(pb):
