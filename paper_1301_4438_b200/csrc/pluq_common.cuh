@@ -27,6 +27,7 @@ struct ModP {
   uint32_t mu32;     // floor((2^32 - 1) / p) when p < 2^16 (32-bit Barrett), else 0
   uint64_t mu;       // floor((2^64 - 1) / p), Barrett constant
   uint64_t kchunk;   // max number of (p-1)^2 products summable in uint64 without overflow
+  const uint32_t* itab32;  // device table of inverses for 2^16 <= p <= 2^25 (a^-1 at index a), or nullptr
 
   static ModP make(uint32_t p_) {
     ModP m;
@@ -36,6 +37,7 @@ struct ModP {
     unsigned __int128 sq = (unsigned __int128)(p_ - 1) * (p_ - 1);
     m.kchunk = sq ? (uint64_t)(((unsigned __int128)~0ull - (unsigned __int128)(p_ - 1)) / sq) : ~0ull;
     if (m.kchunk == 0) m.kchunk = 1;
+    m.itab32 = nullptr;
     return m;
   }
 };
@@ -85,6 +87,11 @@ PLUQ_HD uint32_t submod(uint32_t a, uint32_t b, const ModP m) {
 // Multiplicative inverse via extended Euclid (field.py:41-52); a != 0 mod p.
 // 32-bit arithmetic throughout: remainders are < p < 2^31 and |Bezout coefficients| <= p.
 PLUQ_HD uint32_t invmod(uint32_t a, const ModP m) {
+#ifdef __CUDA_ARCH__
+  // primes of 17..25 bits (cfg4: 23 bits): one table load (L2-resident) instead of ~40 dependent
+  // divisions on the pivot chain of every base-case / diagonal-block / TRSM kernel
+  if (m.itab32) return __ldg(m.itab32 + a);
+#endif
   uint32_t old_r = a, r = m.p;
   int32_t old_s = 1, s = 0;
   while (r) {

@@ -180,6 +180,7 @@ struct pluq_ctx {
   int64_t tc_min_k = 32;
   int64_t try_generic = 1;         // speculative no-pivot path for generic-profile blocks
   int64_t time_kernels = 0;        // batched path: time the generic and fallback kernels (adds a sync)
+  int64_t inv32 = 1;               // 32-bit inverse table in global memory for primes of 17..25 bits (ModP::itab32)
   int64_t batch_dp = 1;            // 64x64 batch kernel: dp2a version (pluq_kernels.cuh crout_dp_kernel)
   int64_t fixed_kernels = 1;       // shape-specialised generic kernels (64x64) when they apply
   int64_t diag_lazy = 4;           // speculative LU diagonal block: 4 = run-ahead register kernel (pluq_diag2.cuh; full 128-blocks, 512 <= p < 2^16, else 3), 3 = lock-step register kernel (pluq_diag.cuh), 1/2 = lazy smem-image, 0 = Crout
@@ -253,6 +254,29 @@ struct pluq_ctx {
   int64_t gcount_key[3] = {-1, -1, -1};
   size_t rpm_smem_set[3] = {0, 0, 0};        // dynamic smem already granted to rpm_pluq_kernel<shape>
   uint32_t invtab_p = 0;
+
+  // ModP with the 32-bit inverse table attached when p has 17..25 bits (option inv32)
+  uint32_t* d_invtab32 = nullptr;
+  uint32_t invtab32_p = 0;
+  size_t invtab32_cap = 0;
+  ModP modp(uint32_t p) {
+    ModP m = ModP::make(p);
+    if (!inv32 || p < 65536u || p > (1u << 25)) return m;
+    if (invtab32_p != p) {
+      if (invtab32_cap < p) {
+        if (d_invtab32) CU(cudaFree(d_invtab32));
+        d_invtab32 = nullptr;
+        CU(cudaMalloc((void**)&d_invtab32, (size_t)p * sizeof(uint32_t)));
+        invtab32_cap = p;
+      }
+      invtab32_kernel<<<148 * 8, 256, 0, stream>>>(d_invtab32, m);
+      check_launch();
+      invtab32_p = p;
+      CU(cudaStreamSynchronize(stream));  // one-time; the table may be read from other streams
+    }
+    m.itab32 = d_invtab32;
+    return m;
+  }
 
   const uint16_t* invtab(uint32_t p) {
     if (p >= 65536) return nullptr;
@@ -1045,7 +1069,7 @@ struct Driver {
   Counts host_counts{0, 0, 0, 0};
   Ops ops;
 
-  Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ModP::make(p)), threshold(thr), ops{ctx, ModP::make(p)} {}
+  Driver(pluq_ctx* ctx, uint32_t p, int thr) : c(ctx), mp(ctx->modp(p)), threshold(thr), ops{ctx, ctx->modp(p)} {}
 
   bool fits_small(int64_t m, int64_t n) const {
     return m * n <= c->small_cap && block_smem_bytes(m, n, threshold) <= kMaxDynSmem;
@@ -2093,6 +2117,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_abort) cudaFree(c->d_abort);
+  if (c->d_invtab32) cudaFree(c->d_invtab32);
   if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->d_zflags) cudaFree(c->d_zflags);
   if (c->d_stop) cudaFree(c->d_stop);
@@ -2130,7 +2155,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(tc_k_pass, c->tc.k_pass_override) X(tc_cfg, c->tc.variant) X(tc_mnb, c->tc.mn_b)               \
   X(tc_group, c->tc.raster_group) X(tc_cpf, c->tc.c_prefetch) X(tc_grid, c->tc.grid_override)      \
   X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma) X(tc_epi, c->tc.epi_warps)  \
-  X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) \
+  X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
   X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_reserve_big, c->la_reserve_big)                             \
@@ -2351,7 +2376,7 @@ int pluq_factor_batched(pluq_ctx* c, uint32_t* dA, int64_t stride, int64_t batch
     a.abort_flag = check_async ? c->d_abort : nullptr;
     a.a = dA; a.lda = n; a.bstride = stride; a.m = (int)m; a.n = (int)n;
     a.threshold = (int)std::min<int64_t>(threshold, INT32_MAX);
-    a.mp = ModP::make((uint32_t)p);
+    a.mp = c->modp((uint32_t)p);
     a.p_out = d_p; a.q_out = d_q; a.r_out = d_rank;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(d_counts);
     if (!cnt) cnt = c->dalloc<unsigned long long>(4 * (size_t)batch);
@@ -2808,7 +2833,7 @@ int pluq_factor_batched_host_f64(pluq_ctx* c, double* hA, int64_t batch, int64_t
     // widened to the caller's int64 arrays while later chunks are still in flight
     int32_t* host = c->batch_results((size_t)(batch * (m + n + 1)));
     const auto h0 = std::chrono::steady_clock::now();
-    const ModP mp = ModP::make((uint32_t)p);
+    const ModP mp = c->modp((uint32_t)p);
     SmallArgs a;
     a.batch_dp = (int)c->batch_dp;
     a.lda = n; a.bstride = mn; a.m = (int)m; a.n = (int)n;
@@ -2922,7 +2947,7 @@ int pluq_modgemm_sub(pluq_ctx* c, uint32_t* dC, int64_t ldc, const uint32_t* dA,
   if (int v = validate(m, n, p)) return v;
   if (k < 0 || k > INT32_MAX / 2) return kInvalid;
   return guarded(c, [&] {
-    Ops ops{c, ModP::make((uint32_t)p)};
+    Ops ops{c, c->modp((uint32_t)p)};
     ops.gemm(View{dC, ldc, (int)m, (int)n}, View{const_cast<uint32_t*>(dA), lda, (int)m, (int)k},
              View{const_cast<uint32_t*>(dB), ldb, (int)k, (int)n});
   });
@@ -2946,7 +2971,7 @@ int pluq_trsm_llu(pluq_ctx* c, const uint32_t* dL, int64_t ldl, uint32_t* dB, in
                   int64_t n, int64_t p) {
   if (int v = validate(r, n, p)) return v;
   return guarded(c, [&] {
-    Ops ops{c, ModP::make((uint32_t)p)};
+    Ops ops{c, c->modp((uint32_t)p)};
     ops.trsm_l(View{const_cast<uint32_t*>(dL), ldl, (int)r, (int)r}, View{dB, ldb, (int)r, (int)n});
   });
 }
@@ -2965,7 +2990,7 @@ int pluq_trsm_ru(pluq_ctx* c, uint32_t* dB, int64_t ldb, const uint32_t* dU, int
       c->sync();
       if (*c->h_flag) { zero = 1; return; }
     }
-    Ops ops{c, ModP::make((uint32_t)p)};
+    Ops ops{c, c->modp((uint32_t)p)};
     ops.trsm_u(View{dB, ldb, (int)m, (int)r}, u);
   });
   if (g != kOk) return g;

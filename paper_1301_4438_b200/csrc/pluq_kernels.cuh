@@ -1479,6 +1479,13 @@ __global__ void copy_view_kernel(View dst, View src) {
       dst.at(i, j) = src.at(i, j);
 }
 
+// 32-bit table of inverses for 2^16 <= p <= 2^25 (ModP::itab32): tab[a] = a^-1, tab[0] = 0.
+// mp must come without a table (Euclid builds it).
+__global__ void invtab32_kernel(uint32_t* tab, ModP mp) {
+  for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < mp.p; a += gridDim.x * blockDim.x)
+    tab[a] = a ? invmod(a, mp) : 0u;
+}
+
 // Table of inverses mod p (p < 2^16): tab[a] = a^-1, tab[0] = 0.
 __global__ void invtab_kernel(uint16_t* tab, ModP mp) {
   for (uint32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < mp.p; a += gridDim.x * blockDim.x)
