@@ -190,6 +190,8 @@ struct pluq_ctx {
   int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
   int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t la_prio = 0;            // speculative LU: critical path on a greatest-priority stream
+  int64_t la_free = 0;            // group look-ahead: far update as one CTA per tile on all SMs (use with la_prio)
   int64_t panel_inv = 1;          // recursive panel: accumulate I - L^-1 of the panel (U12 solves as single GEMMs)
   int64_t la_first_single = 1;    // group look-ahead: the first panel of a node is not grouped
   int64_t la_preinv = 1;          // group look-ahead: I - L11^-1 of a panel formed right after its factorization
@@ -314,9 +316,22 @@ struct pluq_ctx {
   }
 
   cudaStream_t* side_streams() {
-    if (!side[0])
-      for (auto& s : side) CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    if (!side[0]) {
+      int lo = 0, hi = 0;
+      CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi = greatest priority (numerically lowest)
+      for (int i = 0; i < 6; ++i)  // 2 and 4 carry critical-path solves of the speculative LU
+        CU(cudaStreamCreateWithPriority(&side[i], cudaStreamNonBlocking, (i == 2 || i == 4) ? hi : lo));
+    }
     return side;
+  }
+  cudaStream_t hi_stream_ = nullptr;
+  cudaStream_t hi_stream() {  // greatest-priority stream for the panel path under a running far update
+    if (!hi_stream_) {
+      int lo = 0, hi = 0;
+      CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CU(cudaStreamCreateWithPriority(&hi_stream_, cudaStreamNonBlocking, hi));
+    }
+    return hi_stream_;
   }
   cudaEvent_t* events(size_t count) {
     while (evpool.size() < count) {
@@ -1224,7 +1239,35 @@ struct Driver {
   // g = min(m, n) if there was none; otherwise g < min(m, n) with x holding exactly the
   // state after g pivots: [L11\U11, U12; L21, S], S = x[g:, g:] the Schur complement, whose
   // (0, 0) entry is 0.
+  // la_prio: the whole critical path runs on a greatest-priority stream (the far updates on
+  // default-priority side streams), so its short kernels are dispatched ahead of pending far
+  // update CTAs whenever an SM frees up.
   int spec_core(const View& x, int64_t panel_elems) {
+    if (!c->la_prio) return spec_core_impl(x, panel_elems);
+    cudaStream_t user = c->stream, hi = c->hi_stream();
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    CU(cudaEventRecord(e0, user));
+    CU(cudaStreamWaitEvent(hi, e0, 0));
+    c->stream = hi;
+    int g = 0;
+    try {
+      g = spec_core_impl(x, panel_elems);
+    } catch (...) {
+      c->stream = user;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      throw;
+    }
+    CU(cudaEventRecord(e1, hi));
+    CU(cudaStreamWaitEvent(user, e1, 0));
+    c->stream = user;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return g;
+  }
+  int spec_core_impl(const View& x, int64_t panel_elems) {
     const int m = x.m, n = x.n, mn = std::min(m, n);
     const int BS = (int)c->spec_block;
     // very large nodes amortise a wider outer panel (fewer, longer-K trailing updates)
@@ -1557,7 +1600,9 @@ struct Driver {
           Ops aops = ops;
           aops.st = side;
           aops.stop = snap + pidx;
-          aops.max_ctas = std::max(1, c->tc.num_sms() - la_reserve);
+          // la_free: one CTA per tile (not persistent) on every SM; with la_prio the panel path's
+          // kernels are dispatched ahead of the pending tiles as SMs free up
+          aops.max_ctas = c->la_free ? -1 : std::max(1, c->tc.num_sms() - la_reserve);
           const int n2 = std::min(nn + W, n);  // first the columns of the panel after next
           aops.gemm(x.sub(pe, nn, m - pe, n2 - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n2 - nn));
           CU(cudaEventRecord(ev_side1, side));
@@ -2158,7 +2203,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

@@ -398,6 +398,12 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
       }
       const uint32_t lane_base = tbase + buf * ACC_COLS + ((uint32_t)(q * 32) << 16);
       if constexpr (CAT && NBUF == 1 && NCH <= 4) {
+        // (tools/gemm_ab.py: +18 % at 16384^2 x 1024, but 2-3 % SLOWER on the power-capped far
+        // updates of cfg5, so only outputs up to 2^28 entries take it; dbg 8 / 16 force off / on)
+        const bool fast40 = mp.mu32 != 0u && mp.p >= 512u && !(dbg & 8) &&
+                            ((dbg & 16) || (long long)c.m * c.n <= (1ll << 28));
+        const uint32_t e32f = fast40 ? (uint32_t)((1ull << 32) % mp.p) : 0u;
+        const uint32_t mu40f = fast40 ? (uint32_t)((1ull << 40) / mp.p) : 0u, np40 = 0u - mp.p;
         // two limbs, single accumulator set: the critical section (TMEM busy, tensor pipe
         // idle) holds only the drain and the exact 48-bit recombination, two IMAD.WIDE per
         // value: x = P0 + 2^8 P1 + 2^16 P2 < 2^31 (1 + 2^8 + 2^16).  TMEM is released
@@ -422,8 +428,18 @@ __global__ void __launch_bounds__(TcEpi<EPI>::THREADS, 1)
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           uint32_t v[TC_CW];
+          if (fast40) {
+            // p < 2^16: fold the high word (x < 2^47: hi < 2^15) with 2^32 mod p, then the
+            // 5-instruction reduction of pluq_diag2.cuh (7 instructions instead of ~18)
 #pragma unroll
-          for (int t = 0; t < TC_CW; ++t) v[t] = reduce64(xv[ch][t], mp);
+            for (int t = 0; t < TC_CW; ++t) {
+              const uint64_t y = (uint64_t)(uint32_t)(xv[ch][t] >> 32) * e32f + (uint32_t)xv[ch][t];
+              v[t] = red40(y, mp.p, np40, mu40f);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < TC_CW; ++t) v[t] = reduce64(xv[ch][t], mp);
+          }
           apply(m0, n0, h * HALF + ch * TC_CW, v);
         }
       } else if constexpr (NBUF == 1 && NCH <= 4) {
