@@ -190,6 +190,8 @@ struct pluq_ctx {
   int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
   int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t la_adapt = 1;           // group look-ahead: SM split between far update and panels chosen per group
+  int64_t la_side_solve = 0;      // group look-ahead: U rows of the far columns solved on the side stream
   int64_t la_prio = 0;            // speculative LU: critical path on a greatest-priority stream
   int64_t la_free = 0;            // group look-ahead: far update as one CTA per tile on all SMs (use with la_prio)
   int64_t panel_inv = 1;          // recursive panel: accumulate I - L^-1 of the panel (U12 solves as single GEMMs)
@@ -1571,6 +1573,7 @@ struct Driver {
           xg0 = xcur;
           continue;
         }
+        mark("P" + std::to_string(pidx) + " inner_end", c->stream);  // before the wait for the far update
         if (side_pending) {
           CU(cudaStreamWaitEvent(c->stream, ev_side, 0));
           side_pending = false;
@@ -1579,19 +1582,29 @@ struct Driver {
         sops.max_ctas = 0;
         mark("P" + std::to_string(pidx) + " outer", c->stream);
         const int gs2 = gfirst >= 0 ? gfirst : ps;  // group start (or this panel alone)
-        if (gfirst >= 0 && pe < n) {  // U rows of P for every column right of the group, P's
-          // contribution to P+1's rows there, then U rows of P+1
-          const View l0 = x.sub(gfirst, gfirst, ps - gfirst, ps - gfirst);
-          solve(xg0, l0, x.sub(gfirst, pe, ps - gfirst, n - pe));
-          sops.gemm(x.sub(ps, pe, pe - ps, n - pe), x.sub(ps, gfirst, pe - ps, ps - gfirst),
-                    x.sub(gfirst, pe, ps - gfirst, n - pe));
-        }
-        if (xg0) c->dfree(xg0);
-        xg0 = nullptr;
+        const int gf = gfirst;
+        // U rows of the group for the columns [ca, cb): U rows of P, P's contribution to P+1's
+        // rows there, then U rows of P+1
+        auto outer_cols = [&](Ops& o, int ca, int cb) {
+          if (cb <= ca) return;
+          auto solve_o = [&](uint32_t* X, const View& l, const View& b) {
+            if (X && b.n >= c->tc_trsm_min) o.trsm_l_pre(X, l.m, b);
+            else o.trsm_l(l, b);
+          };
+          if (gf >= 0) {
+            const View l0 = x.sub(gf, gf, ps - gf, ps - gf);
+            solve_o(xg0, l0, x.sub(gf, ca, ps - gf, cb - ca));
+            o.gemm(x.sub(ps, ca, pe - ps, cb - ca), x.sub(ps, gf, pe - ps, ps - gf), x.sub(gf, ca, ps - gf, cb - ca));
+          }
+          solve_o(xcur, l11, x.sub(ps, ca, pe - ps, cb - ca));
+        };
         gfirst = -1;
         const int nn = std::min(pe + W, n);  // the next panel's columns are updated on this stream
         if (pe < mn && nn < n) {
-          solve(xcur, l11, x.sub(ps, pe, pe - ps, n - pe));
+          // critical path: only the next panel's columns; the far columns' U rows are solved on
+          // the side stream right before the far update that consumes them (option la_side_solve)
+          const bool ss = c->la_side_solve != 0;
+          outer_cols(sops, pe, ss ? nn : n);
           sops.gemm(x.sub(pe, pe, m - pe, nn - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, nn - pe));
           CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
           CU(cudaEventRecord(ev_main, c->stream));
@@ -1602,20 +1615,51 @@ struct Driver {
           aops.stop = snap + pidx;
           // la_free: one CTA per tile (not persistent) on every SM; with la_prio the panel path's
           // kernels are dispatched ahead of the pending tiles as SMs free up
-          aops.max_ctas = c->la_free ? -1 : std::max(1, c->tc.num_sms() - la_reserve);
+          // Adaptive split of the SMs (option la_adapt, 2048-wide panels): the far update with
+          // K = pe - gs2 on (SMs - r) persistent CTAs against the next group's two panel
+          // factorizations on the r SMs left.  Fits of the cfg5 traces at r = 24 / 40 / 56
+          // (profiles/r2/NOTES.md): T_far(r) = MACs / ((SMs - r) * rate) with rate = 2.55e12
+          // field-MAC/s per SM at K = 4096 (2.29e12 at K = 2048) for two-limb primes, and
+          // T_panels(r) = 7.9 ms + 483 ms*SM / r for a pair of 2048-wide panels (nearly
+          // independent of the row count: the chain is latency-bound); r minimises the larger.
+          int resv = la_reserve;
+          if (c->la_adapt && bigw && W == 2048) {
+            const int sms = c->tc.num_sms();
+            const double limbs = (double)TcGemm::limbs(mp.p);
+            const double macs = (double)(m - pe) * (double)(n - nn) * (double)(pe - gs2);
+            const double rate = (pe - gs2 >= 4096 ? 2.55e12 : 2.29e12) * 4.0 / (limbs * limbs);
+            double best = 1e30;
+            for (int r = 16; r <= 64; r += 2) {
+              const double tf = 1e3 * macs / ((sms - r) * rate), tp = 7.9 + 483.0 / r;
+              const double t = std::max(tf, tp);
+              if (t < best) { best = t; resv = r; }
+            }
+          }
+          if (trace) fprintf(stderr, "spec %dx%d: P%d far update K=%d on %d SMs (reserve %d)\n", m, n, pidx, pe - gs2, c->tc.num_sms() - resv, resv);
+          aops.max_ctas = c->la_free ? -1 : std::max(1, c->tc.num_sms() - resv);
           const int n2 = std::min(nn + W, n);  // first the columns of the panel after next
+          if (ss) outer_cols(aops, nn, n2);
           aops.gemm(x.sub(pe, nn, m - pe, n2 - nn), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, nn, pe - gs2, n2 - nn));
           CU(cudaEventRecord(ev_side1, side));
           side1_pending = true;
-          if (n2 < n)
+          if (n2 < n) {
+            if (ss) outer_cols(aops, n2, n);
             aops.gemm(x.sub(pe, n2, m - pe, n - n2), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, n2, pe - gs2, n - n2));
+          }
+          // the inverses are last used on the side stream: released there
+          if (xg0) c->dfree_on(xg0, side);
+          if (xcur) c->dfree_on(xcur, side);
+          xg0 = nullptr;
+          xcur = nullptr;
           CU(cudaEventRecord(ev_side, side));
           mark("P" + std::to_string(pidx) + " side_end", side);
           side_pending = true;
         } else {
-          solve(xcur, l11, x.sub(ps, pe, pe - ps, n - pe));
+          outer_cols(sops, pe, n);
           sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, n - pe));
         }
+        if (xg0) c->dfree(xg0);
+        xg0 = nullptr;
         if (xcur) c->dfree(xcur);
         continue;
       }
@@ -2203,7 +2247,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
