@@ -190,6 +190,8 @@ struct pluq_ctx {
   int64_t panel_rec = 1;          // speculative LU: recursive (halving) panel factorization instead of 128-block right-looking (1: panels >= 2048 wide, 2: always)
   int64_t gather_inplace = 1;     // column gathers: one in-place pass through shared memory when the span fits
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
+  int64_t spec_backup = 2;        // speculative LU: 1 = backup copy of the node, 0 = un-factor in place on failure, 2 = backup below spec_unfactor_elems entries
+  int64_t spec_unfactor_elems = 1ll << 28;
   int64_t la_adapt = 1;           // group look-ahead: SM split between far update and panels chosen per group
   int64_t la_side_solve = 0;      // group look-ahead: U rows of the far columns solved on the side stream
   int64_t la_prio = 0;            // speculative LU: critical path on a greatest-priority stream
@@ -641,6 +643,79 @@ struct Ops {
     trsm_u_rec(b.sub(0, h, b.m, r - h), u.sub(h, h, r - h, r - h), inv + (size_t)(h / TR_BASE) * TR_BASE * TR_BASE);
   }
 
+  // ---- un-factoring: partial factors back to the matrix they came from, in place -------
+  // C <- C + A B through C <- C - (-A) B (A negated in place and back).
+  void gemm_add(const View& cv, const View& av, const View& bv) {
+    if (cv.m == 0 || cv.n == 0 || av.n == 0) return;
+    negate(av);
+    gemm(cv, av, bv);
+    negate(av);
+  }
+  // X <- X U, U upper triangular (g x g), in place: [X1 X2] [Ua Ub; 0 Uc] = [X1 Ua, X1 Ub + X2 Uc].
+  void trmm_ru(const View& xv, const View& u) {
+    const int g = u.m;
+    if (g == 0 || xv.m == 0) return;
+    if (g <= TR_BASE) {
+      uint32_t* d = c->dalloc_on<uint32_t>(TR_BASE * TR_BASE, s());
+      tri_extract_kernel<<<1, 256, 0, s()>>>(u, d, 1);
+      c->check_launch();
+      trsm_apply_right_kernel<<<(xv.m + 31) / 32, 128, 0, s()>>>(xv, d, mp, stop);  // X <- X D (dense product)
+      c->check_launch();
+      c->dfree_on(d, s());
+      return;
+    }
+    const int h = split(g);
+    trmm_ru(xv.sub(0, h, xv.m, g - h), u.sub(h, h, g - h, g - h));
+    gemm_add(xv.sub(0, h, xv.m, g - h), xv.sub(0, 0, xv.m, h), u.sub(0, h, h, g - h));
+    trmm_ru(xv.sub(0, 0, xv.m, h), u.sub(0, 0, h, h));
+  }
+  // Y <- L Y, L unit lower triangular (g x g), in place: [La 0; Lb Lc] [Y1; Y2] = [La Y1; Lb Y1 + Lc Y2].
+  void trmm_ll(const View& l, const View& yv) {
+    const int g = l.m;
+    if (g == 0 || yv.n == 0) return;
+    if (g <= TR_BASE) {
+      uint32_t* d = c->dalloc_on<uint32_t>(TR_BASE * TR_BASE, s());
+      tri_extract_kernel<<<1, 256, 0, s()>>>(l, d, 0);
+      c->check_launch();
+      trsm_apply_left_kernel<<<(yv.n + 31) / 32, 128, 0, s()>>>(d, yv, mp, stop);  // Y <- D Y
+      c->check_launch();
+      c->dfree_on(d, s());
+      return;
+    }
+    const int h = split(g);
+    trmm_ll(l.sub(h, h, g - h, g - h), yv.sub(h, 0, g - h, yv.n));
+    gemm_add(yv.sub(h, 0, g - h, yv.n), l.sub(h, 0, g - h, h), yv.sub(0, 0, h, yv.n));
+    trmm_ll(l.sub(0, 0, h, h), yv.sub(0, 0, h, yv.n));
+  }
+  // X (g x g, packed L\U) <- L U in place.
+  void lu_mult(const View& xv) {
+    const int g = xv.m;
+    if (g == 0) return;
+    if (g <= TR_BASE) {
+      lu_mult_kernel<<<1, 256, 0, s()>>>(xv, mp);
+      c->check_launch();
+      return;
+    }
+    const int h = split(g);
+    const View x11 = xv.sub(0, 0, h, h), x12 = xv.sub(0, h, h, g - h), x21 = xv.sub(h, 0, g - h, h),
+               x22 = xv.sub(h, h, g - h, g - h);
+    lu_mult(x22);               // Lc Uc
+    gemm_add(x22, x21, x12);    // + Lb Ub (both still factors)
+    trmm_ll(x11, x12);          // La Ub
+    trmm_ru(x21, x11);          // Lb Ua
+    lu_mult(x11);               // La Ua
+  }
+  // x = [L11\U11, U12; L21, S] after g pivots of the unpivoted LU (S the Schur complement)
+  // back to the matrix it was computed from.
+  void unfactor(const View& xv, int g) {
+    if (g <= 0) return;
+    const int m = xv.m, n = xv.n;
+    gemm_add(xv.sub(g, g, m - g, n - g), xv.sub(g, 0, m - g, g), xv.sub(0, g, g, n - g));  // A22 = S + L21 U12
+    trmm_ll(xv.sub(0, 0, g, g), xv.sub(0, g, g, n - g));                                  // A12 = L11 U12
+    trmm_ru(xv.sub(g, 0, m - g, g), xv.sub(0, 0, g, g));                                  // A21 = L21 U11
+    lu_mult(xv.sub(0, 0, g, g));                                                         // A11 = L11 U11
+  }
+
   // ---- gathers restricted to the moved set (matrix.py:249-283) ----------------------
   void gather_rows(const View& x, const Perm& g) {
     if (x.m == 0 || x.n == 0) return;
@@ -1078,6 +1153,8 @@ static void launch_exact(pluq_ctx* c, const SmallArgs& a, unsigned grid, unsigne
   }
   c->check_launch();
 }
+
+void check_residues(pluq_ctx* c, const View& x, uint32_t p);
 
 struct Driver {
   pluq_ctx* c;
@@ -1822,28 +1899,46 @@ struct Driver {
   int speculative_lu(const View& x, int& rank, Perm& p_out, Perm& q, Counts& cnt) {
     const int m = x.m, n = x.n, mn = std::min(m, n);
     const bool b16 = mp.p <= 65536u;  // residues fit 16 bits: half the backup traffic
-    void* backup = c->backup_buffer((size_t)m * n * (b16 ? 2 : 4));
+    // spec_backup = 0: no backup copy of the node; a failed speculation is undone by
+    // re-multiplying the partial factors in place (Ops::unfactor) and undoing the repairs'
+    // column rotations.  Extra storage then stays O(panel) instead of O(m n).
+    const bool use_backup = c->spec_backup == 1 || (c->spec_backup == 2 && (int64_t)m * n < c->spec_unfactor_elems);
+    void* backup = use_backup ? c->backup_buffer((size_t)m * n * (b16 ? 2 : 4)) : nullptr;
     View bk{static_cast<uint32_t*>(backup), n, m, n};
     // the backup copy doubles as the deferred input range check of the top node (pluq_factor)
     const bool check = c->range_check_pending;
     c->range_check_pending = false;
-    if (check) CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+    if (check && use_backup) CU(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
     auto save = [&]() {
       if (b16) ops.copy_to16(static_cast<uint16_t*>(backup), x, check ? c->d_flag : nullptr);
       else if (check) ops.backup32(static_cast<uint32_t*>(backup), x, c->d_flag);
       else ops.copy(bk, x);
     };
-    auto restore = [&]() { b16 ? ops.copy_from16(x, static_cast<const uint16_t*>(backup)) : ops.copy(x, bk); };
-    save();
-    if (check) {  // nothing was modified yet
-      CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      c->sync();
-      if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
-    }
     Perm sig = ident(n);
+    int g_state = 0;  // pivots of the partial factorization currently held in x
+    auto restore = [&]() {
+      if (use_backup) {
+        b16 ? ops.copy_from16(x, static_cast<const uint16_t*>(backup)) : ops.copy(x, bk);
+        return;
+      }
+      ops.unfactor(x, g_state);
+      if (!is_ident(sig)) ops.gather_cols(x, inverse(sig));  // column k holds original column sig[k]
+      g_state = 0;
+    };
+    if (use_backup) {
+      save();
+      if (check) {  // nothing was modified yet
+        CU(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (*c->h_flag) throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
+      }
+    } else if (check) {
+      check_residues(c, x, mp.p);
+    }
     int g0 = 0, repairs = 0, res = 0;
     for (;;) {
       const int g = g0 + spec_core(x.sub(g0, g0, m - g0, n - g0), (int64_t)m * n);
+      g_state = std::min(g, mn);
       if (g >= mn) { rank = mn; res = 1; break; }
       if (!ops.nonzero(x.sub(g, g, m - g, n - g))) { rank = g; res = 1; break; }
       if (repairs >= c->spec_repairs) break;
@@ -2247,7 +2342,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \

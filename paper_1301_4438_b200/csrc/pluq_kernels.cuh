@@ -1382,6 +1382,44 @@ __global__ void __launch_bounds__(1024, 1) cols_inplace_kernel(View x, const int
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Un-factoring (Driver::unfactor): re-multiplying partial factors in place, so that a failed
+// speculative LU restores its node without a backup copy of the whole matrix.
+// ---------------------------------------------------------------------------------
+// Dense 64 x 64 copy (pitch TR_BASE) of a triangle of t (w <= 64): upper = 1 keeps i <= j,
+// upper = 0 keeps i > j and puts 1 on the diagonal (unit lower); zeros elsewhere.
+__global__ void tri_extract_kernel(View t, uint32_t* out, int upper) {
+  const int w = t.m;
+  for (int idx = threadIdx.x; idx < TR_BASE * TR_BASE; idx += blockDim.x) {
+    const int i = idx >> 6, j = idx & 63;
+    uint32_t v = 0u;
+    if (i < w && j < w) {
+      if (upper) v = i <= j ? t.at(i, j) : 0u;
+      else v = i > j ? t.at(i, j) : (i == j ? 1u : 0u);
+    }
+    out[idx] = v;
+  }
+}
+// X (w x w, w <= 64, packed unit-lower L below the diagonal and U on/above it) <- L U, one CTA.
+__global__ void __launch_bounds__(256) lu_mult_kernel(View x, ModP mp) {
+  __shared__ uint32_t S[TR_BASE][TR_BASE + 1];
+  const int w = x.m;
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) S[idx / w][idx % w] = x.at(idx / w, idx % w);
+  __syncthreads();
+  const bool fast = mp.kchunk >= TR_BASE + 1;
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    const int i = idx / w, j = idx % w, kmax = min(i, j);  // sum over k < min(i, j), then the k = min term
+    unsigned long long acc = 0;
+    for (int k = 0; k < kmax; ++k) {
+      acc += (unsigned long long)S[i][k] * S[k][j];
+      if (!fast) acc = reduce64(acc, mp);
+    }
+    // k = min(i, j): L[i][i] = 1 when i <= j, else L[i][j] U[j][j]
+    acc += i <= j ? (unsigned long long)S[i][j] : (unsigned long long)S[i][j] * S[j][j];
+    x.at(i, j) = reduce64(acc, mp);
+  }
+}
+
 // *out <- min(*out, smallest column of a nonzero in row 0 of x) (pivot repair of the
 // speculative LU: row-order elimination picks the leftmost nonzero, pluq_rpm.cuh phase a).
 __global__ void first_nonzero_kernel(View x, int* out) {

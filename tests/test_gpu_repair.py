@@ -269,3 +269,54 @@ def test_group_lookahead_variants(pb, name, m, n, r, gs, first_single, preinv):
     assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
     assert np.array_equal(a.data, x)
     assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+
+
+UNFACTOR_CASES = [
+    # name, m, n, zero rows (rows without a pivot: the speculation must fail there), coincidences, p, repairs allowed
+    ("zero_row_early", 500, 520, [3], [], 65521, 32),
+    ("zero_row_late", 500, 500, [300], [], 65521, 32),
+    ("zero_row_block_edge", 640, 600, [255], [], 65521, 32),
+    ("repair_then_zero_row", 600, 640, [350], [(100, 1)], 65521, 32),
+    ("two_repairs_then_zero_row", 700, 700, [520], [(60, 1), (300, 2)], 65521, 32),
+    ("coincidence_no_repairs", 400, 420, [], [(57, 1)], 65521, 0),
+    ("p23_zero_row", 380, 400, [200], [], 8388593, 32),
+    ("tall_zero_row", 900, 300, [150], [], 65521, 32),
+    ("wide_zero_row", 300, 900, [150], [], 65521, 32),
+]
+
+
+@pytest.mark.parametrize("name,m,n,zrows,gs,p,reps", UNFACTOR_CASES, ids=[c[0] for c in UNFACTOR_CASES])
+def test_unfactor_restores_without_backup(pb, name, m, n, zrows, gs, p, reps):
+    """spec_backup = 0: a failed speculative LU re-multiplies its partial factors in place
+    (Ops::unfactor: A22 = S + L21 U12, A12 = L11 U12, A21 = L21 U11, A11 = L11 U11) and undoes
+    the repairs' column rotations instead of copying a backup back; the exact recursion that
+    follows must then see the original matrix — bit-exact against the oracle."""
+    from paper_1301_4438_b200 import _native
+
+    rng = np.random.default_rng(m * 13 + n)
+    a0 = np.asarray(rng.integers(0, p, (m, n)), np.int64)
+    for g, w in gs:
+        _vanish(a0, g, w, p, rng)
+    for zr in zrows:  # row zr = combination of the rows above: no pivot in that row
+        coef = rng.integers(0, p, zr).astype(object)
+        a0[zr, :] = np.array((coef @ a0[:zr, :].astype(object)) % p, dtype=np.int64) if zr else 0
+    x = a0.astype(orc.field_dtype(p))
+    cc = orc.Counts()
+    P, Q, R, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(small_cap=1, spec_panel=256, spec_repairs=reps, spec_backup=0)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(orc.field_dtype(p)))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = pb.last_stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert st["speculative_fail"] >= 1, st
+    assert f.rank == R and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
