@@ -480,7 +480,7 @@ def main():
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--selftest-ranks", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -601,6 +601,7 @@ def bench_single(pb, name, args, dev, world, rank):
                                "threads convert the float64 buffer to a uint16 wire (p <= 2^16) in pinned chunks, "
                                "widened on the device; the reverse on the way back",
                        "steps": len(ts), "ms_per_step": 1e3 * sum(ts) / len(ts),
+                       "median_ms": 1e3 * sorted(ts)[len(ts) // 2],
                        "step_ms": [round(1e3 * v, 2) for v in ts]}
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline_leg()
