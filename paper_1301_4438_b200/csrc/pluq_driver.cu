@@ -2301,6 +2301,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->h_counts) cudaFreeHost(c->h_counts);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_abort) cudaFree(c->d_abort);
+  if (c->hi_stream_) cudaStreamDestroy(c->hi_stream_);
   if (c->d_invtab32) cudaFree(c->d_invtab32);
   if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->d_zflags) cudaFree(c->d_zflags);
