@@ -2339,7 +2339,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(use_tc, c->use_tc) X(tc_min_dim, c->tc_min_dim) X(tc_min_k, c->tc_min_k)                        \
   X(tc_k_pass, c->tc.k_pass_override) X(tc_cfg, c->tc.variant) X(tc_mnb, c->tc.mn_b)               \
   X(tc_group, c->tc.raster_group) X(tc_cpf, c->tc.c_prefetch) X(tc_grid, c->tc.grid_override)      \
-  X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_time, c->tc.time_mma) X(tc_epi, c->tc.epi_warps)  \
+  X(tc_dbg, c->tc.dbg) X(tc_vec, c->tc.vec_limbs) X(tc_pair, c->tc.pair_split) X(tc_time, c->tc.time_mma) X(tc_epi, c->tc.epi_warps)  \
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \

@@ -702,8 +702,7 @@ __global__ void limb_cols_kernel(View b, uint8_t* out, int L, int n_pad, int k_p
 
 // Vectorised limb split of a row-major view: 16 consecutive k per thread, one 16-byte
 // store per limb plane (k_pad is a multiple of 128, so every store is aligned).
-__global__ void limb_rows16_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad, const int* stop) {
-  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+__device__ __forceinline__ void limb_rows16_body(const View& v, uint8_t* out, int L, int rows_pad, int k_pad) {
   const int64_t plane = (int64_t)rows_pad * k_pad;
   const int kq = k_pad / 16;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rows_pad * kq;
@@ -736,6 +735,19 @@ __global__ void limb_rows16_kernel(View v, uint8_t* out, int L, int rows_pad, in
       *reinterpret_cast<uint4*>(out + l * plane + (int64_t)i * k_pad + k16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
   }
+}
+
+__global__ void limb_rows16_kernel(View v, uint8_t* out, int L, int rows_pad, int k_pad, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  limb_rows16_body(v, out, L, rows_pad, k_pad);
+}
+// Both operands of one GEMM call in ONE launch (blockIdx.y selects the operand): the small
+// GEMMs of the panel chain pay one launch latency less per call.
+__global__ void limb_rows16_pair_kernel(View va, uint8_t* outa, int rows_a, int k_a, View vb, uint8_t* outb, int rows_b,
+                                        int k_b, int L, const int* stop) {
+  if (stop && *reinterpret_cast<const volatile int*>(stop)) return;
+  if (blockIdx.y == 0) limb_rows16_body(va, outa, L, rows_a, k_a);
+  else limb_rows16_body(vb, outb, L, rows_b, k_b);
 }
 
 // ------------------------- peak microbenchmarks -------------------------
@@ -805,6 +817,7 @@ struct TcGemm {
   int grid_override = 0;        // tests/diagnostics: CTAs of the persistent kernel (option tc_grid)
   int dbg = 0;                  // diagnostics only (option tc_dbg): 1 = skip operand loads after the first ring, 2 = skip the epilogue
   int vec_limbs = 1;            // vectorised limb-split kernels (option tc_vec)
+  int pair_split = 1;           // both operands' limb split in one launch (option tc_pair)
   int time_mma = 0;             // option tc_time: time the MMA kernel alone (adds a sync)
   int mn_b = 1;                 // option tc_mnb: MN-major B operand when the tile allows it (no transpose)
   int raster_group = 8;         // option tc_group: tile rows per rasterisation group (0: row-major tiles)
@@ -908,6 +921,11 @@ struct TcGemm {
       const int k_pad = (kc + TC_BK - 1) / TC_BK * TC_BK;
       View as = a.sub(0, (int)k0, m, kc);
       View bs = b.sub((int)k0, 0, kc, n);
+      if (vec_limbs && MNB && pair_split) {  // A and B (row-major planes) in one launch
+        const int64_t wa = (int64_t)m_pad * (k_pad / 16), wb = (int64_t)k_pad * (n_pad / 16);
+        const int gx = (int)std::min<int64_t>((std::max(wa, wb) + 255) / 256, 148 * 16);
+        limb_rows16_pair_kernel<<<dim3((unsigned)gx, 2), 256, 0, st>>>(as, da, m_pad, k_pad, bs, db, k_pad, n_pad, L, stop);
+      } else {
       if (vec_limbs) {
         const int64_t work = (int64_t)m_pad * (k_pad / 16);
         const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
@@ -924,6 +942,7 @@ struct TcGemm {
       } else {
         dim3 cgrid(n_pad / 32, k_pad / 32);
         limb_cols_kernel<<<cgrid, 256, 0, st>>>(bs, db, L, n_pad, k_pad, stop);
+      }
       }
       CUtensorMap ta, tb;
       const bool okb = MNB ? make_map(&tb, db, n_pad, (int64_t)L * k_pad, TC_BK, BN)
