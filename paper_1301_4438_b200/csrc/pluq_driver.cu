@@ -729,6 +729,19 @@ struct Ops {
     both.insert(both.end(), dst.begin(), dst.end());
     void* h = c->stage(both.data(), both.size() * 4);
     CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    if (c->gather_inplace && nmv <= 1536) {  // small moved set: one in-place pass by column strips
+      const size_t sm = (size_t)nmv * 32 * sizeof(uint32_t);
+      static bool attr_set = false;
+      if (sm > 48 * 1024 && !attr_set) {
+        CU(cudaFuncSetAttribute(rows_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1536 * 32 * 4));
+        attr_set = true;
+      }
+      const int strips = (x.n + 31) / 32;
+      rows_inplace_kernel<<<std::min(strips, c->tc.num_sms() * 8), 256, sm, c->stream>>>(x, d_idx, d_idx + nmv, nmv);
+      c->check_launch();
+      c->dfree(d_idx);
+      return;
+    }
     uint32_t* tmp = c->dalloc<uint32_t>((size_t)nmv * x.n);
     dim3 grid((unsigned)std::max(1, std::min(8, (x.n / 4 + 255) / 256)), grid_rows(nmv));
     rows_to_tmp_kernel<<<grid, 256, 0, c->stream>>>(x, d_idx, nmv, tmp);

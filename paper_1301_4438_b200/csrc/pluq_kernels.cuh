@@ -1331,6 +1331,24 @@ __global__ void tmp_to_cols_kernel(View x, const int* dst, int nmv, const uint32
   }
 }
 
+// Row gather in ONE pass for small moved sets (the exact recursion's many small gathers): each
+// CTA owns strips of 32 columns, stages the moved rows' 128-byte segments in shared memory and
+// writes them back permuted — one launch, no temporary.
+__global__ void __launch_bounds__(256) rows_inplace_kernel(View x, const int* __restrict__ src,
+                                                           const int* __restrict__ dst, int nmv) {
+  extern __shared__ __align__(16) uint32_t s_seg[];  // [nmv][32]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c0 = blockIdx.x * 32; c0 < x.n; c0 += gridDim.x * 32) {
+    const int col = c0 + lane;
+    if (col < x.n)
+      for (int q = w; q < nmv; q += 8) s_seg[q * 32 + lane] = x.at(src[q], col);
+    __syncthreads();
+    if (col < x.n)
+      for (int q = w; q < nmv; q += 8) x.at(dst[q], col) = s_seg[q * 32 + lane];
+    __syncthreads();
+  }
+}
+
 // Column gather in ONE pass, in place: the moved set of a column permutation is closed, so a
 // row's moved entries all lie in the column span [lo, lo + span).  Each CTA stages that span
 // of a row in shared memory (cp.async, 16-byte chunks where the row is aligned; the next row

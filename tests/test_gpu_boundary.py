@@ -313,3 +313,37 @@ def test_permute_cols_paths(pb, rows, cols, ld, off, kind, inplace):
     mask = torch.ones_like(buf, dtype=torch.bool)
     mask[off:off + rows * ld].view(rows, ld)[:, :cols] = False
     assert torch.equal(buf[mask], before[mask])
+
+
+@pytest.mark.parametrize("inplace", [0, 1])
+@pytest.mark.parametrize("rows,cols,ld,off,moved", [(300, 1000, 1000, 0, 300), (2000, 777, 1031, 3, 40),
+                                                    (5000, 4096, 4100, 1, 1536), (5000, 300, 300, 0, 1537),
+                                                    (64, 33, 40, 2, 64), (4000, 20000, 20000, 0, 700)])
+def test_permute_rows_paths(pb, rows, cols, ld, off, moved, inplace):
+    """apply_rows through the C ABI (matrix.py:249-265 of the reference: X[i, :] <- X[g[i], :]),
+    one-pass strip gather for small moved sets vs the two-pass path through a temporary."""
+    import torch
+    from paper_1301_4438_b200 import _native
+
+    rng = np.random.default_rng(rows * 7 + cols)
+    g = np.arange(rows)
+    idx = np.sort(rng.choice(rows, moved, replace=False))
+    g[idx] = rng.permutation(idx)
+    buf = torch.randint(0, 65521, (rows * ld + off + 8,), dtype=torch.int32, device="cuda")
+    before = buf.clone()
+    view = buf[off:off + rows * ld].view(rows, ld)
+    want = view[:, :cols].cpu().numpy()[g]
+    ctx = _native.context()
+    old = ctx.get_option("gather_inplace")
+    ctx.set_option("gather_inplace", inplace)
+    try:
+        gp = (ctypes.c_int64 * rows)(*g.tolist())
+        st = ctx.lib.pluq_permute_rows(ctx.handle, buf.data_ptr() + 4 * off, ld, rows, cols, gp)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_option("gather_inplace", old)
+    assert st == 0
+    assert np.array_equal(view[:, :cols].cpu().numpy(), want)
+    mask = torch.ones_like(buf, dtype=torch.bool)
+    mask[off:off + rows * ld].view(rows, ld)[:, :cols] = False
+    assert torch.equal(buf[mask], before[mask])
