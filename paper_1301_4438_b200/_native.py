@@ -127,12 +127,12 @@ class Context:
         return int(out.value)
 
     def stats(self) -> dict:
-        buf = (ctypes.c_int64 * 18)()
-        self.lib.pluq_last_stats(self.handle, buf, 18)
+        buf = (ctypes.c_int64 * 19)()
+        self.lib.pluq_last_stats(self.handle, buf, 19)
         keys = ["launches", "host_syncs", "nodes", "small_node_kernels", "basecase_kernels",
                 "tc_gemms", "simt_gemms", "zero_skips", "generic_leaves", "speculative_ok",
                 "speculative_fail", "t_generic_ns", "t_fallback_ns", "t_tc_mma_ns",
-                "tc_timed_launches", "tc_timed_ns", "tc_timed_int8_ops", "spec_repairs"]
+                "tc_timed_launches", "tc_timed_ns", "tc_timed_int8_ops", "spec_repairs", "early_chunks"]
         return dict(zip(keys, list(buf)))
 
     def measure_peaks(self) -> dict:

@@ -159,6 +159,17 @@ struct pluq_ctx {
   unsigned long long* h_counts = nullptr;
   int* d_flag = nullptr;
   int* d_abort = nullptr;  // residue check of a batch, read back at the end of the call
+  // Early download (factor_host, option host_early): rows of the ROOT matrix that the speculative
+  // LU has finished are copied back and widened while the factorization is still running.
+  std::atomic<int64_t> early_rows{0};          // rows [0, early_rows) of the root are final on the device
+  std::atomic<bool> early_invalid{false};      // the final rows were modified again (failure / re-permutation)
+  bool early_on = false;                       // factor_host is listening
+  bool early_root = false;                     // the node being speculated on is the root matrix
+  int64_t early_row0 = 0;                      // global row of the current spec_core view
+  std::vector<std::pair<int, int>> early_patches;  // pivot repairs (g, cpos): columns [g, g + cpos] rotated in ALL rows
+  int* h_estop = nullptr;                      // pinned stop-flag snapshots, one per publication
+  int h_estop_n = 0, h_estop_cap = 0;
+  int64_t st_early_chunks = 0;                  // chunks downloaded before the factorization ended (last host call)
   int* h_flag = nullptr;
   int* d_stop = nullptr;     // [stop, k0, t] of the speculative no-pivot path
   int* h_stop = nullptr;
@@ -192,6 +203,7 @@ struct pluq_ctx {
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
   int64_t spec_backup = 2;        // speculative LU: 1 = backup copy of the node, 0 = un-factor in place on failure, 2 = backup below spec_unfactor_elems entries
   int64_t spec_unfactor_elems = 1ll << 28;
+  int64_t host_early = 1;         // host-buffer pipeline: download final rows while the speculative LU still runs
   int64_t la_adapt = 1;           // group look-ahead: SM split between far update and panels chosen per group
   int64_t la_side_solve = 0;      // group look-ahead: U rows of the far columns solved on the side stream
   int64_t la_prio = 0;            // speculative LU: critical path on a greatest-priority stream
@@ -355,6 +367,7 @@ struct pluq_ctx {
   }
 
   void reset_stats() {
+    st_early_chunks = 0;
     st_launch = st_sync = st_nodes = st_small = st_base = st_tc = st_simt = st_zero_skips = st_generic = st_spec_ok =
         st_spec_fail = st_repairs = 0;
     tc.acc_launches = 0;
@@ -1331,6 +1344,25 @@ struct Driver {
   // g = min(m, n) if there was none; otherwise g < min(m, n) with x holding exactly the
   // state after g pivots: [L11\U11, U12; L21, S], S = x[g:, g:] the Schur complement, whose
   // (0, 0) entry is 0.
+  // Early download: announce that rows [0, rows) of the root are final once the stream gets here,
+  // unless the stop flag was raised before (then the solves before this point were skipped).
+  struct EarlyPub { pluq_ctx* c; int slot; int64_t rows; };
+  static void CUDART_CB early_publish_cb(void* p) {
+    EarlyPub* e = static_cast<EarlyPub*>(p);
+    if (e->c->h_estop[e->slot] == 0) {
+      int64_t cur = e->c->early_rows.load();
+      while (cur < e->rows && !e->c->early_rows.compare_exchange_weak(cur, e->rows)) {}
+    }
+    delete e;
+  }
+  void early_publish(int64_t local_rows) {
+    if (!c->early_on || !c->early_root) return;
+    if (c->h_estop_n >= c->h_estop_cap) return;  // out of snapshot slots: just stop announcing
+    const int slot = c->h_estop_n++;
+    CU(cudaMemcpyAsync(c->h_estop + slot, c->d_stop, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaLaunchHostFunc(c->stream, early_publish_cb, new EarlyPub{c, slot, c->early_row0 + local_rows}));
+  }
+
   // la_prio: the whole critical path runs on a greatest-priority stream (the far updates on
   // default-priority side streams), so its short kernels are dispatched ahead of pending far
   // update CTAs whenever an SM frees up.
@@ -1695,6 +1727,7 @@ struct Driver {
           // the side stream right before the far update that consumes them (option la_side_solve)
           const bool ss = c->la_side_solve != 0;
           outer_cols(sops, pe, ss ? nn : n);
+          if (!ss) early_publish(pe);  // rows < pe: L part and U rows final
           sops.gemm(x.sub(pe, pe, m - pe, nn - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, nn - pe));
           CU(cudaMemcpyAsync(snap + pidx, c->d_stop, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
           CU(cudaEventRecord(ev_main, c->stream));
@@ -1746,6 +1779,7 @@ struct Driver {
           side_pending = true;
         } else {
           outer_cols(sops, pe, n);
+          early_publish(pe);
           sops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, gs2, m - pe, pe - gs2), x.sub(gs2, pe, pe - gs2, n - pe));
         }
         if (xg0) c->dfree(xg0);
@@ -1949,7 +1983,9 @@ struct Driver {
       check_residues(c, x, mp.p);
     }
     int g0 = 0, repairs = 0, res = 0;
+    c->early_root = c->early_on && depth == 0;
     for (;;) {
+      c->early_row0 = g0;
       const int g = g0 + spec_core(x.sub(g0, g0, m - g0, n - g0), (int64_t)m * n);
       g_state = std::min(g, mn);
       if (g >= mn) { rank = mn; res = 1; break; }
@@ -1958,6 +1994,7 @@ struct Driver {
       const int cpos = ops.first_nonzero_col(x.sub(g, g, 1, n - g));
       if (cpos <= 0) break;  // row g has no pivot (rows would move): exact recursion
       ++repairs;
+      if (c->early_root) c->early_patches.emplace_back(g, cpos);
       Perm rot(cpos + 1);
       rot[0] = cpos;
       for (int j = 1; j <= cpos; ++j) rot[j] = j - 1;
@@ -1980,6 +2017,7 @@ struct Driver {
         // one column inside a base case): R_A is still exact, so the packed output is the
         // unpivoted LU of A' = A[P^-1][:, Q], whose leading minors 1..r are nonzero (fact 2):
         // restore, permute, and factor A' without pivoting.
+        if (c->early_root) c->early_invalid.store(true);
         restore();
         ops.gather_rows(x, inverse(P));
         ops.gather_cols(x, Q);
@@ -1994,9 +2032,11 @@ struct Driver {
       ++c->st_spec_ok;
       c->st_repairs += repairs;
     } else {
+      if (c->early_root) c->early_invalid.store(true);
       restore();
       ++c->st_spec_fail;
     }
+    c->early_root = false;
     return res;
   }
 
@@ -2315,6 +2355,7 @@ int pluq_destroy(pluq_ctx* c) {
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_abort) cudaFree(c->d_abort);
   if (c->hi_stream_) cudaStreamDestroy(c->hi_stream_);
+  if (c->h_estop) cudaFreeHost(c->h_estop);
   if (c->d_invtab32) cudaFree(c->d_invtab32);
   if (c->d_invtab) cudaFree(c->d_invtab);
   if (c->d_zflags) cudaFree(c->d_zflags);
@@ -2356,7 +2397,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(host_early, c->host_early) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
@@ -2501,12 +2542,12 @@ int pluq_generic_counts(int64_t m, int64_t n, int64_t rank, int64_t threshold, i
 
 int pluq_last_stats(pluq_ctx* c, int64_t* out, int64_t nout) {
   if (!c || !out) return kInvalid;
-  int64_t v[18] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
+  int64_t v[19] = {c->st_launch, c->st_sync, c->st_nodes, c->st_small, c->st_base, c->st_tc, c->st_simt,
                    c->st_zero_skips, c->st_generic, c->st_spec_ok, c->st_spec_fail,
                    (int64_t)(c->t_generic_ms * 1e6f), (int64_t)(c->t_fallback_ms * 1e6f),
                    (int64_t)(c->tc.mma_ms * 1e6f), c->tc.acc_launches, (int64_t)(c->tc.acc_ms * 1e6),
-                   (int64_t)c->tc.acc_ops, c->st_repairs};
-  for (int64_t i = 0; i < nout && i < 18; ++i) out[i] = v[i];
+                   (int64_t)c->tc.acc_ops, c->st_repairs, c->st_early_chunks};
+  for (int64_t i = 0; i < nout && i < 19; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -2915,9 +2956,6 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       c->sync();
       throw PluqError(kInvalid, "matrix entries must be canonical residues in [0, p)");
     }
-    factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
-    CU(cudaEventRecord(je[0], c->stream));
-    CU(cudaStreamWaitEvent(sout, je[0], 0));
     auto issue = [&](int64_t k) {
       const int s = (int)(k % pluq_ctx::kRing);
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
@@ -2930,10 +2968,8 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       }
       CU(cudaEventRecord(ev[s], sout));
     };
-    for (int64_t k = 0; k < std::min<int64_t>(nch, pluq_ctx::kRing); ++k) issue(k);
-    for (int64_t k = 0; k < nch; ++k) {
+    auto widen = [&](int64_t k) {  // chunk k has arrived in its ring slot: widen it into the caller's buffer
       const int s = (int)(k % pluq_ctx::kRing);
-      CU(cudaEventSynchronize(ev[s]));
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
       const uint32_t* slot = reinterpret_cast<const uint32_t*>(ring + (size_t)s * chunk);
       const uint16_t* slot16 = reinterpret_cast<const uint16_t*>(ring + (size_t)s * chunk);
@@ -2945,7 +2981,98 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
         if (w16) host_from_u16(slot16 + a, is_f64, dst + (size_t)a * esz, b - a);
         else host_from_u32(slot + a, is_f64, dst + (size_t)a * esz, b - a);
       });
+    };
+    // Early download (option host_early): while the speculative LU of the root still runs, a
+    // second host thread copies back and widens every chunk whose rows it has announced final
+    // (Driver::early_publish); the caller's buffer was validated during the upload, so writing
+    // results into it early is safe.  Pivot repairs rotate a few columns in ALL rows: those
+    // columns are fetched again at the end; a failed speculation invalidates the early chunks.
+    int64_t kdone = 0;
+    std::thread dl;
+    std::atomic<bool> fin{false};
+    std::exception_ptr dl_err;
+    const bool early = c->host_early != 0 && nch > 2 * pluq_ctx::kRing;
+    if (early) {
+      c->early_rows.store(0);
+      c->early_invalid.store(false);
+      c->early_patches.clear();
+      const int want = 4096;
+      if (c->h_estop_cap < want) {
+        if (c->h_estop) CU(cudaFreeHost(c->h_estop));
+        CU(cudaHostAlloc((void**)&c->h_estop, want * sizeof(int), cudaHostAllocDefault));
+        c->h_estop_cap = want;
+      }
+      c->h_estop_n = 0;
+      c->early_on = true;
+      dl = std::thread([&] {
+        try {
+          CU(cudaSetDevice(c->device));
+          auto final_chunk = [&](int64_t k) {  // every row of chunk k announced final
+            if (k >= nch) return false;
+            const int64_t e_end = std::min<int64_t>((k + 1) * (int64_t)ce, cnt);
+            return (e_end - 1) / n < c->early_rows.load();
+          };
+          int64_t issued = 0;
+          while (!fin.load()) {
+            if (c->early_invalid.load()) break;
+            while (issued < kdone + pluq_ctx::kRing - 1 && final_chunk(issued)) issue(issued++);
+            if (kdone < issued) {
+              CU(cudaEventSynchronize(ev[kdone % pluq_ctx::kRing]));
+              widen(kdone);
+              ++kdone;
+            } else {
+              std::this_thread::sleep_for(std::chrono::microseconds(200));
+            }
+          }
+          for (; kdone < issued; ++kdone) {  // drain what was issued
+            CU(cudaEventSynchronize(ev[kdone % pluq_ctx::kRing]));
+            widen(kdone);
+          }
+        } catch (...) {
+          dl_err = std::current_exception();
+        }
+      });
+    }
+    try {
+      factor_device(c, dA, n, m, n, p, threshold, psig, qsig, rank, counts, false);
+    } catch (...) {
+      fin.store(true);
+      if (dl.joinable()) dl.join();
+      c->early_on = false;
+      throw;
+    }
+    fin.store(true);
+    if (dl.joinable()) dl.join();
+    c->early_on = false;
+    if (dl_err) std::rethrow_exception(dl_err);
+    if (early && c->early_invalid.load()) kdone = 0;
+    c->st_early_chunks = kdone;
+    CU(cudaEventRecord(je[0], c->stream));
+    CU(cudaStreamWaitEvent(sout, je[0], 0));
+    const int64_t k_first = kdone;
+    for (int64_t k = k_first; k < std::min<int64_t>(nch, k_first + pluq_ctx::kRing); ++k) issue(k);
+    for (int64_t k = k_first; k < nch; ++k) {
+      CU(cudaEventSynchronize(ev[k % pluq_ctx::kRing]));
+      widen(k);
       if (k + pluq_ctx::kRing < nch) issue(k + pluq_ctx::kRing);
+    }
+    if (early && k_first > 0) {
+      // columns rotated by pivot repairs after some of their rows had been downloaded
+      const int64_t rows_early = std::min<int64_t>(m, (k_first * (int64_t)ce + n - 1) / n);
+      for (const auto& pr : c->early_patches) {
+        const int64_t pr_rows = std::min<int64_t>(pr.first, rows_early), c0 = pr.first, w = pr.second + 1;
+        if (pr_rows <= 0) continue;
+        std::vector<uint32_t> tmp((size_t)pr_rows * w);
+        CU(cudaMemcpy2DAsync(tmp.data(), (size_t)w * 4, dA + c0, (size_t)n * 4, (size_t)w * 4, (size_t)pr_rows,
+                             cudaMemcpyDeviceToHost, sout));
+        CU(cudaStreamSynchronize(sout));
+        for (int64_t i = 0; i < pr_rows; ++i)
+          for (int64_t j = 0; j < w; ++j) {
+            const size_t e = (size_t)i * n + c0 + j;
+            if (is_f64) static_cast<double*>(hA)[e] = (double)tmp[(size_t)i * w + j];
+            else static_cast<int64_t*>(hA)[e] = (int64_t)tmp[(size_t)i * w + j];
+          }
+      }
     }
     CU(cudaEventRecord(je[1], sout));
     CU(cudaStreamWaitEvent(c->stream, je[1], 0));

@@ -347,3 +347,59 @@ def test_permute_rows_paths(pb, rows, cols, ld, off, moved, inplace):
     mask = torch.ones_like(buf, dtype=torch.bool)
     mask[off:off + rows * ld].view(rows, ld)[:, :cols] = False
     assert torch.equal(buf[mask], before[mask])
+
+
+@pytest.mark.parametrize("early", [0, 1])
+@pytest.mark.parametrize("kind", ["generic", "rank", "repair", "two_repairs", "fails", "i64"])
+def test_host_early_download_vs_oracle(pb, kind, early):
+    """Host-buffer pipeline with the early download (option host_early): rows the speculative LU
+    announces final are copied back while it still runs (group look-ahead forced on 256-wide
+    panels, 1 MiB chunks).  Pivot repairs rotate columns of rows already downloaded (patched
+    at the end); a failed speculation invalidates the early chunks.  Bit-exact vs the oracle."""
+    from paper_1301_4438_b200 import _native
+
+    p = 8388593 if kind == "i64" else 65521
+    dtype = np.int64 if kind == "i64" else np.float64
+    m, n = 2600, 2500
+    rng = np.random.default_rng(17)
+    if kind in ("rank",):
+        a0 = np.asarray(orc.gen_xy_rank(m, n, 1800, p, 5), np.int64)
+    else:
+        a0 = np.asarray(rng.integers(0, p, (m, n)), np.int64)
+
+    def vanish(g, w):
+        coef = rng.integers(0, p, g).astype(object)
+        a0[g, :g + w] = np.array((coef @ a0[:g, :g + w].astype(object)) % p, dtype=np.int64)
+
+    if kind == "repair":
+        vanish(1300, 1)
+    if kind == "two_repairs":
+        vanish(700, 1); vanish(1900, 2)
+    if kind == "fails":  # a row without a pivot deep inside: the speculation fails after many rows were sent
+        coef = rng.integers(0, p, 1500).astype(object)
+        a0[1500, :] = np.array((coef @ a0[:1500, :].astype(object)) % p, dtype=np.int64)
+    x = a0.astype(orc.field_dtype(p))
+    cc = orc.Counts()
+    P, Q, r, _ = orc.pluq(x, p, 30, cc)
+    ctx = _native.context()
+    opts = dict(host_chunk_mb=1, host_early=early, small_cap=1, spec_panel=256, la_pair=2, panel_rec=2)
+    old = {k: ctx.get_option(k) for k in opts}
+    for k, v in opts.items():
+        ctx.set_option(k, v)
+    try:
+        a = pb.DenseMatrix(pb.PrimeField(p), a0.astype(dtype))
+        c = pb.OpCounts()
+        f = pb.pluq(a, counts=c)
+        st = ctx.stats()
+    finally:
+        for k, v in old.items():
+            ctx.set_option(k, v)
+    assert f.rank == r and np.array_equal(f.p_perm.sigma, P) and np.array_equal(f.q_perm.sigma, Q)
+    assert np.array_equal(a.data, x)
+    assert (c.field_mul, c.field_add, c.field_inv, c.modular_reductions) == cc.as_tuple()
+    if not early or kind == "fails":
+        assert st["early_chunks"] == 0
+    elif kind != "two_repairs":  # chunks did leave while the factorization was still running
+        # (two_repairs: the two-column repair makes Alg. 1 order the pivots differently, the node
+        # is re-permuted and factored again, which invalidates the early chunks)
+        assert st["early_chunks"] > 0, st
