@@ -150,7 +150,8 @@ int pluq_measure_peaks(pluq_ctx* ctx, double* out, int64_t nout);
  * generic- and fallback-kernel ns of a batch (option time_kernels), the MMA-kernel ns of
  * the last tensor-core GEMM (option tc_time), and — option tc_time, summed over the call —
  * MMA-kernel launches, their CUDA-event ns and their algorithmic int8 ops (2 m n k L^2), and
- * the zero pivots the speculative LU repaired by a column rotation. */
+ * the zero pivots the speculative LU repaired by a column rotation, and the chunks of the
+ * last host-buffer call that were downloaded while its factorization was still running. */
 int pluq_last_stats(pluq_ctx* ctx, int64_t* out, int64_t nout);
 
 #ifdef __cplusplus
