@@ -601,7 +601,8 @@ def bench_single(pb, name, args, dev, world, rank):
                        "host_buffer_bytes": nbytes,
                        "path": "pluq(DenseMatrix(PrimeField(p), float64 numpy)) -> C ABI pluq_factor_host_f64: host "
                                "threads convert the float64 buffer to a uint16 wire (p <= 2^16) in pinned chunks, "
-                               "widened on the device; the reverse on the way back",
+                               "widened on the device; the reverse on the way back, rows the LU has finished leaving while it "
+                               "still runs (host_early)",
                        "steps": len(ts), "ms_per_step": 1e3 * sorted(ts)[len(ts) // 2],
                        "mean_ms": 1e3 * sum(ts) / len(ts), "value_at": "median step",
                        "step_ms": [round(1e3 * v, 2) for v in ts]}

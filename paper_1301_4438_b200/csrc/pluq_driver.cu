@@ -169,6 +169,7 @@ struct pluq_ctx {
   std::vector<std::pair<int, int>> early_patches;  // pivot repairs (g, cpos): columns [g, g + cpos] rotated in ALL rows
   int* h_estop = nullptr;                      // pinned stop-flag snapshots, one per publication
   int h_estop_n = 0, h_estop_cap = 0;
+  bool attr_cols_set = false, attr_rows_set = false;  // shared-memory attributes of the in-place gathers
   int64_t st_early_chunks = 0;                  // chunks downloaded before the factorization ended (last host call)
   int* h_flag = nullptr;
   int* d_stop = nullptr;     // [stop, k0, t] of the speculative no-pivot path
@@ -744,10 +745,9 @@ struct Ops {
     CU(cudaMemcpyAsync(d_idx, h, both.size() * 4, cudaMemcpyHostToDevice, c->stream));
     if (c->gather_inplace && nmv <= 1536) {  // small moved set: one in-place pass by column strips
       const size_t sm = (size_t)nmv * 32 * sizeof(uint32_t);
-      static bool attr_set = false;
-      if (sm > 48 * 1024 && !attr_set) {
+      if (sm > 48 * 1024 && !c->attr_rows_set) {
         CU(cudaFuncSetAttribute(rows_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1536 * 32 * 4));
-        attr_set = true;
+        c->attr_rows_set = true;
       }
       const int strips = (x.n + 31) / 32;
       rows_inplace_kernel<<<std::min(strips, c->tc.num_sms() * 8), 256, sm, c->stream>>>(x, d_idx, d_idx + nmv, nmv);
@@ -783,10 +783,9 @@ struct Ops {
     if (c->gather_inplace && (int64_t)nmv * 8 >= span && pitch * 4 <= (size_t)220 * 1024) {
       const int nbuf = 2 * pitch * 4 <= (size_t)220 * 1024 ? 2 : 1;
       const size_t sm = nbuf * pitch * 4;
-      static size_t sm_set = 0;
-      if (sm > sm_set) {
+      if (!c->attr_cols_set) {  // per context (= per device), not per process
         CU(cudaFuncSetAttribute(cols_inplace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        sm_set = (size_t)220 * 1024;
+        c->attr_cols_set = true;
       }
       const int threads = span >= 8192 ? 1024 : span >= 2048 ? 512 : 256;
       const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2048 / threads, (size_t)220 * 1024 / (sm + 1024)));
