@@ -167,6 +167,36 @@ def test_cfg5_family_rank_inside_big_panel(pb):
     _assert_same(f, c, t, _oracle(a0, p))
 
 
+@pytest.mark.parametrize("rank,coincidence", [(None, 5000), (6000, None)], ids=["full_rank_repair", "rank6000"])
+def test_wide_panel_group_lookahead_bit_exact(pb, rank, coincidence):
+    """8192^2 through the scheduling cfg5 uses at its production panel width: four 2048-wide
+    panels (first panel alone, then a group of two with the K = 4096 far update split in two
+    parts, SM split chosen per group, recursive panels with the accumulated inverse), with a
+    coincidental zero minor repaired in the group's panel / a zero Schur complement inside the
+    group's second panel — bit for bit against the oracle (P, Q, rank, packed, OpCounts)."""
+    import torch
+
+    p, n = 65521, 8192
+    if rank is None:
+        rng = np.random.default_rng(123)
+        a0 = np.asarray(rng.integers(0, p, (n, n)), np.int64)
+        g = coincidence  # leading minor g + 1 vanishes: row g (columns <= g) = combination of the rows above
+        coef = rng.integers(0, p, g)
+        acc = np.zeros(g + 1, dtype=np.int64)
+        for k0 in range(0, g, 512):  # exact: 512 products below 2^32 each
+            k1 = min(k0 + 512, g)
+            acc = (acc + coef[k0:k1] @ a0[k0:k1, :g + 1]) % p
+        a0[g, :g + 1] = acc
+    else:
+        a0 = np.asarray(orc.gen_xy_rank(n, n, rank, p, 4), np.int64)
+    t = torch.from_numpy(a0).cuda().to(torch.int32)
+    f, c, st = _factor_device(pb, t, p, spec_big_elems=1 << 20, spec_panel_big=2048)
+    assert st["speculative_ok"] >= 1 and st["speculative_fail"] == 0
+    if rank is None:
+        assert st["spec_repairs"] >= 1  # the planted one (a random 8192^2 input may bring its own)
+    _assert_same(f, c, t, _oracle(a0, p))
+
+
 def test_full_size_cfg4_cfg5_invariants(pb):
     """cfg4 and cfg5 at their BASELINE sizes on the §8(d) seed-0 inputs: rank, packed
     structure, Freivalds reconstruction, and cfg4's prescribed profiles (I, J)."""
