@@ -217,3 +217,28 @@ def test_full_size_cfg4_cfg5_invariants(pb):
     assert verify.structure_ok(f) and verify.freivalds(a5, f, probes=2)
     del a5, f
     torch.cuda.empty_cache()
+
+
+def test_cfg5_full_size_host_buffers_equal_device_result(pb):
+    """cfg5 at its BASELINE size through HOST float64 buffers (pipelined upload, early download of
+    finished rows while the LU still runs, the seed-0 repair's rotated columns re-fetched) gives
+    exactly the packed matrix, P, Q and rank of the device-resident run."""
+    import torch
+    from paper_1301_4438_b200 import _native, gen
+
+    p = 65521
+    a5 = gen.gen_cfg5_device(seed=0)
+    host = np.empty(a5.shape, dtype=np.float64)
+    for r0 in range(0, a5.shape[0], 4096):  # chunked: no 32 GiB temporary
+        host[r0:r0 + 4096] = a5[r0:r0 + 4096].cpu().numpy()
+    fd = pb.pluq(pb.DenseMatrix(pb.PrimeField(p), a5))  # in place on the device
+    dm = pb.DenseMatrix(pb.PrimeField(p), host)
+    fh = pb.pluq(dm)
+    st = _native.context().stats()
+    assert fh.rank == fd.rank == 32768
+    assert np.array_equal(fh.p_perm.sigma, fd.p_perm.sigma) and np.array_equal(fh.q_perm.sigma, fd.q_perm.sigma)
+    assert st["early_chunks"] > 0, st  # rows did leave while the factorization was running
+    for r0 in range(0, a5.shape[0], 4096):
+        assert np.array_equal(host[r0:r0 + 4096], a5[r0:r0 + 4096].cpu().numpy()), r0
+    del a5, fd, fh, dm, host
+    torch.cuda.empty_cache()
