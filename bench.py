@@ -59,12 +59,12 @@ GRIDS = {1: None, 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 
 # dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the dominant kernel at
 # cfg5's first merged trailing update (61440 x 59392 x 4096) from the committed ncu --set full
-# capture profiles/r2/prof_gemm4096_v3_raw.txt: 44.44 GB read + 14.61 GB write, against
+# capture profiles/r2/prof_gemm4096_v4_raw.txt (final kernel): 44.49 GB read + 14.79 GB write, against
 # 30.2 GB algorithmic (C read + write 29.2 GB, limb planes 1.0 GB): the B limb panel is
 # re-read once per 8-tile-row rasterisation group
-TRAFFIC = 59_053_396_000
+TRAFFIC = 59_278_041_000
 TRAFFIC_SHAPE = {"m": 61440, "n": 59392, "k": 4096, "algorithmic_bytes": 30_178_000_000,
-                 "capture": "profiles/r2/prof_gemm4096_v3_raw.txt"}
+                 "capture": "profiles/r2/prof_gemm4096_v4_raw.txt"}
 
 
 def work(m, n, r):
