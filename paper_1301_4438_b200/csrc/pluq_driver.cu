@@ -2960,7 +2960,10 @@ static int factor_host(pluq_ctx* c, void* hA, bool is_f64, int64_t m, int64_t n,
       const int64_t e0 = k * (int64_t)ce, ne = std::min<int64_t>((int64_t)ce, cnt - e0);
       if (w16) {
         narrow16_kernel<<<wgrid(ne), 256, 0, sout>>>(dA + e0, dstage + (size_t)s * ce, ne);
-        c->check_launch();
+        {  // not c->check_launch(): this lambda also runs on the early-download thread (no shared counters)
+          const cudaError_t le = cudaGetLastError();
+          if (le != cudaSuccess) throw PluqError(kCuda, std::string("kernel launch: ") + cudaGetErrorString(le));
+        }
         CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dstage + (size_t)s * ce, (size_t)ne * 2, cudaMemcpyDeviceToHost, sout));
       } else {
         CU(cudaMemcpyAsync(ring + (size_t)s * chunk, dA + e0, (size_t)ne * 4, cudaMemcpyDeviceToHost, sout));
