@@ -1983,12 +1983,26 @@ struct Driver {
     }
     int g0 = 0, repairs = 0, res = 0;
     c->early_root = c->early_on && depth == 0;
+    // option trace_pipeline: host-clock phase times of this function (device synchronised at each mark)
+    const bool ptrace = c->trace_pipeline != 0;
+    auto tp0 = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+      if (!ptrace) return;
+      CU(cudaDeviceSynchronize());
+      const auto t1 = std::chrono::steady_clock::now();
+      fprintf(stderr, "spec_lu %dx%d: %-22s %8.3f ms\n", m, n, what, std::chrono::duration<double, std::milli>(t1 - tp0).count());
+      tp0 = t1;
+    };
+    phase("backup / range check");
     for (;;) {
       c->early_row0 = g0;
       const int g = g0 + spec_core(x.sub(g0, g0, m - g0, n - g0), (int64_t)m * n);
+      phase("spec_core + finishing");
       g_state = std::min(g, mn);
       if (g >= mn) { rank = mn; res = 1; break; }
-      if (!ops.nonzero(x.sub(g, g, m - g, n - g))) { rank = g; res = 1; break; }
+      const bool nzs = ops.nonzero(x.sub(g, g, m - g, n - g));
+      phase("zero test of S");
+      if (!nzs) { rank = g; res = 1; break; }
       if (repairs >= c->spec_repairs) break;
       const int cpos = ops.first_nonzero_col(x.sub(g, g, 1, n - g));
       if (cpos <= 0) break;  // row g has no pivot (rows would move): exact recursion
@@ -1999,6 +2013,7 @@ struct Driver {
       for (int j = 1; j <= cpos; ++j) rot[j] = j - 1;
       ops.gather_cols(x.sub(0, g, m, cpos + 1), rot);
       std::rotate(sig.begin() + g, sig.begin() + g + cpos, sig.begin() + g + cpos + 1);
+      phase("repair (rotate column)");
       g0 = g;
     }
     if (res == 1 && repairs > 0) {
@@ -2007,6 +2022,7 @@ struct Driver {
       Perm P, Q;
       Counts sc{0, 0, 0, 0};
       symbolic_replay(m, n, threshold, prow, pcol, P, Q, sc);
+      phase("symbolic replay (host)");
       res = 2;
       cnt = sc;
       if (is_ident(P) && Q == sig) {
