@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -204,6 +205,7 @@ struct pluq_ctx {
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
   int64_t spec_backup = 2;        // speculative LU: 1 = backup copy of the node, 0 = un-factor in place on failure, 2 = backup below spec_unfactor_elems entries
   int64_t spec_unfactor_elems = 1ll << 28;
+  int64_t replay_async = 1;       // pivot repair: Alg. 1 replayed on a host thread under the last stop's GPU work
   int64_t host_early = 1;         // host-buffer pipeline: download final rows while the speculative LU still runs
   int64_t la_adapt = 1;           // group look-ahead: SM split between far update and panels chosen per group
   int64_t la_side_solve = 0;      // group look-ahead: U rows of the far columns solved on the side stream
@@ -1994,15 +1996,33 @@ struct Driver {
       tp0 = t1;
     };
     phase("backup / range check");
+    struct ReplayOut { Perm P, Q; Counts sc{0, 0, 0, 0}; int rank = -1; };
+    ReplayOut pre;  // replay finished under the last stop's GPU work
     for (;;) {
       c->early_row0 = g0;
       const int g = g0 + spec_core(x.sub(g0, g0, m - g0, n - g0), (int64_t)m * n);
       phase("spec_core + finishing");
+      // The host is about to wait ~15-20 ms for the finishing GEMMs and the zero test of S: if this
+      // stop ends the factorization (S = 0 or g = min(m, n)) the rank is g, so Alg. 1 is replayed on
+      // R_A = {(k, sig[k]), k < g} on a host thread meanwhile (6 ms at cfg5); discarded otherwise.
+      std::future<ReplayOut> fut;
+      if (repairs > 0 && c->replay_async) {
+        const int rg = std::min(g, mn), thr = threshold;
+        Perm sig_copy = sig;
+        fut = std::async(std::launch::async, [rg, m, n, thr, sig_copy]() {
+          ReplayOut r;
+          std::vector<int> prow(rg), pcol(rg);
+          for (int k = 0; k < rg; ++k) { prow[k] = k; pcol[k] = sig_copy[k]; }
+          symbolic_replay(m, n, thr, prow, pcol, r.P, r.Q, r.sc);
+          r.rank = rg;
+          return r;
+        });
+      }
       g_state = std::min(g, mn);
-      if (g >= mn) { rank = mn; res = 1; break; }
+      if (g >= mn) { rank = mn; res = 1; if (fut.valid()) pre = fut.get(); break; }
       const bool nzs = ops.nonzero(x.sub(g, g, m - g, n - g));
       phase("zero test of S");
-      if (!nzs) { rank = g; res = 1; break; }
+      if (!nzs) { rank = g; res = 1; if (fut.valid()) pre = fut.get(); break; }
       if (repairs >= c->spec_repairs) break;
       const int cpos = ops.first_nonzero_col(x.sub(g, g, 1, n - g));
       if (cpos <= 0) break;  // row g has no pivot (rows would move): exact recursion
@@ -2021,7 +2041,13 @@ struct Driver {
       for (int k = 0; k < rank; ++k) { prow[k] = k; pcol[k] = sig[k]; }
       Perm P, Q;
       Counts sc{0, 0, 0, 0};
-      symbolic_replay(m, n, threshold, prow, pcol, P, Q, sc);
+      if (pre.rank == rank) {
+        P.swap(pre.P);
+        Q.swap(pre.Q);
+        sc = pre.sc;
+      } else {
+        symbolic_replay(m, n, threshold, prow, pcol, P, Q, sc);
+      }
       phase("symbolic replay (host)");
       res = 2;
       cnt = sc;
@@ -2412,7 +2438,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(host_early, c->host_early) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(host_early, c->host_early) X(replay_async, c->replay_async) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
