@@ -205,6 +205,7 @@ struct pluq_ctx {
   int64_t la_cap = 0;              // ... this stream's tensor-core GEMMs meanwhile: 0 persistent, 1 la_reserve CTAs, 2 one CTA per tile
   int64_t spec_backup = 2;        // speculative LU: 1 = backup copy of the node, 0 = un-factor in place on failure, 2 = backup below spec_unfactor_elems entries
   int64_t spec_unfactor_elems = 1ll << 28;
+  int64_t fin_merge = 1;          // group look-ahead: merged K = W + (g - ps) finishing update after a stop
   int64_t replay_async = 1;       // pivot repair: Alg. 1 replayed on a host thread under the last stop's GPU work
   int64_t host_early = 1;         // host-buffer pipeline: download final rows while the speculative LU still runs
   int64_t la_adapt = 1;           // group look-ahead: SM split between far update and panels chosen per group
@@ -1885,12 +1886,17 @@ struct Driver {
         // below this panel (its own rows already have it), columns right of this panel
         ops.gemm(x.sub(pe, pe, m - pe, n - pe), x.sub(pe, ps - W, m - pe, W), x.sub(ps - W, pe, W, n - pe));
       }
+      // (fin_merge: when pivots [ps, g) of this panel follow, the rows below g take the first
+      // panel's K = W update and this panel's K = g - ps update as ONE GEMM with K = W + g - ps:
+      // one pass over the (m - g) x (n - pe) block instead of two)
+      const bool fin_merge = c->fin_merge && ps >= W && grouped[ps / W - 1] && pe < n && g > ps;
       if (ps >= W && grouped[ps / W - 1] && pe < n) {
         // group look-ahead, stop in the group's second panel: the first panel's U rows and
         // its contribution to every row below it, right of this panel, are still pending
         const View l0 = x.sub(ps - W, ps - W, W, W);
         ops.trsm_l(l0, x.sub(ps - W, pe, W, n - pe));
-        ops.gemm(x.sub(ps, pe, m - ps, n - pe), x.sub(ps, ps - W, m - ps, W), x.sub(ps - W, pe, W, n - pe));
+        const int rows1 = fin_merge ? g - ps : m - ps;  // merged: only this panel's pivot rows now
+        ops.gemm(x.sub(ps, pe, rows1, n - pe), x.sub(ps, ps - W, rows1, W), x.sub(ps - W, pe, W, n - pe));
       }
       if (t > 0 && prec_on) {
         // recursive panel: the block's own columns only; the panel columns right of it follow
@@ -1924,7 +1930,10 @@ struct Driver {
       }
       if (g > ps) {
         ops.trsm_l(x.sub(ps, ps, g - ps, g - ps), x.sub(ps, pe, g - ps, n - pe));
-        ops.gemm(x.sub(g, pe, m - g, n - pe), x.sub(g, ps, m - g, g - ps), x.sub(ps, pe, g - ps, n - pe));
+        if (fin_merge)  // L columns [ps - W, g) against U rows [ps - W, g): both contiguous
+          ops.gemm(x.sub(g, pe, m - g, n - pe), x.sub(g, ps - W, m - g, W + g - ps), x.sub(ps - W, pe, W + g - ps, n - pe));
+        else
+          ops.gemm(x.sub(g, pe, m - g, n - pe), x.sub(g, ps, m - g, g - ps), x.sub(ps, pe, g - ps, n - pe));
       }
       return g;
     }
@@ -2438,7 +2447,7 @@ int pluq_set_stream(pluq_ctx* c, void* stream) {
   X(try_generic, c->try_generic) X(time_kernels, c->time_kernels) X(fixed_kernels, c->fixed_kernels) X(batch_dp, c->batch_dp) X(inv32, c->inv32) \
   X(host_chunks, c->host_chunks) X(chunk_shape, c->chunk_shape) X(diag_lazy, c->diag_lazy)          \
   X(lookahead, c->lookahead) X(la_reserve, c->la_reserve) X(exact_kernel, c->exact_kernel)          \
-  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(host_early, c->host_early) X(replay_async, c->replay_async) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
+  X(la_pair, c->la_pair) X(la_cap, c->la_cap) X(inner_la, c->inner_la) X(gather_inplace, c->gather_inplace) X(panel_rec, c->panel_rec) X(la_pair_big, c->la_pair_big) X(la_preinv, c->la_preinv) X(la_first_single, c->la_first_single) X(panel_inv, c->panel_inv) X(la_prio, c->la_prio) X(la_side_solve, c->la_side_solve) X(la_adapt, c->la_adapt) X(host_early, c->host_early) X(replay_async, c->replay_async) X(fin_merge, c->fin_merge) X(spec_backup, c->spec_backup) X(spec_unfactor_elems, c->spec_unfactor_elems) X(la_free, c->la_free) X(la_reserve_big, c->la_reserve_big)                             \
   X(rpm_threads, c->rpm_threads) X(rpm_lazy, c->rpm_lazy) X(par_trsm, c->par_trsm)                  \
   X(sym_par, c->sym_par) X(tc_trsm, c->tc_trsm) X(pair_leaves, c->pair_leaves)                      \
   X(stream_fb, c->stream_fb) X(stream_fb_spin, c->stream_fb_spin) X(fb_prefix, c->fb_prefix)        \
